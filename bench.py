@@ -1,0 +1,507 @@
+#!/usr/bin/env python
+"""Benchmark: one Gauss-Newton / LM iteration of photometric BA at the
+finest pyramid level (solve + pose update + linearise + assemble), the
+metric of BASELINE.json ("GN iteration time (ms) and pixel-pair
+residuals/sec at 1/2/4/8 B200; % HBM roofline").
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4|c2|c1]
+                  [--impl ours|reference]
+
+value    = pixel-pair residuals per second of GN iteration, whole job
+           (sum over pairs of depth-valid source pixels / iteration time),
+           inputs resident in HBM.
+e2e      = the same metric through the host-facing level session: every
+           step copies the poses in from pinned host memory and reads the
+           updated poses + cost back.
+roofline = the linearisation kernel's algorithmic bytes (80 B per
+           pixel-pair) / its CUDA-event time vs the measured
+           HBM copy bandwidth of MEASURED_PEAKS.json.
+cpu_baseline / --impl reference = the oracle C port of the reference path
+           (oracle/, a test-infrastructure restatement of
+           pkg/src/photoba/solver.py) on the host cores, on a bounded sample
+           of pairs, extrapolated by pixel count, plus the full dense
+           np.linalg.solve the reference performs.
+Multi-GPU (torchrun): pairs are sharded, records gathered to rank 0,
+poses broadcast; time = max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+BYTES_PER_PIXEL_PAIR = 80  # 5 fp64 cue values source + destination
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+# ---------------------------------------------------------------------------
+# workloads
+# ---------------------------------------------------------------------------
+CONFIGS = {
+    "c1": dict(desc="synthetic RGB-D pinhole 10 frames 160x120, 1 level", kind="room", n=10,
+               factors=(1,), max_translation=1.0),
+    "c2": dict(desc="synthetic LiDAR spherical 64x1024 (HDL-64), 100 scans, 3 levels",
+               kind="hdl64", n=100, spacing=0.1, factors=(4, 2, 1), max_translation=1.0),
+    "c4": dict(desc="synthetic OS0-128 128x1024, 1000 scans, 2 km corridor, 3 levels, ~20k pairs",
+               kind="os0", n=1000, spacing=2.0, factors=(4, 2, 1), max_translation=40.0),
+}
+
+
+def build_problem(name: str, device, n_override=None):
+    import torch
+
+    import paper_2303_16878_b200 as P
+    from paper_2303_16878_b200 import scenes as S
+
+    c = CONFIGS[name]
+    n = n_override or c["n"]
+    if c["kind"] == "room":
+        cam, scene = S.rgbd_160(), S.BoxScene()
+        gt = S.room_loop(n)
+        ext = P.Pose.identity()
+    elif c["kind"] == "hdl64":
+        cam = S.hdl64()
+        gt = S.corridor_trajectory(n, c["spacing"])
+        scene = S.corridor_scene(c["spacing"] * n + 20.0)
+        ext = P.Pose.identity()
+    else:
+        cam = S.lidar_os0_128()
+        gt = S.corridor_trajectory(n, c["spacing"])
+        scene = S.corridor_scene(c["spacing"] * n + 20.0)
+        ext = P.Pose(np.eye(3), [0.0, 0.0, -0.05])
+    guess = S.perturb(gt, 0.05, math.radians(2.0), 11)
+    pyrs = S.device_pyramids(scene, cam, gt, ext, c["factors"], device)
+    nodes = [P.FrameNode(k, guess[k], pyrs[k], 0.1 * k) for k in range(n)]
+    crit = P.MatchCriteria(max_translation=c["max_translation"])
+    sensor_ext = P.SensorExtrinsics(ext)
+    t0 = time.perf_counter()
+    graph = P.build_graph(nodes, crit, extrinsics=sensor_ext, threads=8)
+    t_graph = time.perf_counter() - t0
+    prob = P.BAProblem(graph, {"sensor0": sensor_ext})
+    return prob, guess, gt, dict(name=name, desc=c["desc"], frames=n, cam=cam,
+                                 level=len(c["factors"]) - 1, graph_seconds=t_graph)
+
+
+def valid_pixel_pairs(prob, level) -> int:
+    """sum over pairs of depth-valid source pixels (solver.py:200-205)."""
+    import torch
+
+    counts = {}
+    total = 0
+    nodes = {n.id: n for n in prob.graph.nodes}
+    for e in prob.graph.edges:
+        cue = nodes[e.i].pyramid.levels[level]
+        key = id(cue)
+        if key not in counts:
+            d = getattr(cue, "device_depth", None)
+            cam = cue.intrinsics
+            if d is not None:
+                counts[key] = int(((d >= cam.depth_min) & (d <= cam.depth_max) & (d > 0)).sum())
+            else:
+                counts[key] = int(np.asarray(cue.depth_valid).sum())
+        total += counts[key]
+    return total
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (B200_PROFILING.md recipe)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak_hbm():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+        except Exception:
+            pass
+    return FALLBACK_HBM_GBS, "fallback"
+
+
+def ncu_traffic(name):
+    """dram bytes per pixel-pair of the linearisation kernel from the committed
+    ncu --set full summary (profiles/), scaled to this launch; None if absent."""
+    p = ROOT / "profiles" / "linearize_traffic.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())
+        return d
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle port on a bounded sample
+# ---------------------------------------------------------------------------
+def cpu_baseline(prob, guess, level, total_pp, target_seconds=12.0, threads=None):
+    import copy
+
+    import paper_2303_16878_b200 as P
+    from oracle import oracle as O
+
+    threads = threads or os.cpu_count() or 1
+    cfg = P.SolverConfig()
+    rows, _ = P.se3.pose_rows(guess)
+
+    def sub_problem(k):
+        g = P.MatchGraph(prob.graph.nodes, prob.graph.edges[:k])
+        return P.BAProblem(g, prob.extrinsics, prob.gauge_index)
+
+    # calibrate on a few pairs, then size the sample to ~target_seconds
+    k = min(4, len(prob.graph.edges))
+    lp = O.OracleLevel([sub_problem(k)], level, cfg)
+    t0 = time.perf_counter()
+    lp.records(rows, True, threads)
+    dt = max(time.perf_counter() - t0, 1e-6)
+    per_pair = dt / k * min(k, threads) / threads if k < threads else dt / k
+    k2 = int(max(k, min(len(prob.graph.edges), target_seconds / max(per_pair, 1e-6))))
+    k2 = max(threads, min(k2, len(prob.graph.edges)))
+    lp = O.OracleLevel([sub_problem(k2)], level, cfg)
+    sample_pp = valid_pixel_pairs(sub_problem(k2), level)
+    t0 = time.perf_counter()
+    lp.records(rows, True, threads)
+    t_lin = time.perf_counter() - t0
+    # dense LU of the reference (np.linalg.solve on dim 6(N-1)), timed in full
+    n = len(prob.graph.nodes)
+    dim = 6 * (n - 1)
+    rng = np.random.default_rng(0)
+    A = rng.normal(size=(dim, 64))
+    H = A @ A.T + np.eye(dim)
+    b = rng.normal(size=dim)
+    t0 = time.perf_counter()
+    np.linalg.solve(H + 1e-3 * np.diag(np.diag(H)), -b)
+    t_solve = time.perf_counter() - t0
+    gens = np.zeros(n, np.int64)
+    t0 = time.perf_counter()
+    lp.apply_step(rows, gens, np.zeros(dim))
+    t_upd = time.perf_counter() - t0
+    t_iter = t_lin * (total_pp / max(sample_pp, 1)) + t_solve + t_upd
+    return {
+        "value": total_pp / t_iter,
+        "unit": "pixel-pairs/s",
+        "cores": threads,
+        "kind": "port",
+        "sample": (f"oracle C port (OpenMP {threads} threads) linearising the first {k2} of "
+                   f"{len(prob.graph.edges)} pairs ({sample_pp} pixel-pairs, {t_lin:.2f} s), "
+                   f"extrapolated by pixel count to {total_pp}; + full np.linalg.solve dim {dim} "
+                   f"({t_solve:.2f} s) + apply_step ({t_upd * 1e3:.1f} ms)"),
+        "gn_iteration_ms_extrapolated": t_iter * 1e3,
+    }
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2303_16878_b200 as P
+    from paper_2303_16878_b200 import distributed as D
+    from paper_2303_16878_b200 import native
+    from paper_2303_16878_b200.device import DeviceLevel, FrameStore
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    lib = native.load()
+
+    t_setup = time.perf_counter()
+    prob, guess, gt, meta = build_problem(args.config, device, args.frames)
+    level = meta["level"]
+    cfg = P.SolverConfig()
+    store = FrameStore(device)
+    group = D.current_group()
+    backend = D.make_level([prob], level, cfg, store, group)
+    local_level = backend.local if hasattr(backend, "local") else backend
+    rows, gens = P.se3.pose_rows(guess)
+    backend.set_poses(rows, gens)
+    cost0, count0 = backend.evaluate_current()
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t_setup
+    total_pp = valid_pixel_pairs(prob, level)
+    n_pairs = len(prob.graph.edges)
+
+    lam = cfg.lm_initial_lambda
+    state = {"cost": cost0, "lam": lam}
+
+    def step():
+        ok_s, ok_u, c, n = backend.try_step(state["lam"])
+        if ok_s and ok_u and c < state["cost"] and n > 0:
+            backend.accept()
+            state["cost"] = c
+            state["lam"] = max(state["lam"] * 0.5, 1e-12)
+        else:
+            state["lam"] *= cfg.lm_factor
+
+    for _ in range(args.warmup):
+        step()
+    stream = torch.cuda.current_stream(device)
+    local_level.kernel_events = []
+    launches0 = lib.pba_kernel_launches()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    elapsed_ms = e0.elapsed_time(e1)
+    launches = (lib.pba_kernel_launches() - launches0) / args.steps
+    lin_ms = [a.elapsed_time(b) for a, b in local_level.kernel_events]
+    local_level.kernel_events = None
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(t.item())
+    ms_per_step = elapsed_ms / args.steps
+
+    # ---- e2e: host pose buffers in, poses + cost out, every step --------
+    e2e = None
+    if hasattr(backend, "set_poses"):
+        host_in = torch.from_numpy(rows).pin_memory()
+        gens_in = torch.from_numpy(gens.astype(np.int32)).pin_memory()
+        host_out = torch.empty_like(host_in).pin_memory()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            L = local_level
+            L.poses[L.cur].copy_(host_in, non_blocking=True)
+            L.gens[L.cur].copy_(gens_in, non_blocking=True)
+            backend.try_step(cfg.lm_initial_lambda)
+            host_out.copy_(L.poses[1 - L.cur], non_blocking=True)
+            stream.synchronize()
+        f1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = f0.elapsed_time(f1) / args.steps
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=device)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+        e2e = {"value": total_pp / (e2e_ms / 1e3), "unit": "pixel-pairs/s",
+               "h2d_bytes_per_step": int(host_in.numel() * 8 + gens_in.numel() * 4),
+               "d2h_bytes_per_step": int(host_out.numel() * 8 + 64),
+               "ms_per_step": e2e_ms}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return None
+
+    peak, peak_kind = measured_peak_hbm()
+    lin_avg_ms = statistics.mean(lin_ms) if lin_ms else float("nan")
+    my_pp = getattr(local_level, "pixels_shard", None)
+    shard_pp = total_pp if world == 1 else valid_pixel_pairs_shard(prob, level, local_level)
+    achieved = shard_pp * BYTES_PER_PIXEL_PAIR / (lin_avg_ms / 1e3) / 1e9
+    trafficd = ncu_traffic(args.config)
+    traffic = None
+    if trafficd and trafficd.get("dram_bytes_per_pixel_pair"):
+        traffic = trafficd["dram_bytes_per_pixel_pair"] * shard_pp
+    line = {
+        "metric": "GN iteration throughput: pixel-pair residuals/s (one LM iteration at the "
+                  "finest level: solve + pose update + linearise + assemble)",
+        "value": total_pp / (ms_per_step / 1e3),
+        "unit": "pixel-pairs/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {
+            "workload": f"{args.config}: {meta['desc']}",
+            "frames": meta["frames"],
+            "pairs": n_pairs,
+            "pixel_pairs_per_iteration": total_pp,
+            "level": f"finest ({meta['cam'].height}x{meta['cam'].width})",
+            "parallelism": f"pair-sharded x{world}" if world > 1 else "single GPU",
+            "l2": "inputs larger than L2: %.1f GB of resident texels" % (store.texel_bytes() / 1e9),
+            "precision": "fp64 geometry/residuals/Jacobians/b/cost, fp32 per-thread H partials",
+            "gn_iteration_ms": ms_per_step,
+            "setup_seconds": round(t_setup, 2),
+            "graph_seconds": round(meta["graph_seconds"], 2),
+            "initial_cost": cost0,
+            "initial_valid_blocks": count0,
+        },
+        "roofline": {
+            "bound": "hbm",
+            "kernel": "linearize_kernel (+ per-pair chunk reduce) via pba_linearize",
+            "achieved": achieved,
+            "peak": peak,
+            "peak_kind": peak_kind,
+            "unit": "GB/s",
+            "frac": achieved / peak,
+            "traffic": traffic,
+            "linearize_ms": lin_avg_ms,
+            "linearize_share_of_step": lin_avg_ms / ms_per_step,
+            "algorithmic_bytes_per_launch": shard_pp * BYTES_PER_PIXEL_PAIR,
+        },
+        "e2e": e2e,
+        "gpu_launches": int(round(launches)),
+        "clocks": clocks.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(prob, guess, level, total_pp)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return line
+
+
+def valid_pixel_pairs_shard(prob, level, local_level):
+    import paper_2303_16878_b200 as P
+
+    lo, hi = local_level.pair_lo, local_level.pair_hi
+    g = P.MatchGraph(prob.graph.nodes, prob.graph.edges[lo:hi])
+    return valid_pixel_pairs(P.BAProblem(g, prob.extrinsics, prob.gauge_index), level)
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the oracle port on the host cores (rank 0 only)
+# ---------------------------------------------------------------------------
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    import torch
+
+    device = torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
+    prob, guess, gt, meta = build_problem(args.config, device, args.frames)
+    level = meta["level"]
+    total_pp = valid_pixel_pairs(prob, level)
+    vals = []
+    for k in range(args.warmup + args.steps):
+        cb = cpu_baseline(prob, guess, level, total_pp, target_seconds=args.ref_seconds)
+        if k >= args.warmup:
+            vals.append(cb)
+    v = statistics.median(c["value"] for c in vals)
+    ms = statistics.median(c["gn_iteration_ms_extrapolated"] for c in vals)
+    line = {
+        "impl": "reference",
+        "metric": "GN iteration throughput: pixel-pair residuals/s (one LM iteration at the "
+                  "finest level: solve + pose update + linearise + assemble)",
+        "value": v,
+        "unit": "pixel-pairs/s",
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{args.config}: {meta['desc']}", "frames": meta["frames"],
+                   "pairs": len(prob.graph.edges), "pixel_pairs_per_iteration": total_pp},
+        "cpu_baseline": {"value": v, "unit": "pixel-pairs/s", "cores": vals[-1]["cores"],
+                         "kind": "port", "sample": vals[-1]["sample"]},
+        "e2e": {"value": v, "unit": "pixel-pairs/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--frames", type=int, default=None, help="override the frame count")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-seconds", type=float, default=4.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,200 @@
+/*
+ * pba.h — C ABI of the B200-native photometric bundle-adjustment hot path.
+ *
+ * The reference (photoba, pure Python/numpy) has no FFI; its internal seam
+ * for this path is `_LevelProblem` (pkg/src/photoba/solver.py:393-460) plus
+ * the solve/update lines of `_solve_level_multi` (solver.py:505-537).  Each
+ * entry point below replaces one piece of that seam; the comment on each
+ * names the reference code it stands in for.  A maintainer binds these with
+ * ctypes; the Python package
+ * `paper_2303_16878_b200` is exactly such a binding.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Pointers documented as "device" are
+ *    CUDA device pointers owned by the caller (torch tensors in the Python
+ *    host); the library never frees caller memory and allocates nothing on
+ *    the device itself.  "host" pointers are ordinary CPU memory.
+ *  - Every call enqueues work on `stream` (a cudaStream_t passed as void*,
+ *    NULL = legacy default stream) and returns without synchronising,
+ *    except where a function is documented to read back a status word.
+ *  - Return 0 on success, otherwise one of PBA_ERR_*; `pba_last_error()`
+ *    returns a human-readable message for the calling thread.
+ *  - Poses and extrinsics are rows of 12 doubles: rotation row-major (9)
+ *    followed by translation (3).  This is Pose.rotation / Pose.translation
+ *    (geometry.py:101-122) flattened.
+ */
+#ifndef PBA_B200_H
+#define PBA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PBA_OK 0
+#define PBA_ERR_ARG 1          /* -> ValueError */
+#define PBA_ERR_CUDA 2         /* -> RuntimeError(pba_last_error()) */
+#define PBA_ERR_SINGULAR 3     /* -> UnderConstrainedError / LM lambda bump (solver.py:513-522) */
+#define PBA_ERR_PERTURBATION 4 /* -> InvalidPerturbationError (geometry.py:208-212) */
+
+#define PBA_PINHOLE 0   /* sensors.py PINHOLE */
+#define PBA_SPHERICAL 1 /* sensors.py SPHERICAL */
+
+/* Per-pair record of the linearisation: the reference `_EdgeTerm`
+ * (solver.py:343-353) flattened to 92 doubles.
+ *   [ 0..20]  H_ii upper triangle, row-major   (sum J_i^T W J_i)
+ *   [21..41]  H_jj upper triangle, row-major   (sum J_j^T W J_j)
+ *   [42..77]  H_ij full 6x6, row-major         (sum J_i^T W J_j)
+ *   [78..83]  b_i                               (sum J_i^T W e)
+ *   [84..89]  b_j
+ *   [90]      cost  (sum of Huber losses, solver.py:374)
+ *   [91]      count (number of valid blocks, exact integer in a double) */
+#define PBA_RECORD_DOUBLES 92
+#define PBA_REC_HII 0
+#define PBA_REC_HJJ 21
+#define PBA_REC_HIJ 42
+#define PBA_REC_BI 78
+#define PBA_REC_BJ 84
+#define PBA_REC_COST 90
+#define PBA_REC_COUNT 91
+
+/* Texel mask bits (also stored in the separate per-pixel mask plane). */
+#define PBA_MASK_DEPTH_VALID 1u   /* CueImage.depth_valid        (cues.py:117)     */
+#define PBA_MASK_NORMAL_VALID 2u  /* CueImage.normal_valid       (cues.py:120)     */
+#define PBA_MASK_SAMP_CORE 4u     /* sampleable_intensity & _depth (cues.py:132-133) */
+#define PBA_MASK_SAMP_NORMAL 8u   /* sampleable_normals          (cues.py:134)     */
+
+/* Sensor intrinsics of one pyramid level: `Intrinsics` (sensors.py:31-76). */
+typedef struct pba_camera {
+  int32_t model; /* PBA_PINHOLE | PBA_SPHERICAL */
+  int32_t width;
+  int32_t height;
+  int32_t _pad;
+  double fx, fy, cx, cy;
+  double depth_min, depth_max;
+} pba_camera; /* 64 bytes */
+
+/* One (frame, level) image resident in HBM. */
+typedef struct pba_frame {
+  const void* texels;      /* device: width*height texels, pba_texel_bytes() each */
+  const uint8_t* mask;     /* device: width*height mask bytes (PBA_MASK_*) */
+  const double* ray_table; /* device: per-column/row unprojection table, see pba_ray_table_doubles() */
+  pba_camera cam;
+} pba_frame; /* 88 bytes */
+
+/* One directed residual pair i -> j: a `_LevelProblem.contexts` entry
+ * (solver.py:400-414). */
+typedef struct pba_pair {
+  int32_t pose_i, pose_j; /* rows of the pose array (reference node positions) */
+  int32_t src, dst;       /* slots in the frame table */
+  int32_t ext;            /* row of the extrinsics array (SensorExtrinsics.offset) */
+  int32_t n_chunks;       /* number of pixel chunks of this pair (filled by pba_plan_chunks) */
+  double occ_tol;         /* occlusion tolerance at this level (solver.py:410); +inf disables */
+} pba_pair; /* 32 bytes */
+
+/* Robust-kernel and sampling controls: `SolverConfig` (solver.py:56-91). */
+typedef struct pba_config {
+  double huber_delta[3]; /* intensity, depth, normal */
+  double omega[5];       /* [I, D, nx, ny, nz] = omega_diagonal() (solver.py:90-91) */
+  int32_t pixel_stride;  /* source pixel stride (solver.py:200-207) */
+  int32_t _pad;
+} pba_config;
+
+/* ---- layout queries --------------------------------------------------- */
+size_t pba_texel_bytes(void);
+/* Number of doubles in a ray table for `cam`: 2*width + 2*height.
+ * Pinhole: [ (u-cx)/fx for u<W | unused W | (v-cy)/fy for v<H | unused H ]
+ * Spherical: [ cos az_u | sin az_u | cos el_v | sin el_v ]
+ * It is filled on the host (unproject, sensors.py:133-154). */
+size_t pba_ray_table_doubles(const pba_camera* cam);
+/* Library version string. */
+const char* pba_version(void);
+/* Message of the last failing call on this thread. */
+const char* pba_last_error(void);
+/* Number of kernels this library has launched in this process (diagnostics;
+ * bench.py reports it per timed step). */
+uint64_t pba_kernel_launches(void);
+
+/* ---- per-frame preprocessing: CueImage.__post_init__ (cues.py:106-147) --
+ * intensity/depth (H*W doubles) and normals (H*W*3 doubles) are device
+ * pointers.  Applies the depth clamp, validity masks, neighbour coherence
+ * and central-difference gradients and writes the texel image + mask plane.
+ * `scratch` must hold pba_build_texels_scratch_bytes(cam) bytes. */
+size_t pba_build_texels_scratch_bytes(const pba_camera* cam);
+int pba_build_texels(const pba_camera* cam, const double* intensity, const double* depth,
+                     const double* normals, void* texels, uint8_t* mask, void* scratch,
+                     void* stream);
+
+/* ---- linearisation: _LevelProblem.evaluate per-pair part --------------
+ * (solver.py:416-426 -> _edge_term :356-390 -> PairContext.evaluate :222-303)
+ *
+ * Work is split into chunks of `chunk_pixels` source pixels (of the
+ * strided source grid).  pba_plan_chunks fills pairs[].n_chunks (host) and
+ * writes the chunk table (host, 2 int32 per chunk: pair index, first pixel)
+ * and the per-pair chunk offsets (host, n_pairs+1 int32).  Returns the chunk
+ * count via *n_chunks_out.  Pass chunk_table == NULL to only count. */
+int pba_plan_chunks(pba_pair* pairs, int32_t n_pairs, const pba_camera* src_cams,
+                    int32_t pixel_stride, int32_t chunk_pixels, int32_t* chunk_table,
+                    int32_t* pair_chunk_offsets, int64_t* n_chunks_out);
+
+/* frames, pairs, chunk_table, pair_chunk_offsets, poses (n_poses x 12),
+ * extrinsics (n_ext x 12), partials (n_chunks x 92) and records
+ * (n_pairs x 92) are device pointers; cfg is a host pointer.
+ * want_jacobians = 0 is the cost-only path of total_error
+ * (solver.py:655-670): ok_jac is not applied and only cost/count are
+ * produced (the H/b fields are zero). */
+int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int32_t n_pairs,
+                  const int32_t* chunk_table, int64_t n_chunks, const int32_t* pair_chunk_offsets,
+                  int32_t chunk_pixels, const double* poses, const double* extrinsics,
+                  const pba_config* cfg, int32_t want_jacobians, double* partials,
+                  double* records, void* stream);
+
+/* ---- assembly: _LevelProblem.evaluate dense part (solver.py:428-449) ---
+ * Fixed-edge-order sums of per-pair records into the dense normal
+ * equations.  The assembly plan is built on the host by pba_plan_assembly:
+ *   slot_of_pose[n_poses] (host in): 6x6 slot of each pose, -1 for the gauge
+ *   pair_pose_i/j (host in): pose indices per pair (edge order)
+ * Outputs (host): diag_ptr[n_free+1], diag_items[2*n_pairs] (pair<<1|side),
+ * off_ptr[n_off+1], off_rc[2*n_off] (row slot, col slot), off_items[n_pairs]
+ * (pair<<1|transposed).  *n_off_out receives the number of off-diagonal
+ * blocks; pass NULL outputs to only count. */
+int pba_plan_assembly(const int32_t* slot_of_pose, int32_t n_poses, const int32_t* pair_pose_i,
+                      const int32_t* pair_pose_j, int32_t n_pairs, int32_t* diag_ptr,
+                      int32_t* diag_items, int32_t* off_ptr, int32_t* off_rc, int32_t* off_items,
+                      int32_t* n_off_out);
+
+/* records (device, n_pairs x 92), plan arrays (device), H (device,
+ * dim x dim, row-major, dim = 6*n_free), b (device, dim), totals (device,
+ * 2 doubles: cost, count summed in edge order). H is fully overwritten. */
+int pba_assemble(const double* records, int32_t n_pairs, int32_t n_free, const int32_t* diag_ptr,
+                 const int32_t* diag_items, int32_t n_off, const int32_t* off_ptr,
+                 const int32_t* off_rc, const int32_t* off_items, double* H, double* b,
+                 double* totals, void* stream);
+/* Cost/count only (cost-only path and the LM acceptance test). */
+int pba_sum_totals(const double* records, int32_t n_pairs, double* totals, void* stream);
+
+/* ---- linear solve: np.linalg.solve(H + lam*diag(H), -b) (solver.py:510-512)
+ * Dense fp64 Cholesky of the damped system.  H, b: device inputs (not
+ * modified).  work: device, pba_solve_work_bytes(dim) bytes.  delta: device
+ * output.  status: device int32 written 0 on success, 1 when the damped
+ * matrix is not positive definite (the reference's LinAlgError). */
+size_t pba_solve_work_bytes(int32_t dim);
+int pba_solve_dense(const double* H, const double* b, int32_t dim, double lam, void* work,
+                    double* delta, int32_t* status, void* stream);
+
+/* ---- pose update: _LevelProblem.apply_step (solver.py:451-460) --------
+ * poses_out[k] = poses_in[k] * exp(delta[slot_k]) for every non-gauge pose
+ * (geometry.py:202-219), in fp64.  generation (device int32, n_poses) is
+ * Pose.generation; gen_out receives the new counters and rotations are
+ * re-orthonormalised when they reach 1000 (geometry.py:17, 137-143).
+ * status (device int32) is set to 1 when some ||dq|| >= 1. */
+int pba_apply_step(const double* poses_in, const int32_t* gen_in, const double* delta,
+                   int32_t n_poses, int32_t gauge, double* poses_out, int32_t* gen_out,
+                   int32_t* status, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PBA_B200_H */

@@ -1,0 +1,33 @@
+"""B200-native photometric bundle adjustment (arXiv 2303.16878 hot path).
+
+Drop-in for the BA entry points and data types of the reference package
+`photoba` (pkg/src/photoba/__init__.py:9-71): the same names, arguments and
+results, with the per-iteration work — warp, residuals and Jacobians, the
+12x12 JᵀWJ / JᵀWe accumulation, dense assembly, the damped linear solve and
+the pose update — executed by hand-written sm_100a kernels
+(csrc/*.cu, C ABI in include/pba.h).
+"""
+
+from .se3 import (InvalidPerturbationError, PerturbationVector, Pose, boxplus, exp, relative,
+                  rotation_angle, skew)
+from .camera import (PINHOLE, SPHERICAL, Intrinsics, SensorExtrinsics, project,
+                     projective_jacobian, unproject)
+from .cueimage import CueImage, CuePyramid, DeviceCueImage, PyramidConfigError, footprint_index
+from .pairgraph import (COVISIBILITY, ODOMETRY, Edge, FrameNode, GraphConfigError, MatchCriteria,
+                        MatchGraph, build_graph, dump_edges, overlap_ratio)
+from .bundle import (CONSECUTIVE, COUPLED, BAProblem, FusionConfigError, IterationRecord,
+                     SolveResult, SolverConfig, UnderConstrainedError, check_connectivity,
+                     solve_fusion, solve_hierarchical, solve_level, total_error)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "BAProblem", "CONSECUTIVE", "COUPLED", "COVISIBILITY", "CueImage", "CuePyramid",
+    "DeviceCueImage", "Edge", "FrameNode", "FusionConfigError", "GraphConfigError",
+    "InvalidPerturbationError", "Intrinsics", "IterationRecord", "MatchCriteria", "MatchGraph",
+    "ODOMETRY", "PINHOLE", "PerturbationVector", "Pose", "PyramidConfigError", "SPHERICAL",
+    "SensorExtrinsics", "SolveResult", "SolverConfig", "UnderConstrainedError", "boxplus",
+    "build_graph", "check_connectivity", "dump_edges", "exp", "footprint_index",
+    "overlap_ratio", "project", "projective_jacobian", "relative", "rotation_angle", "skew",
+    "solve_fusion", "solve_hierarchical", "solve_level", "total_error", "unproject",
+]

@@ -1,0 +1,256 @@
+"""Five-channel cue images and pyramids of the drop-in API.
+
+Mirrors `CueImage`, `CuePyramid` and the pyramid index map of the reference
+(pkg/src/photoba/cues.py:84-166, 254-261).  A cue image stacks intensity,
+depth/range and a unit-normal field; the derived validity masks and
+central-difference gradients follow cues.py:106-147 exactly (they are also
+rebuilt on the device by csrc/texels.cu when a frame is uploaded, and the
+two are checked against each other and against the reference).
+
+`DeviceCueImage` is the GPU-resident variant used when frames are produced
+on the device (synthetic benchmarks): it holds torch CUDA tensors and only
+materialises host arrays on request.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .camera import Intrinsics
+
+NORMAL_COHERENCE_MIN_DOT = 0.9  # cues.py:44
+
+
+class PyramidConfigError(ValueError):
+    """Bad scale list for pyramid construction (cues.py:22-23)."""
+
+
+def _interior(a: np.ndarray) -> np.ndarray:
+    return a[1:-1, 1:-1]
+
+
+def _four_neighbours(a: np.ndarray):
+    """(right, left, down, up) neighbours of every interior pixel."""
+    return a[1:-1, 2:], a[1:-1, :-2], a[2:, 1:-1], a[:-2, 1:-1]
+
+
+def central_gradients(values: np.ndarray, valid: np.ndarray):
+    """[d/dcol, d/drow] half central differences, zero unless the pixel and its
+    4-neighbourhood are valid; the border never has a gradient (cues.py:63-81)."""
+    ok = np.zeros(valid.shape, dtype=bool)
+    inner = _interior(valid).copy()
+    for nb in _four_neighbours(valid):
+        inner &= nb
+    ok[1:-1, 1:-1] = inner
+    grad = np.zeros(values.shape + (2,))
+    right, left, down, up = _four_neighbours(values)
+    grad[1:-1, 1:-1, ..., 0] = 0.5 * (right - left)
+    grad[1:-1, 1:-1, ..., 1] = 0.5 * (down - up)
+    grad[~ok] = 0.0
+    return grad, ok
+
+
+def neighbour_coherence(normals: np.ndarray, valid: np.ndarray) -> np.ndarray:
+    """Interior pixels whose four neighbours' normals agree (dot >= 0.9)."""
+    ok = np.zeros(valid.shape, dtype=bool)
+    c = _interior(normals)
+    agree = np.ones(c.shape[:2], dtype=bool)
+    for nb in _four_neighbours(normals):
+        dot = (c[..., 0] * nb[..., 0] + c[..., 1] * nb[..., 1]) + c[..., 2] * nb[..., 2]
+        agree &= dot >= NORMAL_COHERENCE_MIN_DOT
+    ok[1:-1, 1:-1] = agree
+    return ok
+
+
+_DERIVED = ("depth_valid", "normal_valid", "grad_intensity", "grad_depth", "grad_normals",
+            "sampleable_intensity", "sampleable_depth", "sampleable_normals")
+
+
+@dataclass
+class CueImage:
+    """Intensity in [0,1], depth/range in metres, normals; masks derived eagerly."""
+
+    intensity: np.ndarray
+    depth: np.ndarray
+    normals: np.ndarray
+    intrinsics: Intrinsics
+
+    depth_valid: np.ndarray = field(init=False, repr=False)
+    normal_valid: np.ndarray = field(init=False, repr=False)
+    grad_intensity: np.ndarray = field(init=False, repr=False)
+    grad_depth: np.ndarray = field(init=False, repr=False)
+    grad_normals: np.ndarray = field(init=False, repr=False)
+    sampleable_intensity: np.ndarray = field(init=False, repr=False)
+    sampleable_depth: np.ndarray = field(init=False, repr=False)
+    sampleable_normals: np.ndarray = field(init=False, repr=False)
+
+    def __post_init__(self) -> None:
+        inten = np.asarray(self.intensity, dtype=float)
+        h, w = inten.shape
+        depth = np.array(self.depth, dtype=float)
+        normals = np.array(self.normals, dtype=float)
+        if depth.shape != (h, w) or normals.shape != (h, w, 3):
+            raise ValueError("cue channel shapes disagree")
+        cam = self.intrinsics
+        if (cam.height, cam.width) != (h, w):
+            raise ValueError("intrinsics do not match image size")
+        with np.errstate(invalid="ignore"):
+            out_of_range = ~np.isfinite(depth) | (depth < cam.depth_min) | (depth > cam.depth_max)
+        depth[out_of_range] = 0.0
+        depth_valid = depth > 0.0
+        nrm = np.sqrt((normals[..., 0] ** 2 + normals[..., 1] ** 2) + normals[..., 2] ** 2)
+        normal_valid = (nrm > 0.5) & depth_valid
+        normals[~normal_valid] = 0.0
+        g_i, ok_i = central_gradients(inten, depth_valid)
+        g_d, ok_d = central_gradients(depth, depth_valid)
+        coherent = normal_valid & neighbour_coherence(normals, normal_valid)
+        g_n, ok_n = central_gradients(normals, coherent)
+        fields = dict(intensity=inten, depth=depth, normals=normals, depth_valid=depth_valid,
+                      normal_valid=normal_valid, grad_intensity=g_i, grad_depth=g_d,
+                      grad_normals=g_n, sampleable_intensity=ok_i, sampleable_depth=ok_d,
+                      sampleable_normals=ok_n)
+        for name, arr in fields.items():
+            arr = np.array(arr, copy=True) if not arr.flags.owndata else arr
+            arr.flags.writeable = False
+            setattr(self, name, arr)
+
+    @property
+    def shape(self) -> tuple[int, int]:
+        return self.intensity.shape
+
+
+class DeviceCueImage:
+    """A cue image whose channels live on the GPU as torch tensors.
+
+    Used for device-generated inputs (the synthetic benchmark path); the
+    device store consumes the tensors directly.  Host arrays are produced
+    lazily, e.g. `depth_valid` for graph construction.
+    """
+
+    def __init__(self, intensity, depth, normals, intrinsics: Intrinsics):
+        self.device_intensity = intensity
+        self.device_depth = depth
+        self.device_normals = normals
+        self.intrinsics = intrinsics
+        self._host: CueImage | None = None
+
+    @property
+    def shape(self) -> tuple[int, int]:
+        return tuple(self.device_intensity.shape)
+
+    def host(self) -> CueImage:
+        if self._host is None:
+            self._host = CueImage(self.device_intensity.cpu().numpy(),
+                                  self.device_depth.cpu().numpy(),
+                                  self.device_normals.cpu().numpy(), self.intrinsics)
+        return self._host
+
+    @property
+    def depth_valid(self) -> np.ndarray:
+        d = self.device_depth
+        cam = self.intrinsics
+        ok = (d >= cam.depth_min) & (d <= cam.depth_max) & (d > 0)
+        return ok.cpu().numpy()
+
+    @property
+    def depth(self) -> np.ndarray:
+        return self.host().depth
+
+    def __getattr__(self, name):
+        if name in _DERIVED or name in ("intensity", "normals"):
+            return getattr(self.host(), name)
+        raise AttributeError(name)
+
+
+@dataclass(frozen=True)
+class CuePyramid:
+    """Cue images of one view, coarsest level first."""
+
+    levels: tuple
+    scales: tuple
+
+    def __post_init__(self) -> None:
+        if len(self.levels) != len(self.scales):
+            raise ValueError("levels and scales disagree")
+
+    def __len__(self) -> int:
+        return len(self.levels)
+
+
+def footprint_index(h: int, w: int, s: float):
+    """Flat output index of every source pixel under u_out = floor(u * s),
+    the kept mask and the output size (cues.py:254-261; bit-exact)."""
+    out_h, out_w = int(math.floor(h * s)), int(math.floor(w * s))
+    rows = np.floor(np.arange(h) * s).astype(np.int64)
+    cols = np.floor(np.arange(w) * s).astype(np.int64)
+    keep = (rows[:, None] < out_h) & (cols[None, :] < out_w)
+    return rows[:, None] * out_w + cols[None, :], keep, out_h, out_w
+
+
+def validate_scales(scales) -> tuple:
+    scales = tuple(float(s) for s in scales)
+    if not scales:
+        raise PyramidConfigError("need at least one pyramid scale")
+    if any(not 0.0 < s <= 1.0 for s in scales):
+        raise PyramidConfigError(f"scales must lie in (0, 1], got {scales}")
+    if any(b <= a for a, b in zip(scales, scales[1:])):
+        raise PyramidConfigError(f"scales must increase toward the finest level, got {scales}")
+    return scales
+
+
+def downscale_cues(intensity, depth, normals, depth_ok, normal_ok, s):
+    """One pyramid level (cues.py:278-326): valid-mean intensity (plain mean
+    when a footprint has no valid return), lower-median depth, averaged and
+    renormalised normals (dropped when incoherent)."""
+    h, w = depth.shape
+    idx, keep, out_h, out_w = footprint_index(h, w, s)
+    n_out = out_h * out_w
+    flat = idx[keep]
+    dok = depth_ok[keep]
+    nok = normal_ok[keep]
+    vals = np.asarray(intensity, dtype=float)[keep]
+    sum_v = np.bincount(flat[dok], weights=vals[dok], minlength=n_out)
+    cnt_v = np.bincount(flat[dok], minlength=n_out)
+    sum_a = np.bincount(flat, weights=vals, minlength=n_out)
+    cnt_a = np.bincount(flat, minlength=n_out)
+    out_i = np.where(cnt_v > 0, sum_v / np.maximum(cnt_v, 1), sum_a / np.maximum(cnt_a, 1))
+    # lower median of each footprint's valid depths
+    grp = flat[dok]
+    dv = np.asarray(depth, dtype=float)[keep][dok]
+    order = np.lexsort((dv, grp))
+    g_sorted, d_sorted = grp[order], dv[order]
+    lo = np.searchsorted(g_sorted, np.arange(n_out), side="left")
+    hi = np.searchsorted(g_sorted, np.arange(n_out), side="right")
+    out_d = np.zeros(n_out)
+    has = hi > lo
+    out_d[has] = d_sorted[lo[has] + (hi[has] - lo[has] - 1) // 2]
+    # normals: mean of valid normals, renormalised where coherent
+    cnt_n = np.bincount(flat[nok], minlength=n_out)
+    mean_n = np.zeros((n_out, 3))
+    for k in range(3):
+        mean_n[:, k] = np.bincount(flat[nok], weights=np.asarray(normals)[..., k][keep][nok],
+                                   minlength=n_out)
+    with np.errstate(invalid="ignore", divide="ignore"):
+        mean_n = mean_n / np.maximum(cnt_n, 1)[:, None]
+    nrm = np.linalg.norm(mean_n, axis=-1)
+    good = (cnt_n > 0) & (nrm >= 0.5)
+    unit = np.zeros_like(mean_n)
+    unit[good] = mean_n[good] / nrm[good, None]
+    return out_i.reshape(out_h, out_w), out_d.reshape(out_h, out_w), unit.reshape(out_h, out_w, 3)
+
+
+def build_pyramid_from_normals(intensity, depth, normals, cam: Intrinsics, scales) -> CuePyramid:
+    """Pyramid from full-resolution cues with given normals (cues.py:342-375,
+    with the normal-estimation step replaced by the provided field)."""
+    scales = validate_scales(scales)
+    depth = np.where(np.isfinite(depth), depth, 0.0)
+    depth_ok = (depth >= cam.depth_min) & (depth <= cam.depth_max)
+    normal_ok = np.linalg.norm(normals, axis=-1) > 0.5
+    levels = []
+    for s in scales:
+        li, ld, ln = downscale_cues(intensity, depth, normals, depth_ok, normal_ok, s)
+        levels.append(CueImage(li, ld, ln, cam.scaled(s)))
+    return CuePyramid(tuple(levels), scales)

@@ -1,0 +1,371 @@
+"""GPU-resident state of the BA hot path and the calls into libpba_b200.
+
+`FrameStore` keeps every (frame, level) cue image resident in HBM as the
+128-byte texel layout plus a mask plane (built on the device from the
+reference CueImage channels, csrc/texels.cu).  `DeviceLevel` is the
+device replacement of the reference `_LevelProblem` (solver.py:393-460):
+pair table, chunk plan, assembly plan, and the buffers of one LM level, with
+the linearise / assemble / solve / update steps all enqueued on one CUDA
+stream.  Per LM iteration exactly one 64-byte device->host copy happens
+(cost, count and the two status words).
+
+torch is used only to own device memory and to name the stream.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+import torch
+
+from . import native as N
+from .camera import PINHOLE, ray_table
+
+THREADS_PER_CHUNK = 256
+SM_COUNT = 148
+
+
+def camera_struct(intr) -> N.Camera:
+    return N.Camera(N.PBA_PINHOLE if intr.model == PINHOLE else N.PBA_SPHERICAL,
+                    int(intr.width), int(intr.height), 0, float(intr.fx), float(intr.fy),
+                    float(intr.cx), float(intr.cy), float(intr.depth_min), float(intr.depth_max))
+
+
+def _stream_ptr(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _struct_tensor(arr, device) -> torch.Tensor:
+    raw = bytes(memoryview(arr).cast("B")) if len(arr) else b"\0" * 8
+    return torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(device)
+
+
+def chunk_pixels_for(total_pixels: int) -> int:
+    """Source pixels per CTA.  Chosen from the whole level problem (never
+    from a shard) so per-pair sums are identical for any GPU count: enough
+    CTAs for ~4 waves of 148 SMs, at most 32 pixels per thread."""
+    ppt = total_pixels // (THREADS_PER_CHUNK * SM_COUNT * 4)
+    ppt = max(1, min(32, int(ppt)))
+    return THREADS_PER_CHUNK * ppt
+
+
+class FrameStore:
+    """Device-resident texel images, one per cue image object."""
+
+    def __init__(self, device):
+        self.device = torch.device(device)
+        self._frames: dict[int, tuple] = {}
+        self._rays: dict[tuple, torch.Tensor] = {}
+        self._scratch: torch.Tensor | None = None
+        self._lib = N.load()
+
+    def ray(self, intr) -> torch.Tensor:
+        key = (intr.model, intr.width, intr.height, intr.fx, intr.fy, intr.cx, intr.cy)
+        t = self._rays.get(key)
+        if t is None:
+            t = torch.from_numpy(ray_table(intr)).to(self.device)
+            self._rays[key] = t
+        return t
+
+    def _channels(self, cue):
+        dev = getattr(cue, "device_intensity", None)
+        if dev is not None:
+            return (cue.device_intensity.to(self.device, torch.float64).contiguous(),
+                    cue.device_depth.to(self.device, torch.float64).contiguous(),
+                    cue.device_normals.to(self.device, torch.float64).contiguous())
+        out = []
+        for a in (cue.intensity, cue.depth, cue.normals):
+            h = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
+            out.append(h.to(self.device, non_blocking=False))
+        return tuple(out)
+
+    def frame(self, cue):
+        """(texels, mask, ray table, Camera) of a cue image, uploading on first use."""
+        key = id(cue)
+        hit = self._frames.get(key)
+        if hit is not None:
+            return hit[1:]
+        intr = cue.intrinsics
+        cam = camera_struct(intr)
+        h, w = int(intr.height), int(intr.width)
+        inten, depth, normals = self._channels(cue)
+        if tuple(inten.shape) != (h, w):
+            raise ValueError("intrinsics do not match image size")
+        texels = torch.empty(h * w * int(self._lib.pba_texel_bytes()), dtype=torch.uint8,
+                             device=self.device)
+        mask = torch.empty(h * w, dtype=torch.uint8, device=self.device)
+        need = int(self._lib.pba_build_texels_scratch_bytes(ctypes.byref(cam)))
+        if self._scratch is None or self._scratch.numel() < need:
+            self._scratch = torch.empty(need, dtype=torch.uint8, device=self.device)
+        N.check(self._lib.pba_build_texels(ctypes.byref(cam), inten.data_ptr(), depth.data_ptr(),
+                                           normals.data_ptr(), texels.data_ptr(), mask.data_ptr(),
+                                           self._scratch.data_ptr(), _stream_ptr(self.device)),
+                "pba_build_texels")
+        ray = self.ray(intr)
+        # keep `cue` referenced so its id() stays unique while cached
+        self._frames[key] = (cue, texels, mask, ray, cam)
+        return texels, mask, ray, cam
+
+    def texel_bytes(self) -> int:
+        return sum(v[1].numel() + v[2].numel() for v in self._frames.values())
+
+
+def level_contexts(problems, level, cfg):
+    """Reference contexts of _LevelProblem.__init__ (solver.py:400-414) as
+    (pose_i, pose_j, node_i, node_j, extrinsics, occlusion_tol) tuples."""
+    out = []
+    for problem in problems:
+        nodes = problem.graph.nodes
+        index_of = {n.id: k for k, n in enumerate(nodes)}
+        for edge in problem.graph.edges:
+            ni, nj = nodes[index_of[edge.i]], nodes[index_of[edge.j]]
+            if ni.sensor_id != nj.sensor_id:
+                from .bundle import FusionConfigError
+                raise FusionConfigError("edges must connect frames of one sensor")
+            ext = problem.extrinsics_of(ni.sensor_id)
+            tol = cfg.occlusion_depth_tolerance / ni.pyramid.scales[level]
+            out.append((index_of[edge.i], index_of[edge.j], ni, nj, ext, tol))
+    return out
+
+
+def config_struct(cfg) -> N.Config:
+    c = N.Config()
+    c.huber_delta[:] = [cfg.huber_delta_intensity, cfg.huber_delta_depth, cfg.huber_delta_normal]
+    c.omega[:] = [cfg.omega_intensity, cfg.omega_depth, *cfg.omega_normal]
+    c.pixel_stride = int(cfg.pixel_stride)
+    return c
+
+
+class DeviceLevel:
+    """One pyramid level of one (or several, for fusion) BA problems on one GPU.
+
+    `pair_range` restricts the linearisation to a contiguous slice of the
+    edge-ordered pair list (the multi-GPU shard); `assemble=True` builds the
+    dense-assembly plan and solve buffers (the rank that solves).
+    """
+
+    def __init__(self, problems, level, cfg, store: FrameStore, *, pair_range=None,
+                 assemble=True, tolerance_override=None):
+        self.lib = N.load()
+        self.store = store
+        self.device = store.device
+        self.cfg = cfg
+        self.level = level
+        self.kernel_events = None  # list -> (start, stop) CUDA events per pba_linearize call
+        self.n_poses = len(problems[0].graph.nodes)
+        self.gauge = problems[0].gauge_index
+        self.ccfg = config_struct(cfg)
+        ctxs = level_contexts(problems, level, cfg)
+        if tolerance_override is not None:
+            ctxs = [c[:5] + (tolerance_override,) for c in ctxs]
+        self.n_pairs_total = len(ctxs)
+        self.pose_i = np.array([c[0] for c in ctxs], dtype=np.int32)
+        self.pose_j = np.array([c[1] for c in ctxs], dtype=np.int32)
+        # chunk size from the whole level (shard-independent)
+        stride = int(cfg.pixel_stride)
+        total_px = 0
+        for c in ctxs:
+            intr = c[2].pyramid.levels[level].intrinsics
+            total_px += math.ceil(intr.width / stride) * math.ceil(intr.height / stride)
+        self.total_pixels = total_px
+        self.chunk_pixels = chunk_pixels_for(total_px)
+        lo, hi = (0, len(ctxs)) if pair_range is None else pair_range
+        self.pair_lo, self.pair_hi = lo, hi
+        mine = ctxs[lo:hi]
+        self.n_pairs = len(mine)
+        # frame / extrinsics tables for this shard
+        frames, frame_slot, ext_rows, ext_slot = [], {}, [], {}
+        pairs = (N.Pair * max(1, self.n_pairs))()
+        src_cams = (N.Camera * max(1, self.n_pairs))()
+        for k, (pi, pj, ni, nj, ext, tol) in enumerate(mine):
+            slots = []
+            for node in (ni, nj):
+                cue = node.pyramid.levels[level]
+                if id(cue) not in frame_slot:
+                    tex, mask, ray, cam = store.frame(cue)
+                    frame_slot[id(cue)] = len(frames)
+                    frames.append(N.Frame(tex.data_ptr(), mask.data_ptr(), ray.data_ptr(), cam))
+                slots.append(frame_slot[id(cue)])
+            off = ext.offset
+            ekey = (np.asarray(off.rotation, float).tobytes(), np.asarray(off.translation, float).tobytes())
+            if ekey not in ext_slot:
+                ext_slot[ekey] = len(ext_rows)
+                ext_rows.append(np.concatenate([np.asarray(off.rotation, float).reshape(9),
+                                                np.asarray(off.translation, float).reshape(3)]))
+            pairs[k] = N.Pair(pi, pj, slots[0], slots[1], ext_slot[ekey], 0, float(tol))
+            src_cams[k] = frames[slots[0]].cam
+        n_chunks = ctypes.c_int64(0)
+        N.check(self.lib.pba_plan_chunks(pairs, self.n_pairs, src_cams, stride, self.chunk_pixels,
+                                         None, None, ctypes.byref(n_chunks)), "pba_plan_chunks")
+        self.n_chunks = int(n_chunks.value)
+        chunk_tab = np.zeros(max(1, 2 * self.n_chunks), dtype=np.int32)
+        offsets = np.zeros(self.n_pairs + 1, dtype=np.int32)
+        N.check(self.lib.pba_plan_chunks(pairs, self.n_pairs, src_cams, stride, self.chunk_pixels,
+                                         chunk_tab.ctypes.data, offsets.ctypes.data,
+                                         ctypes.byref(n_chunks)), "pba_plan_chunks")
+        dev = self.device
+        self.frames_t = _struct_tensor((N.Frame * max(1, len(frames)))(*frames), dev)
+        self.pairs_t = _struct_tensor(pairs, dev)
+        self.chunks_t = torch.from_numpy(chunk_tab).to(dev)
+        self.offsets_t = torch.from_numpy(offsets).to(dev)
+        ext_arr = np.array(ext_rows, dtype=np.float64).reshape(-1, 12)
+        self.ext_t = torch.from_numpy(ext_arr if len(ext_arr) else np.zeros((1, 12))).to(dev)
+        self.partials = torch.empty((max(1, self.n_chunks), N.RECORD_DOUBLES), dtype=torch.float64,
+                                    device=dev)
+        self.records = torch.zeros((max(1, self.n_pairs), N.RECORD_DOUBLES), dtype=torch.float64,
+                                   device=dev)
+        self.pixels_shard = sum(
+            math.ceil(c[2].pyramid.levels[level].intrinsics.width / stride)
+            * math.ceil(c[2].pyramid.levels[level].intrinsics.height / stride) for c in mine)
+        self._scal = torch.zeros(8, dtype=torch.float64, device=dev)
+        self._scal_host = torch.zeros(8, dtype=torch.float64).pin_memory()
+        self.poses = [torch.zeros((self.n_poses, 12), dtype=torch.float64, device=dev)
+                      for _ in range(2)]
+        self.gens = [torch.zeros(self.n_poses, dtype=torch.int32, device=dev) for _ in range(2)]
+        self.cur = 0
+        self.has_solver = False
+        if assemble:
+            self._build_solver()
+
+    # ---- solver side --------------------------------------------------------
+    def _build_solver(self):
+        lib, dev = self.lib, self.device
+        slot = np.full(self.n_poses, -1, dtype=np.int32)
+        s = 0
+        for k in range(self.n_poses):
+            if k != self.gauge:
+                slot[k] = s
+                s += 1
+        self.n_free = s
+        self.dim = 6 * s
+        n_off = ctypes.c_int32(0)
+        N.check(lib.pba_plan_assembly(slot.ctypes.data, self.n_poses, self.pose_i.ctypes.data,
+                                      self.pose_j.ctypes.data, self.n_pairs_total, None, None,
+                                      None, None, None, ctypes.byref(n_off)), "pba_plan_assembly")
+        self.n_off = int(n_off.value)
+        diag_ptr = np.zeros(self.n_free + 1, np.int32)
+        diag_items = np.zeros(max(1, 2 * self.n_pairs_total), np.int32)
+        off_ptr = np.zeros(self.n_off + 1, np.int32)
+        off_rc = np.zeros(max(1, 2 * self.n_off), np.int32)
+        off_items = np.zeros(max(1, self.n_pairs_total), np.int32)
+        N.check(lib.pba_plan_assembly(slot.ctypes.data, self.n_poses, self.pose_i.ctypes.data,
+                                      self.pose_j.ctypes.data, self.n_pairs_total,
+                                      diag_ptr.ctypes.data, diag_items.ctypes.data,
+                                      off_ptr.ctypes.data, off_rc.ctypes.data,
+                                      off_items.ctypes.data, ctypes.byref(n_off)),
+                "pba_plan_assembly")
+        t = lambda a: torch.from_numpy(a).to(dev)
+        self.plan = [t(diag_ptr), t(diag_items), t(off_ptr), t(off_rc), t(off_items)]
+        d = max(1, self.dim)
+        self.H = [torch.zeros((d, d), dtype=torch.float64, device=dev) for _ in range(2)]
+        self.b = [torch.zeros(d, dtype=torch.float64, device=dev) for _ in range(2)]
+        self.totals = [torch.zeros(2, dtype=torch.float64, device=dev) for _ in range(2)]
+        self.work = torch.empty(max(8, int(lib.pba_solve_work_bytes(d))), dtype=torch.uint8,
+                                device=dev)
+        self.delta = torch.zeros(d, dtype=torch.float64, device=dev)
+        self.has_solver = True
+
+    # ---- primitive steps -----------------------------------------------------
+    def linearize(self, poses_t: torch.Tensor, want_jacobians: bool = True) -> torch.Tensor:
+        """Per-pair records of this shard at `poses_t` (device (N,12) fp64)."""
+        if self.n_pairs == 0:
+            return self.records[:0]
+        ev = self.kernel_events
+        if ev is not None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record(torch.cuda.current_stream(self.device))
+        N.check(self.lib.pba_linearize(
+            self.frames_t.data_ptr(), self.pairs_t.data_ptr(), self.n_pairs,
+            self.chunks_t.data_ptr(), self.n_chunks, self.offsets_t.data_ptr(), self.chunk_pixels,
+            poses_t.data_ptr(), self.ext_t.data_ptr(), ctypes.byref(self.ccfg),
+            int(bool(want_jacobians)), self.partials.data_ptr(), self.records.data_ptr(),
+            _stream_ptr(self.device)), "pba_linearize")
+        if ev is not None:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record(torch.cuda.current_stream(self.device))
+            ev.append((e0, e1))
+        return self.records[: self.n_pairs]
+
+    def assemble(self, records: torch.Tensor, which: int) -> None:
+        dp, di, op, orc, oi = self.plan
+        N.check(self.lib.pba_assemble(
+            records.data_ptr(), self.n_pairs_total, self.n_free, dp.data_ptr(), di.data_ptr(),
+            self.n_off, op.data_ptr(), orc.data_ptr(), oi.data_ptr(), self.H[which].data_ptr(),
+            self.b[which].data_ptr(), self.totals[which].data_ptr(), _stream_ptr(self.device)),
+            "pba_assemble")
+
+    def sum_totals(self, records: torch.Tensor, out: torch.Tensor) -> None:
+        N.check(self.lib.pba_sum_totals(records.data_ptr(), records.shape[0], out.data_ptr(),
+                                        _stream_ptr(self.device)), "pba_sum_totals")
+
+    def solve(self, which: int, lam: float, status_ptr: int) -> None:
+        N.check(self.lib.pba_solve_dense(self.H[which].data_ptr(), self.b[which].data_ptr(),
+                                         self.dim, float(lam), self.work.data_ptr(),
+                                         self.delta.data_ptr(), status_ptr,
+                                         _stream_ptr(self.device)), "pba_solve_dense")
+
+    def apply_step(self, src: int, dst: int, status_ptr: int) -> None:
+        N.check(self.lib.pba_apply_step(self.poses[src].data_ptr(), self.gens[src].data_ptr(),
+                                        self.delta.data_ptr(), self.n_poses, self.gauge,
+                                        self.poses[dst].data_ptr(), self.gens[dst].data_ptr(),
+                                        status_ptr, _stream_ptr(self.device)), "pba_apply_step")
+
+    # ---- scalar readback -----------------------------------------------------
+    def _read_scalars(self):
+        self._scal_host.copy_(self._scal, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        vals = self._scal_host.numpy().copy()
+        ints = self._scal_host.view(torch.int32).numpy().copy()
+        return vals, ints
+
+    @property
+    def _status_solve_ptr(self) -> int:
+        return self._scal.data_ptr() + 16
+
+    @property
+    def _status_step_ptr(self) -> int:
+        return self._scal.data_ptr() + 24
+
+    # ---- single-GPU LM backend (used by bundle._lm_level) --------------------
+    def set_poses(self, rows: np.ndarray, gens: np.ndarray) -> None:
+        self.cur = 0
+        self.poses[0].copy_(torch.from_numpy(np.ascontiguousarray(rows, dtype=np.float64)))
+        self.gens[0].copy_(torch.from_numpy(np.ascontiguousarray(gens, dtype=np.int32)))
+
+    def evaluate_current(self):
+        """Linearise + assemble at the current poses; returns (cost, count)."""
+        recs = self.linearize(self.poses[self.cur])
+        self.assemble(recs, self.cur)
+        self._scal[0:2].copy_(self.totals[self.cur])
+        vals, _ = self._read_scalars()
+        return float(vals[0]), int(round(vals[1]))
+
+    def try_step(self, lam: float):
+        """solve -> update -> linearise + assemble the candidate, one readback.
+
+        Returns (solve_ok, step_ok, new_cost, new_count)."""
+        cur, cand = self.cur, 1 - self.cur
+        self.solve(cur, lam, self._status_solve_ptr)
+        self.apply_step(cur, cand, self._status_step_ptr)
+        recs = self.linearize(self.poses[cand])
+        self.assemble(recs, cand)
+        self._scal[0:2].copy_(self.totals[cand])
+        vals, ints = self._read_scalars()
+        return ints[4] == 0, ints[6] == 0, float(vals[0]), int(round(vals[1]))
+
+    def accept(self) -> None:
+        self.cur = 1 - self.cur
+
+    def current_rows(self):
+        return (self.poses[self.cur].cpu().numpy().copy(),
+                self.gens[self.cur].cpu().numpy().copy())
+
+    def cost_only(self, rows: np.ndarray):
+        """total_error path: cost/count without Jacobians (solver.py:655-670)."""
+        poses = torch.from_numpy(np.ascontiguousarray(rows, dtype=np.float64)).to(self.device)
+        recs = self.linearize(poses, want_jacobians=False)
+        self.sum_totals(recs, self._scal[0:2])
+        vals, _ = self._read_scalars()
+        return float(vals[0]), int(round(vals[1]))

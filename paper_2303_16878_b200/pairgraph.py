@@ -1,0 +1,181 @@
+"""Match-graph (pair list) construction of the drop-in API.
+
+Mirrors `FrameNode`, `MatchCriteria`, `Edge`, `MatchGraph`, `overlap_ratio`,
+`build_graph`, `dump_edges` (pkg/src/photoba/graph.py:30-181).  The pair
+list feeds the hot path and must match the reference bit for bit, so every
+decision is evaluated with the same numpy expressions in the same order as
+the reference.  What is new is a conservative pre-filter: candidate pairs
+that are rejected by a wide margin on the translation or angle gate are
+dropped with a vectorised test before the exact per-pair evaluation, which
+only ever removes pairs the exact test would also reject (margins are far
+above floating-point noise), so the result is unchanged while an N = 1000
+trajectory is processed in seconds instead of minutes.
+"""
+
+from __future__ import annotations
+
+import math
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass
+
+import numpy as np
+
+from .camera import SensorExtrinsics, project, unproject
+from .se3 import Pose, rotation_angle
+
+COVISIBILITY = "covisibility"
+ODOMETRY = "odometry"
+
+
+class GraphConfigError(ValueError):
+    """Match graph cannot be built from this node set."""
+
+
+@dataclass
+class FrameNode:
+    """One frame: initial pose guess plus its cue pyramid."""
+
+    id: int
+    pose_guess: Pose
+    pyramid: object
+    timestamp: float
+    sensor_id: str = "sensor0"
+
+
+@dataclass(frozen=True)
+class MatchCriteria:
+    """Pairing thresholds: 30 deg, 1 m, one third overlap (graph.py:41-47)."""
+
+    max_angle: float = math.radians(30.0)
+    max_translation: float = 1.0
+    min_overlap_ratio: float = 1.0 / 3.0
+
+
+@dataclass(frozen=True)
+class Edge:
+    i: int
+    j: int
+    kind: str
+
+    def __post_init__(self) -> None:
+        if self.i >= self.j:
+            raise ValueError("edges are stored with i < j")
+
+
+@dataclass
+class MatchGraph:
+    nodes: list
+    edges: list
+
+    def edge_pairs(self) -> list:
+        return [(e.i, e.j) for e in self.edges]
+
+
+def _source_points(src, stride: int, cache: dict | None):
+    """Valid-pixel count and sensor-frame points of a source image; pose
+    independent, so build_graph computes them once per frame."""
+    key = (id(src), stride)
+    if cache is not None and key in cache:
+        return cache[key]
+    valid = np.asarray(src.depth_valid)[::stride, ::stride]
+    n_valid = int(valid.sum())
+    pts = None
+    if n_valid:
+        h, w = src.shape
+        cols, rows = np.meshgrid(np.arange(0, w, stride, dtype=float),
+                                 np.arange(0, h, stride, dtype=float))
+        uv = np.stack([cols[valid], rows[valid]], axis=-1)
+        pts = unproject(src.intrinsics, uv, np.asarray(src.depth)[::stride, ::stride][valid])
+    if cache is not None:
+        cache[key] = (n_valid, pts, src)
+    return n_valid, pts, src
+
+
+def overlap_ratio(node_i: FrameNode, node_j: FrameNode, level: int = 0, stride: int = 1,
+                  extrinsics: SensorExtrinsics | None = None, _cache: dict | None = None) -> float:
+    """Fraction of i's valid pixels reprojecting validly into j (graph.py:70-101)."""
+    off = (extrinsics or SensorExtrinsics.identity()).offset
+    src = node_i.pyramid.levels[level]
+    dst = node_j.pyramid.levels[level]
+    n_valid, pts, _ = _source_points(src, stride, _cache)
+    if n_valid == 0:
+        return 0.0
+    to_j = node_j.pose_guess.compose(off).inverse().compose(node_i.pose_guess.compose(off))
+    _, ok = project(dst.intrinsics, to_j.transform(pts), bound_slack=1e-6)
+    return float(ok.sum()) / float(n_valid)
+
+
+def _gates_pass(ni: FrameNode, nj: FrameNode, crit: MatchCriteria) -> bool:
+    if rotation_angle(nj.pose_guess.rotation.T @ ni.pose_guess.rotation) > crit.max_angle:
+        return False
+    return not (np.linalg.norm(ni.pose_guess.translation - nj.pose_guess.translation)
+                > crit.max_translation)
+
+
+def _pair_matches(ni, nj, crit, extrinsics, level, stride, cache=None) -> bool:
+    if not _gates_pass(ni, nj, crit):
+        return False
+    kw = dict(level=level, stride=stride, extrinsics=extrinsics, _cache=cache)
+    if overlap_ratio(ni, nj, **kw) < crit.min_overlap_ratio:
+        return False
+    return overlap_ratio(nj, ni, **kw) >= crit.min_overlap_ratio
+
+
+def _prefilter(nodes, crit: MatchCriteria) -> list:
+    """Candidate (a, b) index pairs that are not rejected by a wide margin."""
+    n = len(nodes)
+    t = np.array([np.asarray(nd.pose_guess.translation, float) for nd in nodes])
+    r = np.array([np.asarray(nd.pose_guess.rotation, float) for nd in nodes])
+    out = []
+    slack_t = crit.max_translation * (1.0 + 1e-6) + 1e-9
+    # cos(angle) = (tr(R_b^T R_a) - 1)/2 ; reject only if clearly above max_angle
+    cos_lim = math.cos(min(math.pi, crit.max_angle + 1e-6))
+    for a in range(n - 1):
+        d = np.sqrt(((t[a + 1:] - t[a]) ** 2).sum(axis=1))
+        tr = np.einsum("kij,ij->k", r[a + 1:], r[a])
+        c = 0.5 * (tr - 1.0)
+        keep = np.nonzero((d <= slack_t) & (c >= cos_lim - 1e-9))[0]
+        out.extend((a, a + 1 + int(k)) for k in keep)
+    return out
+
+
+def build_graph(nodes, criteria: MatchCriteria | None = None, sequential: bool = True,
+                extrinsics: SensorExtrinsics | None = None, overlap_level: int = 0,
+                overlap_stride: int = 2, threads: int = 1) -> MatchGraph:
+    """Sorted edge list of covisible pairs plus odometry edges (graph.py:123-176)."""
+    crit = criteria or MatchCriteria()
+    if len(nodes) < 2:
+        raise GraphConfigError(f"need at least 2 frames to build a graph, got {len(nodes)}")
+    ids = [nd.id for nd in nodes]
+    if len(set(ids)) != len(ids):
+        raise GraphConfigError("frame ids must be unique")
+    for a, b in zip(nodes, nodes[1:]):
+        if a.sensor_id == b.sensor_id and b.timestamp < a.timestamp:
+            raise GraphConfigError(
+                f"timestamps must be non-decreasing within a sensor stream "
+                f"(frame {b.id} at {b.timestamp} after {a.timestamp})")
+    candidates = _prefilter(nodes, crit)
+    cache: dict = {}
+    for nd in nodes:  # per-frame source points, shared by every pair of the frame
+        _source_points(nd.pyramid.levels[overlap_level], overlap_stride, cache)
+
+    def check(ab):
+        a, b = ab
+        return _pair_matches(nodes[a], nodes[b], crit, extrinsics, overlap_level, overlap_stride,
+                             cache)
+
+    if threads > 1:
+        with ThreadPoolExecutor(max_workers=threads) as pool:
+            verdicts = list(pool.map(check, candidates))
+    else:
+        verdicts = [check(ab) for ab in candidates]
+    kinds = {(ids[a], ids[b]): COVISIBILITY for (a, b), ok in zip(candidates, verdicts) if ok}
+    if sequential:
+        ordered = sorted(ids)
+        for a, b in zip(ordered, ordered[1:]):
+            kinds.setdefault((min(a, b), max(a, b)), ODOMETRY)
+    return MatchGraph(list(nodes), [Edge(i, j, k) for (i, j), k in sorted(kinds.items())])
+
+
+def dump_edges(graph: MatchGraph) -> str:
+    return "".join(f"{e.i} {e.j} {e.kind}\n" for e in graph.edges)

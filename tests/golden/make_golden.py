@@ -1,0 +1,184 @@
+"""Generate the golden fixtures of tests/test_oracle_golden.py and
+tests/test_gpu_parity.py by running the REFERENCE implementation.
+
+Run in the build container (where /root/reference exists):
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+It imports the read-only reference package from /root/reference/pkg/src and
+its test rigs, renders small scenes with the reference renderer and pyramid
+builder, and stores inputs (cleaned CueImage channels, derived masks, poses,
+edge lists) together with reference outputs:
+  - per-pair _EdgeTerm records (solver.py:343-390) at guess and GT poses
+  - total_error with and without occlusion suppression (solver.py:655-670)
+  - the full LM IterationRecord trace and final poses of solve_hierarchical /
+    solve_fusion (solver.py:585-652)
+  - the sorted edge list of build_graph (graph.py:123-176)
+  - the pyramid index map _footprint_index (cues.py:254-261)
+Nothing under tests/golden is read at GPU run time except the .npz files.
+"""
+import math
+import sys
+from pathlib import Path
+
+REF = Path("/root/reference/pkg")
+sys.path.insert(0, str(REF / "src"))
+sys.path.insert(0, str(REF / "tests"))
+
+import numpy as np  # noqa: E402
+
+from photoba.cues import _footprint_index, build_pyramid  # noqa: E402
+from photoba.geometry import Pose, boxplus  # noqa: E402
+from photoba.graph import FrameNode, MatchCriteria, build_graph  # noqa: E402
+from photoba.sensors import PINHOLE, Intrinsics, SensorExtrinsics  # noqa: E402
+from photoba.solver import (BAProblem, SolverConfig, _edge_term, _LevelProblem,  # noqa: E402
+                            solve_fusion, solve_hierarchical, total_error)
+from photoba.synthetic import box_room_scene, render_view  # noqa: E402
+from rigs import loop_trajectory, seeded_perturbation  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+IU = np.triu_indices(6)
+
+
+def cam_row(c):
+    return np.array([c.fx, c.fy, c.cx, c.cy, c.width, c.height, 0 if c.model == PINHOLE else 1,
+                     c.depth_min, c.depth_max])
+
+
+def pose_rows(poses):
+    return np.stack([np.concatenate([p.rotation.reshape(9), p.translation]) for p in poses])
+
+
+def term_rows(terms):
+    out = np.zeros((len(terms), 92))
+    for k, t in enumerate(terms):
+        out[k, 90] = t.cost
+        out[k, 91] = t.count
+        if t.h_ii is not None:
+            out[k, 0:21] = t.h_ii[IU]
+            out[k, 21:42] = t.h_jj[IU]
+            out[k, 42:78] = t.h_ij.reshape(-1)
+            out[k, 78:84] = t.b_i
+            out[k, 84:90] = t.b_j
+    return out
+
+
+def store_pyramids(d, prefix, pyrs):
+    for f, pyr in enumerate(pyrs):
+        for l, img in enumerate(pyr.levels):
+            d[f"{prefix}I_{f}_{l}"] = img.intensity
+            d[f"{prefix}D_{f}_{l}"] = img.depth
+            d[f"{prefix}N_{f}_{l}"] = img.normals
+            d[f"{prefix}M_{f}_{l}"] = (img.depth_valid.astype(np.uint8)
+                                       | (img.normal_valid.astype(np.uint8) << 1)
+                                       | ((img.sampleable_intensity & img.sampleable_depth).astype(np.uint8) << 2)
+                                       | (img.sampleable_normals.astype(np.uint8) << 3))
+            if f == 0:
+                d[f"{prefix}G_{f}_{l}"] = np.concatenate(
+                    [img.grad_intensity.reshape(-1), img.grad_depth.reshape(-1),
+                     img.grad_normals.reshape(-1)])
+    d[f"{prefix}cams"] = np.stack([cam_row(img.intrinsics) for img in pyrs[0].levels])
+    d[f"{prefix}scales"] = np.array(pyrs[0].scales)
+
+
+def level_terms(prob, level, poses, cfg, problems=None):
+    lp = _LevelProblem(problems or [prob], level, cfg)
+    return term_rows([_edge_term(ctx, i, j, poses[i], poses[j], cfg, tol, True)
+                      for i, j, ctx, tol in lp.contexts])
+
+
+def trace_rows(records):
+    return np.array([[r.level, r.iteration, r.lam, r.error, r.valid_blocks, r.accepted]
+                     for r in records], dtype=float).reshape(-1, 6)
+
+
+def single_sensor_case(name, cam, n, scales, ext_t, seed, sigma_t, sigma_r):
+    gt = loop_trajectory(n).poses
+    ext = SensorExtrinsics(Pose(np.eye(3), ext_t))
+    room = box_room_scene()
+    pyrs = []
+    for p in gt:
+        r = render_view(room, cam, p.compose(ext.offset))
+        pyrs.append(build_pyramid(r.intensity, r.depth, cam, scales))
+    rng = np.random.default_rng(seed)
+    guess = [gt[0]] + [boxplus(p, seeded_perturbation(rng, sigma_t, sigma_r)) for p in gt[1:]]
+    nodes = [FrameNode(k, guess[k], pyrs[k], 0.1 * k) for k in range(n)]
+    graph = build_graph(nodes, extrinsics=ext)
+    prob = BAProblem(graph, {"sensor0": ext})
+    cfg = SolverConfig()
+    d = {}
+    store_pyramids(d, "", pyrs)
+    d["gt"] = pose_rows(gt)
+    d["guess"] = pose_rows(guess)
+    d["ext"] = np.concatenate([ext.offset.rotation.reshape(9), ext.offset.translation])
+    d["edges"] = np.array(graph.edge_pairs(), dtype=np.int64).reshape(-1, 2)
+    d["edge_kinds"] = np.array([e.kind == "covisibility" for e in graph.edges])
+    for l in range(len(scales)):
+        d[f"rec_guess_{l}"] = level_terms(prob, l, guess, cfg)
+        d[f"rec_gt_{l}"] = level_terms(prob, l, gt, cfg)
+        d[f"te_{l}"] = np.array([*total_error(prob, guess, l, cfg),
+                                 *total_error(prob, guess, l, cfg, suppress_occlusions=False)])
+    res = solve_hierarchical(prob, cfg)
+    d["trace"] = trace_rows(res.records)
+    d["final"] = pose_rows(res.poses)
+    np.savez_compressed(OUT / f"{name}.npz", **d)
+    print(name, len(graph.edges), "edges;", len(res.records), "LM records;",
+          (OUT / f"{name}.npz").stat().st_size, "bytes")
+
+
+def fusion_case():
+    from rigs import LIDAR_EXTRINSICS, RGBD_EXTRINSICS
+    rgbd = Intrinsics(40.0, 40.0, 32.0, 24.0, 64, 48, PINHOLE, 0.1, 50.0)
+    lidar = Intrinsics(128 / (2 * math.pi), 32 / (math.pi / 2), 64.0, 16.0, 128, 32, "spherical",
+                       0.2, 80.0)
+    gt = Pose(np.eye(3), [-0.4, -0.2, -0.6])
+    rng = np.random.default_rng(4242)
+    bad = boxplus(gt, seeded_perturbation(rng, 0.05, 0.03))
+    room = box_room_scene()
+    d = {}
+    probs = []
+    for tag, cam, ext in (("r_", rgbd, RGBD_EXTRINSICS), ("l_", lidar, LIDAR_EXTRINSICS)):
+        r = render_view(room, cam, gt.compose(ext.offset))
+        pyr = build_pyramid(r.intensity, r.depth, cam, (0.5, 1.0))
+        store_pyramids(d, tag, [pyr])
+        sid = "rgbd" if tag == "r_" else "lidar"
+        nodes = [FrameNode(0, gt, pyr, 0.0, sid), FrameNode(1, bad, pyr, 0.1, sid)]
+        from photoba.graph import Edge, MatchGraph
+        probs.append(BAProblem(MatchGraph(nodes, [Edge(0, 1, "covisibility")]), {sid: ext}))
+        d[tag + "ext"] = np.concatenate([ext.offset.rotation.reshape(9), ext.offset.translation])
+    d["gt"] = pose_rows([gt, gt])
+    d["guess"] = pose_rows([gt, bad])
+    cfg = SolverConfig()
+    for l in range(2):
+        d[f"rec_guess_{l}"] = level_terms(None, l, [gt, bad], cfg, probs)
+    res = solve_fusion(probs[0], probs[1], "coupled", cfg)
+    d["trace"] = trace_rows(res.records)
+    d["final"] = pose_rows(res.poses)
+    res2 = solve_fusion(probs[1], probs[0], "consecutive", cfg)
+    d["trace_consecutive"] = trace_rows(res2.records)
+    d["final_consecutive"] = pose_rows(res2.poses)
+    np.savez_compressed(OUT / "fusion_small.npz", **d)
+    print("fusion_small", len(res.records), (OUT / "fusion_small.npz").stat().st_size, "bytes")
+
+
+def footprint_case():
+    d = {}
+    for k, (h, w, s) in enumerate([(11, 15, 1 / 3), (460, 740, 0.125), (128, 1024, 0.25),
+                                   (96, 128, 0.5), (57, 93, 0.7), (64, 1024, 1.0)]):
+        idx, keep, oh, ow = _footprint_index(h, w, s)
+        d[f"fp_{k}"] = np.array([h, w, s, oh, ow])
+        # the map is separable: row index of column 0 and column index of row 0
+        d[f"fp_rows_{k}"] = np.where(keep[:, 0], idx[:, 0] // max(ow, 1), -1).astype(np.int32)
+        d[f"fp_cols_{k}"] = np.where(keep[0, :], idx[0, :] % max(ow, 1), -1).astype(np.int32)
+        d[f"fp_sum_{k}"] = np.array([int(idx[keep].sum()), int(keep.sum())])
+    np.savez_compressed(OUT / "footprint.npz", **d)
+
+
+if __name__ == "__main__":
+    pin = Intrinsics(40.0, 40.0, 32.0, 24.0, 64, 48, PINHOLE, 0.1, 50.0)
+    single_sensor_case("pinhole_small", pin, 4, (1.0,), [0.0, 0.0, 0.1], 51, 0.04,
+                       math.radians(1.5))
+    sph = Intrinsics(128 / (2 * math.pi), 24 / (math.pi / 2), 64.0, 12.0, 128, 24, "spherical",
+                     0.2, 80.0)
+    single_sensor_case("spherical_small", sph, 4, (0.5, 1.0), [0.0, 0.0, -0.05], 52, 0.04,
+                       math.radians(1.5))
+    fusion_case()
+    footprint_case()

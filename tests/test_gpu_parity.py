@@ -1,0 +1,312 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the oracle and
+the reference's own golden vectors.  Tolerances are SURVEY.md §8(c):
+per-pair H/b max|Δ|/max|ref| <= 1e-5, cost <= 1e-6 relative, counts equal,
+LM trace equal in (level, iteration, accepted, count, lambda), final poses
+<= 1e-5 rad / 1e-5 m."""
+import math
+
+import numpy as np
+import pytest
+
+import paper_2303_16878_b200 as P
+from oracle import oracle as O
+from tests import fixtures as F
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+CASES = ["pinhole_small", "spherical_small"]
+
+
+def _store():
+    from paper_2303_16878_b200.device import FrameStore
+
+    return FrameStore(torch.device("cuda", 0))
+
+
+def _level(problems, level, cfg=None, **kw):
+    from paper_2303_16878_b200.device import DeviceLevel
+
+    return DeviceLevel(problems, level, cfg or P.SolverConfig(), _store(), **kw)
+
+
+def _rows(arr):
+    return torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).cuda()
+
+
+def _pose_err(a_rows, b_rows):
+    worst_r = worst_t = 0.0
+    for a, b in zip(a_rows, b_rows):
+        Ra, Rb = a[:9].reshape(3, 3), b[:9].reshape(3, 3)
+        worst_r = max(worst_r, P.rotation_angle(Rb.T @ Ra))
+        worst_t = max(worst_t, float(np.linalg.norm(a[9:] - b[9:])))
+    return worst_r, worst_t
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_device_texels_bit_exact_masks_and_gradients(name):
+    d = F.load(name)
+    store = _store()
+    for f, pyr in enumerate(F.pyramids(d)):
+        for l, img in enumerate(pyr.levels):
+            tex, mask, _, _ = store.frame(img)
+            torch.cuda.synchronize()
+            m = mask.cpu().numpy().reshape(img.shape)
+            assert np.array_equal(m, d[f"M_{f}_{l}"])
+            t = tex.cpu().numpy().view(np.float64).reshape(img.shape[0], img.shape[1], 16)
+            assert np.array_equal(t[..., 0], img.intensity)
+            assert np.array_equal(t[..., 1], img.depth)
+            assert np.array_equal(t[..., 2:5], img.normals)
+            if f == 0:
+                g = np.concatenate([t[..., 5:7].reshape(-1), t[..., 7:9].reshape(-1),
+                                    t[..., 9:15].reshape(-1)])
+                assert np.array_equal(g, d[f"G_{f}_{l}"])
+
+
+@pytest.mark.parametrize("name", CASES)
+@pytest.mark.parametrize("which", ["guess", "gt"])
+def test_linearize_matches_reference_records(name, which):
+    d = F.load(name)
+    prob, _ = F.single_problem(d)
+    for l in range(len(d["scales"])):
+        lv = _level([prob], l)
+        recs = lv.linearize(_rows(d[which])).cpu().numpy()
+        F.compare_records(recs, d[f"rec_{which}_{l}"])
+        # and against the oracle on the same inputs
+        ol = O.OracleLevel([prob], l, P.SolverConfig())
+        F.compare_records(recs, ol.records(d[which]))
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_total_error_matches_reference(name):
+    d = F.load(name)
+    prob, _ = F.single_problem(d)
+    guess = F.poses(d["guess"])
+    for l in range(len(d["scales"])):
+        c1, n1, c2, n2 = d[f"te_{l}"]
+        cost, count = P.total_error(prob, guess, l)
+        assert count == int(n1) and abs(cost - c1) <= 1e-6 * c1
+        cost, count = P.total_error(prob, guess, l, suppress_occlusions=False)
+        assert count == int(n2) and abs(cost - c2) <= 1e-6 * c2
+
+
+def _check_trace(records, trace, err_tol=1e-6):
+    assert len(records) == len(trace), (len(records), len(trace))
+    for r, t in zip(records, trace):
+        assert (r.level, r.iteration, int(r.accepted), r.valid_blocks) == (
+            int(t[0]), int(t[1]), int(t[5]), int(t[4]))
+        assert r.lam == t[2]
+        assert abs(r.error - t[3]) <= err_tol * abs(t[3])
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_solve_hierarchical_matches_reference_trace(name):
+    d = F.load(name)
+    prob, _ = F.single_problem(d)
+    res = P.solve_hierarchical(prob)
+    _check_trace(res.records, d["trace"])
+    final = np.stack([p.as_row() for p in res.poses])
+    er, et = _pose_err(final, d["final"])
+    assert er <= 1e-5 and et <= 1e-5
+
+
+def test_fusion_matches_reference():
+    d = F.load("fusion_small")
+    probs = F.fusion_problems(d)
+    for l in range(2):
+        lv = _level(probs, l)
+        F.compare_records(lv.linearize(_rows(d["guess"])).cpu().numpy(), d[f"rec_guess_{l}"])
+    res = P.solve_fusion(probs[0], probs[1], "coupled")
+    _check_trace(res.records, d["trace"])
+    er, et = _pose_err(np.stack([p.as_row() for p in res.poses]), d["final"])
+    assert er <= 1e-5 and et <= 1e-5
+    res2 = P.solve_fusion(probs[1], probs[0], "consecutive")
+    _check_trace(res2.records, d["trace_consecutive"])
+    er, et = _pose_err(np.stack([p.as_row() for p in res2.poses]), d["final_consecutive"])
+    assert er <= 1e-5 and et <= 1e-5
+
+
+# ---------------------------------------------------------------------------
+# larger synthetic problems against the oracle (BASELINE config 1 shape etc.)
+# ---------------------------------------------------------------------------
+def _room_problem(n=10, cam=None, scales=(1.0,), seed=11):
+    from paper_2303_16878_b200 import scenes as S
+
+    cam = cam or S.rgbd_160()
+    gt = S.room_loop(n)
+    pyrs = S.host_pyramids(S.BoxScene(), cam, gt, P.Pose.identity(), scales)
+    guess = S.perturb(gt, 0.05, math.radians(2.0), seed)
+    nodes = [P.FrameNode(k, guess[k], pyrs[k], 0.1 * k) for k in range(n)]
+    return P.BAProblem(P.build_graph(nodes)), gt, guess
+
+
+def test_config1_linearize_matches_oracle():
+    prob, gt, guess = _room_problem()
+    assert len(prob.graph.edges) == 24
+    rows, _ = P.se3.pose_rows(guess)
+    lv = _level([prob], 0)
+    got = lv.linearize(_rows(rows)).cpu().numpy()
+    ref = O.OracleLevel([prob], 0, P.SolverConfig()).records(rows)
+    F.compare_records(got, ref)
+    assert int(got[:, 91].sum()) > 0.8 * 24 * 160 * 120 * 0.5
+
+
+def test_config1_lm_trace_matches_oracle():
+    prob, gt, guess = _room_problem()
+    res = P.solve_hierarchical(prob)
+    final_o, recs_o = O.hierarchical([prob], P.SolverConfig())
+    assert [(r.level, r.iteration, r.accepted, r.valid_blocks) for r in res.records] == [
+        (r.level, r.iteration, r.accepted, r.valid_blocks) for r in recs_o]
+    assert [r.lam for r in res.records] == [r.lam for r in recs_o]
+    for a, b in zip(res.records, recs_o):
+        assert abs(a.error - b.error) <= 1e-6 * b.error
+    er, et = _pose_err(np.stack([p.as_row() for p in res.poses]), final_o)
+    assert er <= 1e-5 and et <= 1e-5
+
+
+def test_spherical_corridor_linearize_matches_oracle():
+    from paper_2303_16878_b200 import scenes as S
+
+    cam = S.hdl64(512, 64)
+    gt = S.corridor_trajectory(6, 0.5)
+    ext = P.Pose.identity()
+    pyrs = S.host_pyramids(S.corridor_scene(23.0), cam, gt, ext, (0.25, 0.5, 1.0))
+    guess = S.perturb(gt, 0.05, math.radians(2.0), 11)
+    nodes = [P.FrameNode(k, guess[k], pyrs[k], 0.1 * k) for k in range(len(gt))]
+    prob = P.BAProblem(P.build_graph(nodes))
+    rows, _ = P.se3.pose_rows(guess)
+    for l in range(3):
+        got = _level([prob], l).linearize(_rows(rows)).cpu().numpy()
+        ref = O.OracleLevel([prob], l, P.SolverConfig()).records(rows)
+        F.compare_records(got, ref)
+
+
+def test_pixel_stride_and_cost_only_path():
+    prob, gt, guess = _room_problem(n=5, scales=(0.5, 1.0))
+    rows, _ = P.se3.pose_rows(guess)
+    cfg = P.SolverConfig(pixel_stride=3)
+    got = _level([prob], 1, cfg).linearize(_rows(rows)).cpu().numpy()
+    ref = O.OracleLevel([prob], 1, cfg).records(rows)
+    F.compare_records(got, ref)
+    got = _level([prob], 1, cfg).linearize(_rows(rows), want_jacobians=False).cpu().numpy()
+    ref = O.OracleLevel([prob], 1, cfg).records(rows, want_jacobians=False)
+    assert np.array_equal(got[:, 91], ref[:, 91])
+    assert np.allclose(got[:, 90], ref[:, 90], rtol=1e-9)
+    assert np.all(got[:, :90] == 0.0)
+
+
+def test_deterministic_and_shard_independent():
+    prob, gt, guess = _room_problem()
+    rows, _ = P.se3.pose_rows(guess)
+    full = _level([prob], 0).linearize(_rows(rows)).cpu().numpy()
+    again = _level([prob], 0).linearize(_rows(rows)).cpu().numpy()
+    assert np.array_equal(full, again)
+    parts = [_level([prob], 0, pair_range=r, assemble=False).linearize(_rows(rows)).cpu().numpy()
+             for r in [(0, 7), (7, 15), (15, 24)]]
+    assert np.array_equal(np.concatenate(parts), full)
+
+
+def test_selfalign_gradient_zero_and_identity_solve():
+    d = F.load("pinhole_small")
+    pyr = F.pyramids(d)[0]
+    gt = P.Pose(np.eye(3), [-0.4, 0.2, -0.5])
+    nodes = [P.FrameNode(0, gt, pyr, 0.0), P.FrameNode(1, gt, pyr, 0.1)]
+    prob = P.BAProblem(P.MatchGraph(nodes, [P.Edge(0, 1, P.COVISIBILITY)]))
+    lv = _level([prob], 0)
+    rows, _ = P.se3.pose_rows([gt, gt])
+    rec = lv.linearize(_rows(rows)).cpu().numpy()
+    assert np.max(np.abs(rec[0, 78:90])) < 1e-10
+    res = P.solve_hierarchical(prob)
+    assert np.allclose(res.poses[1].matrix(), gt.matrix(), atol=1e-9)
+
+
+def test_under_constrained_raises():
+    prob, gt, guess = _room_problem(n=4)
+    prob.graph.edges = [e for e in prob.graph.edges if 3 not in (e.i, e.j)]
+    with pytest.raises(P.UnderConstrainedError):
+        P.solve_hierarchical(prob)
+
+
+# ---------------------------------------------------------------------------
+# K3 / K4 kernels in isolation
+# ---------------------------------------------------------------------------
+def _dense_solve(H, b, lam):
+    from paper_2303_16878_b200 import native as N
+
+    lib = N.load()
+    dim = H.shape[0]
+    Ht, bt = _rows(H), _rows(b)
+    work = torch.empty(int(lib.pba_solve_work_bytes(dim)), dtype=torch.uint8, device="cuda")
+    delta = torch.zeros(dim, dtype=torch.float64, device="cuda")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    N.check(lib.pba_solve_dense(Ht.data_ptr(), bt.data_ptr(), dim, lam, work.data_ptr(),
+                                delta.data_ptr(), status.data_ptr(),
+                                torch.cuda.current_stream().cuda_stream), "solve")
+    return delta.cpu().numpy(), int(status.item())
+
+
+@pytest.mark.parametrize("dim,band", [(54, None), (130, None), (594, None), (600, 40), (1998, 126)])
+def test_dense_cholesky_matches_numpy_solve(dim, band):
+    rng = np.random.default_rng(dim)
+    A = rng.normal(size=(dim, dim))
+    if band is not None:
+        A = np.triu(np.tril(A, band), -band)
+    H = A @ A.T + 1e-3 * np.eye(dim)
+    b = rng.normal(size=dim)
+    lam = 1e-3
+    x, st = _dense_solve(H, b, lam)
+    assert st == 0
+    ref = np.linalg.solve(H + lam * np.diag(np.diag(H)), -b)
+    assert np.max(np.abs(x - ref)) <= 1e-8 * np.max(np.abs(ref))
+
+
+def test_dense_cholesky_reports_singular():
+    H = np.eye(12)
+    H[5, 5] = 0.0
+    _, st = _dense_solve(H, np.ones(12), 1e-3)
+    assert st == 1
+
+
+def test_apply_step_matches_host_boxplus():
+    from paper_2303_16878_b200 import native as N
+
+    lib = N.load()
+    rng = np.random.default_rng(5)
+    n, gauge = 7, 2
+    poses = [P.exp(P.PerturbationVector(rng.uniform(-1, 1, 3), rng.uniform(-0.3, 0.3, 3)))
+             for _ in range(n)]
+    rows, gens = P.se3.pose_rows(poses)
+    gens[4] = 999
+    delta = rng.uniform(-0.1, 0.1, 6 * (n - 1))
+    out = torch.zeros((n, 12), dtype=torch.float64, device="cuda")
+    gout = torch.zeros(n, dtype=torch.int32, device="cuda")
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    gin = torch.from_numpy(gens).cuda()
+    N.check(lib.pba_apply_step(_rows(rows).data_ptr(), gin.data_ptr(), _rows(delta).data_ptr(), n,
+                               gauge, out.data_ptr(), gout.data_ptr(), st.data_ptr(),
+                               torch.cuda.current_stream().cuda_stream), "apply")
+    got, g = out.cpu().numpy(), gout.cpu().numpy()
+    assert st.item() == 0
+    s = 0
+    for k in range(n):
+        if k == gauge:
+            assert np.array_equal(got[k], rows[k]) and g[k] == gens[k]
+            continue
+        ref = P.boxplus(P.Pose(poses[k].rotation, poses[k].translation, int(gens[k])),
+                        P.PerturbationVector.from_vector(delta[6 * s:6 * s + 6]))
+        assert np.allclose(got[k], ref.as_row(), atol=1e-14, rtol=0)
+        assert g[k] == ref.generation
+        s += 1
+    bad = delta.copy()
+    bad[3:6] = [0.8, 0.6, 0.1]
+    N.check(lib.pba_apply_step(_rows(rows).data_ptr(), gin.data_ptr(), _rows(bad).data_ptr(), n,
+                               gauge, out.data_ptr(), gout.data_ptr(), st.data_ptr(),
+                               torch.cuda.current_stream().cuda_stream), "apply")
+    assert st.item() == 1
+
+
+def test_smoke_entry():
+    import __graft_entry__
+
+    __graft_entry__.smoke()

@@ -1,0 +1,191 @@
+"""Host-side logic (CPU): drop-in types vs reference semantics, bit-exact
+pair lists and pyramid indices, and the C ABI library surface."""
+import ctypes
+import math
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2303_16878_b200 as P
+from paper_2303_16878_b200 import native
+from oracle import oracle as O
+from tests import fixtures as F
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+@pytest.mark.parametrize("name", ["pinhole_small", "spherical_small"])
+def test_cueimage_derivation_bit_exact(name):
+    d = F.load(name)
+    pyrs = F.pyramids(d)
+    for f, pyr in enumerate(pyrs):
+        for l, img in enumerate(pyr.levels):
+            assert np.array_equal(F.mask_bits(img), d[f"M_{f}_{l}"])
+            if f == 0:
+                g = np.concatenate([img.grad_intensity.reshape(-1), img.grad_depth.reshape(-1),
+                                    img.grad_normals.reshape(-1)])
+                assert np.array_equal(g, d[f"G_{f}_{l}"])
+
+
+def test_footprint_index_bit_exact():
+    d = F.load("footprint")
+    k = 0
+    while f"fp_{k}" in d:
+        h, w, s, oh, ow = d[f"fp_{k}"]
+        idx, keep, out_h, out_w = P.footprint_index(int(h), int(w), float(s))
+        assert (out_h, out_w) == (int(oh), int(ow))
+        rows = np.where(keep[:, 0], idx[:, 0] // max(out_w, 1), -1)
+        cols = np.where(keep[0, :], idx[0, :] % max(out_w, 1), -1)
+        assert np.array_equal(rows, d[f"fp_rows_{k}"])
+        assert np.array_equal(cols, d[f"fp_cols_{k}"])
+        assert [int(idx[keep].sum()), int(keep.sum())] == list(d[f"fp_sum_{k}"])
+        k += 1
+
+
+@pytest.mark.parametrize("name", ["pinhole_small", "spherical_small"])
+def test_build_graph_matches_reference_edge_list(name):
+    d = F.load(name)
+    pyrs = F.pyramids(d)
+    guess = F.poses(d["guess"])
+    nodes = [P.FrameNode(k, guess[k], pyrs[k], 0.1 * k) for k in range(len(pyrs))]
+    ext = P.SensorExtrinsics(P.Pose.from_row(d["ext"]))
+    g = P.build_graph(nodes, extrinsics=ext)
+    assert [(e.i, e.j) for e in g.edges] == [tuple(map(int, e)) for e in d["edges"]]
+    assert [e.kind == P.COVISIBILITY for e in g.edges] == list(d["edge_kinds"])
+    g2 = P.build_graph(nodes, extrinsics=ext, threads=4)
+    assert g2.edges == g.edges
+
+
+def test_build_graph_validation():
+    cam = P.Intrinsics(20, 20, 8, 6, 16, 12, P.PINHOLE, 0.1, 10.0)
+    img = P.CueImage(np.full((12, 16), 0.5), np.full((12, 16), 2.0), np.zeros((12, 16, 3)), cam)
+    pyr = P.CuePyramid((img,), (1.0,))
+    n0 = P.FrameNode(0, P.Pose.identity(), pyr, 0.0)
+    with pytest.raises(P.GraphConfigError):
+        P.build_graph([n0])
+    with pytest.raises(P.GraphConfigError):
+        P.build_graph([n0, P.FrameNode(0, P.Pose.identity(), pyr, 0.1)])
+    with pytest.raises(P.GraphConfigError):
+        P.build_graph([n0, P.FrameNode(1, P.Pose.identity(), pyr, -1.0)])
+
+
+def test_boxplus_matches_oracle_and_sign_convention():
+    rng = np.random.default_rng(3)
+    for _ in range(50):
+        x = P.exp(P.PerturbationVector(rng.uniform(-1, 1, 3), rng.uniform(-0.3, 0.3, 3)))
+        v = np.concatenate([rng.uniform(-0.2, 0.2, 3), rng.uniform(-0.2, 0.2, 3)])
+        y = P.boxplus(x, P.PerturbationVector.from_vector(v))
+        R2, t2, g2 = O.boxplus(x.rotation, x.translation, x.generation, v)
+        assert np.array_equal(y.rotation, R2) and np.array_equal(y.translation, t2)
+        assert y.generation == g2 == 1
+    # d(exp(v) p)/d v_rot = -2 [p]x at v = 0 (Hamilton; reference test_geometry.py:183-197)
+    p = np.array([0.3, -1.2, 2.0])
+    h = 1e-7
+    jac = np.zeros((3, 3))
+    for k in range(3):
+        e = np.zeros(3); e[k] = h
+        jac[:, k] = (P.exp(P.PerturbationVector(np.zeros(3), e)).transform(p)
+                     - P.exp(P.PerturbationVector(np.zeros(3), -e)).transform(p)) / (2 * h)
+    assert np.allclose(jac, -2.0 * P.skew(p), atol=1e-6)
+    with pytest.raises(P.InvalidPerturbationError):
+        P.exp(P.PerturbationVector(np.zeros(3), [0.8, 0.6, 0.1]))
+
+
+def test_reorthonormalisation_after_1000_compositions():
+    x = P.Pose.identity()
+    v = P.PerturbationVector([0.001, 0, 0], [0.001, 0.002, -0.001])
+    for _ in range(999):
+        x = P.boxplus(x, v)
+    assert x.generation == 999
+    x = P.boxplus(x, v)
+    assert x.generation == 0
+    assert np.allclose(x.rotation @ x.rotation.T, np.eye(3), atol=1e-15)
+
+
+def test_intrinsics_scaled_half_pixel_rule():
+    cam = P.Intrinsics(400.0, 400.0, 370.0, 230.0, 740, 460, P.PINHOLE, 0.1, 50.0)
+    dims = [(cam.scaled(s).height, cam.scaled(s).width) for s in (0.125, 0.25, 0.5)]
+    assert dims == [(57, 92), (115, 185), (230, 370)]
+    s = 0.25
+    assert cam.scaled(s).cx == 370.0 * s + (s - 1) / 2
+
+
+def test_solver_config_validation_and_defaults():
+    cfg = P.SolverConfig()
+    assert list(cfg.omega_diagonal()) == [1.0, 10.0, 1.0, 1.0, 1.0]
+    with pytest.raises(ValueError):
+        P.SolverConfig(huber_delta_depth=0.0)
+    with pytest.raises(ValueError):
+        P.SolverConfig(termination_rel_decrease=1.0)
+    with pytest.raises(ValueError):
+        P.SolverConfig(pixel_stride=0)
+
+
+def test_check_connectivity_names_stranded_pose():
+    d = F.load("pinhole_small")
+    prob, _ = F.single_problem(d)
+    prob.graph.edges = [e for e in prob.graph.edges if 3 not in (e.i, e.j)]
+    with pytest.raises(P.UnderConstrainedError, match="3"):
+        P.check_connectivity([prob])
+
+
+def _header_functions():
+    text = (ROOT / "include" / "pba.h").read_text()
+    return sorted(set(re.findall(r"\b(pba_[a-z_]+)\s*\(", text)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = native.load()
+    names = _header_functions()
+    assert set(names) == set(native.EXPORTED)
+    for name in names:
+        assert hasattr(lib, name), name
+    assert lib.pba_texel_bytes() == 128
+    assert b"sm_100a" in lib.pba_version()
+
+
+def test_host_planning_functions():
+    lib = native.load()
+    cam = native.Camera(0, 160, 120, 0, 70.0, 70.0, 80.0, 60.0, 0.1, 50.0)
+    pairs = (native.Pair * 2)(native.Pair(0, 1, 0, 1, 0, 0, 0.05), native.Pair(1, 2, 1, 2, 0, 0, 0.05))
+    cams = (native.Camera * 2)(cam, cam)
+    n = ctypes.c_int64(0)
+    assert lib.pba_plan_chunks(pairs, 2, cams, 1, 4096, None, None, ctypes.byref(n)) == 0
+    assert n.value == 2 * math.ceil(19200 / 4096) and pairs[0].n_chunks == 5
+    tab = np.zeros(2 * n.value, np.int32)
+    off = np.zeros(3, np.int32)
+    assert lib.pba_plan_chunks(pairs, 2, cams, 3, 1024, tab.ctypes.data, off.ctypes.data,
+                               ctypes.byref(n)) == 0
+    assert off[-1] == n.value == 2 * math.ceil(54 * 40 / 1024)
+    # assembly plan: gauge 0, edges (0,1),(1,2),(0,2)
+    slot = np.array([-1, 0, 1], np.int32)
+    pi = np.array([0, 1, 0], np.int32)
+    pj = np.array([1, 2, 2], np.int32)
+    n_off = ctypes.c_int32(0)
+    assert lib.pba_plan_assembly(slot.ctypes.data, 3, pi.ctypes.data, pj.ctypes.data, 3,
+                                 None, None, None, None, None, ctypes.byref(n_off)) == 0
+    assert n_off.value == 1
+    dp = np.zeros(3, np.int32); di = np.zeros(6, np.int32)
+    op = np.zeros(2, np.int32); orc = np.zeros(2, np.int32); oi = np.zeros(3, np.int32)
+    assert lib.pba_plan_assembly(slot.ctypes.data, 3, pi.ctypes.data, pj.ctypes.data, 3,
+                                 dp.ctypes.data, di.ctypes.data, op.ctypes.data, orc.ctypes.data,
+                                 oi.ctypes.data, ctypes.byref(n_off)) == 0
+    # slot 0 (pose 1): edge0 side j, edge1 side i ; slot 1 (pose 2): edge1 j, edge2 j
+    assert list(dp) == [0, 2, 4]
+    assert list(di[:4]) == [(0 << 1) | 1, (1 << 1) | 0, (1 << 1) | 1, (2 << 1) | 1]
+    assert list(orc) == [0, 1] and list(oi[:1]) == [(1 << 1) | 0]
+    assert lib.pba_plan_chunks(pairs, 2, cams, 0, 1024, None, None, ctypes.byref(n)) == 1
+    assert b"stride" in lib.pba_last_error()
+
+
+def test_shard_ranges_balanced_and_contiguous():
+    from paper_2303_16878_b200.distributed import shard_ranges
+
+    px = [100, 100, 50, 50, 200, 100, 100, 100]
+    for world in (1, 2, 3, 4, 8):
+        rs = shard_ranges(px, world)
+        assert rs[0][0] == 0 and rs[-1][1] == len(px)
+        assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+    assert shard_ranges(px, 2) == [(0, 4), (4, 8)]
