@@ -15,12 +15,14 @@ constexpr int kRec = PBA_RECORD_DOUBLES;
 // validity bits, 128 B = one L2 line, so the four bilinear corners of a
 // destination sample are four aligned lines.  Field order follows the
 // reference channels [intensity, depth, nx, ny, nz] (solver.py:340) and the
-// gradient order [d/dcol, d/drow] (cues.py:63-71).
+// gradient order [d/dcol, d/drow] (cues.py:63-71); every (col,row) gradient
+// pair and the (I,D), (nx,ny) value pairs sit on 16-byte boundaries so they
+// load as one 128-bit access.
 struct __align__(16) Texel {
   double v[5];   // I, D, nx, ny, nz                                   0..39
-  double g[10];  // gI(c,r), gD(c,r), gnx(c,r), gny(c,r), gnz(c,r)   40..119
-  uint32_t mask; // PBA_MASK_*                                         120
-  uint32_t pad;  //                                                    124
+  uint32_t mask; // PBA_MASK_*                                         40
+  uint32_t pad;  //                                                    44
+  double g[10];  // gI(c,r), gD(c,r), gnx(c,r), gny(c,r), gnz(c,r)   48..127
 };
 static_assert(sizeof(Texel) == 128, "texel must be one 128-byte line");
 

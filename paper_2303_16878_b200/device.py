@@ -77,7 +77,7 @@ class FrameStore:
                     cue.device_normals.to(self.device, torch.float64).contiguous())
         out = []
         for a in (cue.intensity, cue.depth, cue.normals):
-            h = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
+            h = torch.from_numpy(np.array(a, dtype=np.float64, copy=True))
             out.append(h.to(self.device, non_blocking=False))
         return tuple(out)
 

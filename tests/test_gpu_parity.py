@@ -59,8 +59,8 @@ def test_device_texels_bit_exact_masks_and_gradients(name):
             assert np.array_equal(t[..., 1], img.depth)
             assert np.array_equal(t[..., 2:5], img.normals)
             if f == 0:
-                g = np.concatenate([t[..., 5:7].reshape(-1), t[..., 7:9].reshape(-1),
-                                    t[..., 9:15].reshape(-1)])
+                g = np.concatenate([t[..., 6:8].reshape(-1), t[..., 8:10].reshape(-1),
+                                    t[..., 10:16].reshape(-1)])
                 assert np.array_equal(g, d[f"G_{f}_{l}"])
 
 
