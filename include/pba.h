@@ -60,6 +60,11 @@ extern "C" {
 #define PBA_REC_COST 90
 #define PBA_REC_COUNT 91
 
+/* Per-chunk partial sums written by pba_linearize (scratch for the caller
+ * to allocate): Q = sum w q q^T (21, upper), beta = sum q w e (6), cost,
+ * count, 3 pad — see csrc/linearize.cu for the q-basis. */
+#define PBA_PARTIAL_DOUBLES 32
+
 /* Texel mask bits (also stored in the separate per-pixel mask plane). */
 #define PBA_MASK_DEPTH_VALID 1u   /* CueImage.depth_valid        (cues.py:117)     */
 #define PBA_MASK_NORMAL_VALID 2u  /* CueImage.normal_valid       (cues.py:120)     */
@@ -140,7 +145,7 @@ int pba_plan_chunks(pba_pair* pairs, int32_t n_pairs, const pba_camera* src_cams
                     int32_t* pair_chunk_offsets, int64_t* n_chunks_out);
 
 /* frames, pairs, chunk_table, pair_chunk_offsets, poses (n_poses x 12),
- * extrinsics (n_ext x 12), partials (n_chunks x 92) and records
+ * extrinsics (n_ext x 12), partials (n_chunks x PBA_PARTIAL_DOUBLES) and records
  * (n_pairs x 92) are device pointers; cfg is a host pointer.
  * want_jacobians = 0 is the cost-only path of total_error
  * (solver.py:655-670): ok_jac is not applied and only cost/count are

@@ -8,20 +8,33 @@
 //   robust_cue_weights    solver.py:317-337
 //   _edge_term            solver.py:356-390  (block sums)
 //
+// Structure exploited.  The reference builds, per pixel and cue channel c,
+// J_i = v_c^T a_i (+ normal-cue rotation terms) and J_j = v_c^T a_j (+ ...),
+// with a_i = M_i [I | -2[p_u]x], a_j = [-R_o^T | 2 R_o^T [g]x]
+// (solver.py:265-293).  Because M_i = R_o^T R_j^T R_i and A = R_j^T R_i are
+// rotations and g = A p_u + t_g (t_g = R_j^T (t_i - t_j)), both rows are
+// fixed linear maps of ONE 6-vector per channel,
+//     q_c = [u; r],  u = M_i^T v_c,  r = u x p_u (+ m_k x R_o n for normal k),
+//     J_i = D q_c,   J_j = L q_c,   D = diag(1,1,1,-2,-2,-2),
+//     L = [[-A, 0], [-2 [t_g]x A, 2A]],
+// (the normal-cue terms fold in because A (m_k x n) = (R_o e_k) x (A n)).
+// So a pixel only adds ww q q^T (21 numbers) and q ww e (6) to per-thread
+// sums, and the per-pair finalisation forms H_ii = D Q D, H_jj = L Q L^T,
+// H_ij = D Q L^T, b_i = D beta, b_j = L beta once.  That cuts the per-pixel
+// accumulation from 78+12 to 21+6 fp64 FMAs per channel-row and the live
+// accumulators from 92 to 29, which lets everything — geometry, cue values,
+// residuals, Huber weights, Jacobians and the sums — stay in fp64 (SURVEY.md
+// App. B; fp32 H partials measurably broke the 1e-6 LM-cost parity).
+//
 // Work decomposition: one CTA per chunk of `chunk_pixels` consecutive source
 // pixels of one pair (row-major over the strided source grid).  A thread
 // walks pixels tid, tid+256, ... so a warp reads 32 consecutive source
-// texels and samples a compact destination footprint.  Per-thread sums
-// live in registers (H in fp32, b/cost in fp64), are reduced by a fixed
-// warp-shuffle tree and a fixed cross-warp order into one 92-double partial
-// per chunk; a second kernel sums the chunk partials of each pair in chunk
-// order.  No atomics: results are bit-identical run to run and independent
-// of how pairs are spread over GPUs.
-//
-// Precision: geometry, cue values, residuals, Huber
-// weights, Jacobians, b and cost in fp64; only the H outer products are
-// accumulated in fp32 per thread (<= chunk_pixels/256 terms) before being
-// promoted to fp64 in the reductions.
+// texels and samples a compact destination footprint.  Per-thread sums are
+// reduced by a fixed warp-shuffle tree and a fixed cross-warp order into one
+// 32-double partial per chunk; a finalisation kernel sums the chunk partials
+// of each pair in chunk order and expands them into the 92-double record.
+// No atomics: results are bit-identical run to run and independent of how
+// pairs are spread over GPUs.
 
 #include <math.h>
 
@@ -32,7 +45,8 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kH = 78;  // 21 + 21 + 36 fp32 accumulators
+constexpr int kQ = 21;    // upper triangle of Q (6x6)
+constexpr int kPart = 32; // chunk partial: Q[21], beta[6], cost, count, pad
 
 struct PairSetup {
   double Ri[9], Rj[9], Ro[9];
@@ -124,37 +138,7 @@ __device__ __forceinline__ void cross3(const double* a, const double* b, double*
   c[2] = a[0] * b[1] - a[1] * b[0];
 }
 
-template <int K, int L>
-struct Upper {
-  static constexpr int idx = K * 6 - (K * (K - 1)) / 2 + (L - K);
-};
-
 __device__ __forceinline__ int upper_idx(int k, int l) { return k * 6 - (k * (k - 1)) / 2 + (l - k); }
-
-// Rank-1 updates of the three blocks with one channel's Jacobian rows.
-__device__ __forceinline__ void accumulate_h(float* h, const double* Ji, const double* Jj,
-                                             double ww) {
-  float fi[6], fj[6], ai[6], aj[6];
-  const float wf = (float)ww;
-#pragma unroll
-  for (int k = 0; k < 6; ++k) {
-    fi[k] = (float)Ji[k];
-    fj[k] = (float)Jj[k];
-    ai[k] = wf * fi[k];
-    aj[k] = wf * fj[k];
-  }
-#pragma unroll
-  for (int k = 0; k < 6; ++k)
-#pragma unroll
-    for (int l = k; l < 6; ++l) {
-      h[upper_idx(k, l)] = fmaf(ai[k], fi[l], h[upper_idx(k, l)]);
-      h[21 + upper_idx(k, l)] = fmaf(aj[k], fj[l], h[21 + upper_idx(k, l)]);
-    }
-#pragma unroll
-  for (int k = 0; k < 6; ++k)
-#pragma unroll
-    for (int l = 0; l < 6; ++l) h[42 + 6 * k + l] = fmaf(ai[k], fj[l], h[42 + 6 * k + l]);
-}
 
 template <bool kJac>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -163,7 +147,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                      const double* __restrict__ poses, const double* __restrict__ exts,
                      pba_config cfg, double* __restrict__ partials) {
   __shared__ PairSetup S;
-  __shared__ double red[kWarps][kRec];
+  __shared__ double red[kWarps][kPart];
 
   const long chunk = blockIdx.x;
   const int pair = chunk_table[2 * chunk];
@@ -171,12 +155,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) build_setup(S, frames, pairs[pair], poses, exts, cfg.pixel_stride);
   __syncthreads();
 
-  float h[kH];
+  double Q[kQ];
 #pragma unroll
-  for (int k = 0; k < kH; ++k) h[k] = 0.f;
-  double bi[6], bj[6];
+  for (int k = 0; k < kQ; ++k) Q[k] = 0.0;
+  double beta[6];
 #pragma unroll
-  for (int k = 0; k < 6; ++k) bi[k] = bj[k] = 0.0;
+  for (int k = 0; k < 6; ++k) beta[k] = 0.0;
   double cost = 0.0;
   int count = 0;
 
@@ -198,8 +182,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---- source cue values and unprojection (sensors.py:133-154) ----
     const double2* st = reinterpret_cast<const double2*>(S.src_tex + sp);
     const double2 s_id = __ldg(st + 0);   // I, D
-    const double2 s_n01 = __ldg(st + 1);  // nx, ny
-    const double s_n2 = __ldg(&S.src_tex[sp].v[4]);
     const double d = s_id.y;
     double ps[3];
     if (src_sph) {
@@ -219,13 +201,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int k = 0; k < 3; ++k)
       pu[k] = S.Ro[3 * k + 0] * ps[0] + S.Ro[3 * k + 1] * ps[1] + S.Ro[3 * k + 2] * ps[2] + S.to[k];
     // g = R_j^T (R_i p_u + t_i - t_j);  p_bar = R_o^T (g - t_o)   (solver.py:235-236)
-    double q[3], g[3], pb[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k)
-      q[k] = S.Ri[3 * k + 0] * pu[0] + S.Ri[3 * k + 1] * pu[1] + S.Ri[3 * k + 2] * pu[2] + S.dt[k];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) g[k] = q[0] * S.Rj[k] + q[1] * S.Rj[3 + k] + q[2] * S.Rj[6 + k];
+    double pb[3];
     {
+      double qv[3], g[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        qv[k] = S.Ri[3 * k + 0] * pu[0] + S.Ri[3 * k + 1] * pu[1] + S.Ri[3 * k + 2] * pu[2] + S.dt[k];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) g[k] = qv[0] * S.Rj[k] + qv[1] * S.Rj[3 + k] + qv[2] * S.Rj[6 + k];
       const double a0 = g[0] - S.to[0], a1 = g[1] - S.to[1], a2 = g[2] - S.to[2];
 #pragma unroll
       for (int k = 0; k < 3; ++k) pb[k] = a0 * S.Ro[k] + a1 * S.Ro[3 + k] + a2 * S.Ro[6 + k];
@@ -282,8 +265,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const bool normal_on = (mk & PBA_MASK_SAMP_NORMAL) && (sm & PBA_MASK_NORMAL_VALID);
     double e2 = 0.0, e3 = 0.0, e4 = 0.0;
-    const double ns[3] = {s_n01.x, s_n01.y, s_n2};
+    double ns[3] = {0.0, 0.0, 0.0};
     if (normal_on) {
+      const double2 s_n01 = __ldg(st + 1);  // source nx, ny
+      ns[0] = s_n01.x;
+      ns[1] = s_n01.y;
+      ns[2] = __ldg(&S.src_tex[sp].v[4]);
       const double2 b00 = __ldg(reinterpret_cast<const double2*>(t00) + 1);
       const double2 b01 = __ldg(reinterpret_cast<const double2*>(t01) + 1);
       const double2 b10 = __ldg(reinterpret_cast<const double2*>(t10) + 1);
@@ -305,13 +292,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const double sN = sqrt((e2 * e2 * cfg.omega[2] + e3 * e3 * cfg.omega[3]) + e4 * e4 * cfg.omega[4]);
     const double dI = cfg.huber_delta[0], dD = cfg.huber_delta[1], dN = cfg.huber_delta[2];
     const bool smI = sI <= dI, smD = sD <= dD, smN = sN <= dN;
-    const double wI = smI ? 1.0 : dI / sI;
-    const double wD = smD ? 1.0 : dD / sD;
-    const double wN = smN ? 1.0 : dN / sN;
     cost += (smI ? sI * sI : dI * (2.0 * sI - dI)) + (smD ? sD * sD : dD * (2.0 * sD - dD)) +
             (smN ? sN * sN : dN * (2.0 * sN - dN));
     ++count;
     if (!kJac) continue;
+    const double wI = smI ? 1.0 : dI / sI;
+    const double wD = smD ? 1.0 : dD / sD;
+    const double wN = smN ? 1.0 : dN / sN;
 
     // ---- projective Jacobian (sensors.py:157-188) ----
     double P0[3], P1[3];
@@ -333,91 +320,64 @@ __global__ void __launch_bounds__(kThreads, 1)
       P1[1] = S.dst_cam.fy * iz;
       P1[2] = -S.dst_cam.fy * pb[1] * iz * iz;
     }
-    // depth cue direction: unit p_bar (spherical) or e_z (pinhole)  (solver.py:279-286)
-    double ud[3];
-    if (dst_sph) {
-      ud[0] = pb[0] / zeta;
-      ud[1] = pb[1] / zeta;
-      ud[2] = pb[2] / zeta;
-    } else {
-      ud[0] = 0.0;
-      ud[1] = 0.0;
-      ud[2] = 1.0;
+    // normal-cue rotation terms m_k x (R_o n)  (solver.py:287-291, see header)
+    double xn[9];
+    if (normal_on) {
+      double no[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        no[k] = S.Ro[3 * k + 0] * ns[0] + S.Ro[3 * k + 1] * ns[1] + S.Ro[3 * k + 2] * ns[2];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) cross3(&S.Mi[3 * k], no, &xn[3 * k]);
     }
     const double es[5] = {e0, e1, e2, e3, e4};
     const double wwc[5] = {wI * cfg.omega[0], wD * cfg.omega[1], wN * cfg.omega[2],
                            wN * cfg.omega[3], wN * cfg.omega[4]};
-    // normal-cue rotation blocks need R_o n and R_j^T R_i R_o n (solver.py:287-291)
-    double no[3] = {0.0, 0.0, 0.0}, np_[3] = {0.0, 0.0, 0.0};
-    if (normal_on) {
-#pragma unroll
-      for (int k = 0; k < 3; ++k)
-        no[k] = S.Ro[3 * k + 0] * ns[0] + S.Ro[3 * k + 1] * ns[1] + S.Ro[3 * k + 2] * ns[2];
-      double ri[3];
-#pragma unroll
-      for (int k = 0; k < 3; ++k)
-        ri[k] = S.Ri[3 * k + 0] * no[0] + S.Ri[3 * k + 1] * no[1] + S.Ri[3 * k + 2] * no[2];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) np_[k] = ri[0] * S.Rj[k] + ri[1] * S.Rj[3 + k] + ri[2] * S.Rj[6 + k];
-    }
     const int n_ch = normal_on ? 5 : 2;
     for (int c = 0; c < n_ch; ++c) {
-      // bilinear gradient of channel c (gradients interpolate the
-      // central-difference images, cues.py:448-450)
+      // bilinear gradient of channel c: the gradient images are interpolated
+      // (cues.py:448-450), not differentiated
       const double2 g00 = __ldg(reinterpret_cast<const double2*>(&t00->g[2 * c]));
       const double2 g01 = __ldg(reinterpret_cast<const double2*>(&t01->g[2 * c]));
       const double2 g10 = __ldg(reinterpret_cast<const double2*>(&t10->g[2 * c]));
       const double2 g11 = __ldg(reinterpret_cast<const double2*>(&t11->g[2 * c]));
       const double gc = bil(g00.x, g01.x, g10.x, g11.x, wx, wy);
       const double gr_ = bil(g00.y, g01.y, g10.y, g11.y, wx, wy);
+      // v_c = -(grad . P) (+ depth cue direction: p_bar/|p_bar| or e_z)
       double vv[3];
 #pragma unroll
       for (int k = 0; k < 3; ++k) vv[k] = -(gc * P0[k] + gr_ * P1[k]);
       if (c == 1) {
-#pragma unroll
-        for (int k = 0; k < 3; ++k) vv[k] += ud[k];
-      }
-      double Ji[6], Jj[6], w[3], wp[3], t[3];
-      // v^T a_i = [M_i^T v, -2 (M_i^T v) x p_u]
-#pragma unroll
-      for (int k = 0; k < 3; ++k) w[k] = vv[0] * S.Mi[k] + vv[1] * S.Mi[3 + k] + vv[2] * S.Mi[6 + k];
-      cross3(w, pu, t);
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        Ji[k] = w[k];
-        Ji[3 + k] = -2.0 * t[k];
-      }
-      // v^T a_j = [-R_o v, 2 (R_o v) x g]
-#pragma unroll
-      for (int k = 0; k < 3; ++k)
-        wp[k] = S.Ro[3 * k + 0] * vv[0] + S.Ro[3 * k + 1] * vv[1] + S.Ro[3 * k + 2] * vv[2];
-      cross3(wp, g, t);
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        Jj[k] = -wp[k];
-        Jj[3 + k] = 2.0 * t[k];
-      }
-      if (c >= 2) {
-        const int r = c - 2;
-        const double mrow[3] = {S.Mi[3 * r + 0], S.Mi[3 * r + 1], S.Mi[3 * r + 2]};
-        const double rcol[3] = {S.Ro[r], S.Ro[3 + r], S.Ro[6 + r]};
-        double x1[3], x2[3];
-        cross3(mrow, no, x1);
-        cross3(rcol, np_, x2);
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          Ji[3 + k] -= 2.0 * x1[k];
-          Jj[3 + k] += 2.0 * x2[k];
+        if (dst_sph) {
+          vv[0] += pb[0] / zeta;
+          vv[1] += pb[1] / zeta;
+          vv[2] += pb[2] / zeta;
+        } else {
+          vv[2] += 1.0;
         }
+      }
+      // q = [u; u x p_u (+ m_k x R_o n)],  u = M_i^T v
+      double q[6];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) q[k] = vv[0] * S.Mi[k] + vv[1] * S.Mi[3 + k] + vv[2] * S.Mi[6 + k];
+      cross3(q, pu, &q[3]);
+      if (c >= 2) {
+        q[3] += xn[3 * (c - 2) + 0];
+        q[4] += xn[3 * (c - 2) + 1];
+        q[5] += xn[3 * (c - 2) + 2];
       }
       const double ww = wwc[c];
       const double we = ww * es[c];
+      double a[6];
 #pragma unroll
       for (int k = 0; k < 6; ++k) {
-        bi[k] += Ji[k] * we;
-        bj[k] += Jj[k] * we;
+        a[k] = ww * q[k];
+        beta[k] = fma(q[k], we, beta[k]);
       }
-      accumulate_h(h, Ji, Jj, ww);
+#pragma unroll
+      for (int k = 0; k < 6; ++k)
+#pragma unroll
+        for (int l = k; l < 6; ++l) Q[upper_idx(k, l)] = fma(a[k], q[l], Q[upper_idx(k, l)]);
     }
   }
 
@@ -426,22 +386,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   double cnt = (double)count;
   if (kJac) {
 #pragma unroll
-    for (int k = 0; k < kH; ++k) {
-      float x = h[k];
+    for (int k = 0; k < kQ; ++k) {
+      double x = Q[k];
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
-      h[k] = x;
+      Q[k] = x;
     }
 #pragma unroll
     for (int k = 0; k < 6; ++k) {
-      double x = bi[k], y = bj[k];
+      double x = beta[k];
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        x += __shfl_xor_sync(0xffffffffu, x, off);
-        y += __shfl_xor_sync(0xffffffffu, y, off);
-      }
-      bi[k] = x;
-      bj[k] = y;
+      for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+      beta[k] = x;
     }
   }
 #pragma unroll
@@ -451,40 +407,107 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (lane == 0) {
     double* r = red[warp];
-    if (kJac) {
 #pragma unroll
-      for (int k = 0; k < kH; ++k) r[k] = (double)h[k];
+    for (int k = 0; k < kQ; ++k) r[k] = kJac ? Q[k] : 0.0;
 #pragma unroll
-      for (int k = 0; k < 6; ++k) {
-        r[PBA_REC_BI + k] = bi[k];
-        r[PBA_REC_BJ + k] = bj[k];
-      }
-    } else {
-      for (int k = 0; k < PBA_REC_COST; ++k) r[k] = 0.0;
-    }
-    r[PBA_REC_COST] = cost;
-    r[PBA_REC_COUNT] = cnt;
+    for (int k = 0; k < 6; ++k) r[kQ + k] = kJac ? beta[k] : 0.0;
+    r[27] = cost;
+    r[28] = cnt;
+    r[29] = r[30] = r[31] = 0.0;
   }
   __syncthreads();
-  if (threadIdx.x < kRec) {
+  if (threadIdx.x < kPart) {
     double s = 0.0;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) s += red[w][threadIdx.x];
-    partials[chunk * kRec + threadIdx.x] = s;
+    partials[chunk * kPart + threadIdx.x] = s;
   }
 }
 
-// Sum chunk partials of each pair in chunk order (fixed) -> per-pair record.
-__global__ void reduce_chunks_kernel(const double* __restrict__ partials,
-                                     const int32_t* __restrict__ offsets, int n_pairs,
-                                     double* __restrict__ records) {
-  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (long)n_pairs * kRec) return;
-  const int p = (int)(t / kRec), e = (int)(t - (long)p * kRec);
+// One warp per pair: sum the pair's chunk partials in chunk order, then
+// expand (Q, beta) into the reference _EdgeTerm blocks:
+//   H_ii = D Q D, H_jj = L Q L^T, H_ij = D Q L^T, b_i = D beta, b_j = L beta.
+__global__ void finalize_pairs_kernel(const double* __restrict__ partials,
+                                      const int32_t* __restrict__ offsets,
+                                      const pba_pair* __restrict__ pairs,
+                                      const double* __restrict__ poses, int n_pairs,
+                                      double* __restrict__ records) {
+  __shared__ double sQ[4][kPart];
+  __shared__ double sL[4][36];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int p = blockIdx.x * 4 + w;
+  if (p >= n_pairs) return;
   const int c0 = offsets[p], c1 = offsets[p + 1];
   double s = 0.0;
-  for (int c = c0; c < c1; ++c) s += partials[(long)c * kRec + e];
-  records[t] = s;
+  for (int c = c0; c < c1; ++c) s += partials[(long)c * kPart + lane];
+  sQ[w][lane] = s;
+  if (lane == 0) {
+    const pba_pair P = pairs[p];
+    const double* xi = poses + 12 * P.pose_i;
+    const double* xj = poses + 12 * P.pose_j;
+    double A[9], tg[3], dt[3];
+    for (int k = 0; k < 3; ++k) dt[k] = xi[9 + k] - xj[9 + k];
+    for (int r = 0; r < 3; ++r) {
+      for (int c = 0; c < 3; ++c)  // A = R_j^T R_i
+        A[3 * r + c] = xj[r] * xi[c] + xj[3 + r] * xi[3 + c] + xj[6 + r] * xi[6 + c];
+      tg[r] = xj[r] * dt[0] + xj[3 + r] * dt[1] + xj[6 + r] * dt[2];  // R_j^T (t_i - t_j)
+    }
+    double* L = sL[w];
+    for (int k = 0; k < 36; ++k) L[k] = 0.0;
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) {
+        L[6 * r + c] = -A[3 * r + c];
+        L[6 * (3 + r) + 3 + c] = 2.0 * A[3 * r + c];
+        // -2 [t_g]x A
+        const double sk0 = (r == 0) ? 0.0 : (r == 1 ? tg[2] : -tg[1]);
+        const double sk1 = (r == 0) ? -tg[2] : (r == 1 ? 0.0 : tg[0]);
+        const double sk2 = (r == 0) ? tg[1] : (r == 1 ? -tg[0] : 0.0);
+        L[6 * (3 + r) + c] = -2.0 * (sk0 * A[c] + sk1 * A[3 + c] + sk2 * A[6 + c]);
+      }
+  }
+  __syncwarp();
+  const double* q = sQ[w];
+  const double* L = sL[w];
+  auto Qf = [&](int a, int b) { return a <= b ? q[upper_idx(a, b)] : q[upper_idx(b, a)]; };
+  const double dg[6] = {1.0, 1.0, 1.0, -2.0, -2.0, -2.0};
+  double* rec = records + (long)p * kRec;
+  const bool any = q[28] > 0.0;
+  for (int e = lane; e < kRec; e += 32) {
+    double val = 0.0;
+    if (!any) {
+      val = 0.0;
+    } else if (e < PBA_REC_HJJ) {  // H_ii upper
+      int k = 0, t = e;
+      while (t >= 6 - k) { t -= 6 - k; ++k; }
+      const int l = k + t;
+      val = dg[k] * dg[l] * Qf(k, l);
+    } else if (e < PBA_REC_HIJ) {  // H_jj upper
+      int k = 0, t = e - PBA_REC_HJJ;
+      while (t >= 6 - k) { t -= 6 - k; ++k; }
+      const int l = k + t;
+      for (int a = 0; a < 6; ++a) {
+        if (L[6 * k + a] == 0.0) continue;
+        double inner = 0.0;
+        for (int b = 0; b < 6; ++b) inner += Qf(a, b) * L[6 * l + b];
+        val += L[6 * k + a] * inner;
+      }
+    } else if (e < PBA_REC_BI) {  // H_ij full
+      const int k = (e - PBA_REC_HIJ) / 6, l = (e - PBA_REC_HIJ) % 6;
+      for (int b = 0; b < 6; ++b) val += Qf(k, b) * L[6 * l + b];
+      val *= dg[k];
+    } else if (e < PBA_REC_BJ) {
+      const int k = e - PBA_REC_BI;
+      val = dg[k] * q[kQ + k];
+    } else if (e < PBA_REC_COST) {
+      const int k = e - PBA_REC_BJ;
+      for (int b = 0; b < 6; ++b) val += L[6 * k + b] * q[kQ + b];
+    } else if (e == PBA_REC_COST) {
+      val = q[27];
+    } else {
+      val = q[28];
+    }
+    rec[e] = val;
+  }
 }
 
 }  // namespace
@@ -547,9 +570,8 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
           frames, pairs, chunk_table, chunk_pixels, poses, extrinsics, *cfg, partials);
     PBA_LAUNCH_CHECK();
   }
-  const long total = (long)n_pairs * kRec;
-  reduce_chunks_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
-      partials, pair_chunk_offsets, n_pairs, records);
+  finalize_pairs_kernel<<<(unsigned)((n_pairs + 3) / 4), 128, 0, st>>>(
+      partials, pair_chunk_offsets, pairs, poses, n_pairs, records);
   PBA_LAUNCH_CHECK();
   return PBA_OK;
 }

@@ -22,6 +22,7 @@ PBA_ERR_PERTURBATION = 4
 PBA_PINHOLE = 0
 PBA_SPHERICAL = 1
 RECORD_DOUBLES = 92
+PARTIAL_DOUBLES = 32
 
 # symbols declared in include/pba.h, in header order
 EXPORTED = (
