@@ -332,35 +332,38 @@ def run_ours(args):
     ms_per_step = elapsed_ms / args.steps
 
     # ---- e2e: host pose buffers in, poses + cost out, every step --------
-    e2e = None
-    if hasattr(backend, "set_poses"):
-        host_in = torch.from_numpy(rows).pin_memory()
-        gens_in = torch.from_numpy(gens.astype(np.int32)).pin_memory()
-        host_out = torch.empty_like(host_in).pin_memory()
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        f0 = torch.cuda.Event(enable_timing=True)
-        f1 = torch.cuda.Event(enable_timing=True)
-        f0.record(stream)
-        for _ in range(args.steps):
-            L = local_level
-            L.poses[L.cur].copy_(host_in, non_blocking=True)
-            L.gens[L.cur].copy_(gens_in, non_blocking=True)
-            backend.try_step(cfg.lm_initial_lambda)
-            host_out.copy_(L.poses[1 - L.cur], non_blocking=True)
-            stream.synchronize()
-        f1.record(stream)
-        torch.cuda.synchronize()
-        e2e_ms = f0.elapsed_time(f1) / args.steps
-        t = torch.tensor([e2e_ms], dtype=torch.float64, device=device)
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-        e2e = {"value": total_pp / (e2e_ms / 1e3), "unit": "pixel-pairs/s",
-               "h2d_bytes_per_step": int(host_in.numel() * 8 + gens_in.numel() * 4),
-               "d2h_bytes_per_step": int(host_out.numel() * 8 + 64),
-               "ms_per_step": e2e_ms}
+    # The step's input (current poses + generations) is copied in from pinned
+    # host memory and its result (the accepted poses) copied back out, so the
+    # next step starts from host data; cost/count/status come back inside
+    # try_step's scalar readback.
+    L = local_level
+    host_in = torch.from_numpy(L.poses[L.cur].cpu().numpy()).pin_memory()
+    gens_in = torch.from_numpy(L.gens[L.cur].cpu().numpy()).pin_memory()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    f0 = torch.cuda.Event(enable_timing=True)
+    f1 = torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        L.poses[L.cur].copy_(host_in, non_blocking=True)
+        L.gens[L.cur].copy_(gens_in, non_blocking=True)
+        step()
+        host_in.copy_(L.poses[L.cur], non_blocking=True)
+        gens_in.copy_(L.gens[L.cur], non_blocking=True)
+        stream.synchronize()
+    f1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1) / args.steps
+    t = torch.tensor([e2e_ms], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+    e2e = {"value": total_pp / (e2e_ms / 1e3), "unit": "pixel-pairs/s",
+           "h2d_bytes_per_step": int(host_in.numel() * 8 + gens_in.numel() * 4),
+           "d2h_bytes_per_step": int(host_in.numel() * 8 + gens_in.numel() * 4 + 64),
+           "ms_per_step": e2e_ms,
+           "path": "DeviceLevel.try_step via the C ABI; poses in/out through pinned host buffers"}
 
     if rank != 0:
         if world > 1:

@@ -37,6 +37,7 @@
 // pairs are spread over GPUs.
 
 #include <math.h>
+#include <stdlib.h>
 
 #include "pba_common.cuh"
 
@@ -54,6 +55,7 @@ struct PairSetup {
   double rotn[9];  // R_o^T R_j^T R_i R_o                   (solver.py:241)
   double dt[3];    // t_i - t_j                             (solver.py:235)
   double to[3];
+  double cpb[3];   // R_o^T (R_j^T (t_i - t_j) - t_o): p_bar = M_i p_u + cpb
   double occ_tol;
   const Texel* src_tex;
   const uint8_t* src_mask;
@@ -98,6 +100,13 @@ __device__ void build_setup(PairSetup& S, const pba_frame* frames, const pba_pai
   matmul3(RoT, RjT, tmp);
   matmul3(tmp, S.Ri, S.Mi);
   matmul3(S.Mi, S.Ro, S.rotn);
+  for (int k = 0; k < 3; ++k) {
+    double gt = 0.0;  // (R_j^T dt)_k - t_o,k
+    for (int m = 0; m < 3; ++m) gt += S.Rj[3 * m + k] * S.dt[m];
+    tmp[k] = gt - S.to[k];
+  }
+  for (int k = 0; k < 3; ++k)
+    S.cpb[k] = S.Ro[k] * tmp[0] + S.Ro[3 + k] * tmp[1] + S.Ro[6 + k] * tmp[2];
   S.occ_tol = P.occ_tol;
   const pba_frame& fs = frames[P.src];
   const pba_frame& fd = frames[P.dst];
@@ -140,8 +149,8 @@ __device__ __forceinline__ void cross3(const double* a, const double* b, double*
 
 __device__ __forceinline__ int upper_idx(int k, int l) { return k * 6 - (k * (k - 1)) / 2 + (l - k); }
 
-template <bool kJac>
-__global__ void __launch_bounds__(kThreads, 1)
+template <bool kJac, int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
     linearize_kernel(const pba_frame* __restrict__ frames, const pba_pair* __restrict__ pairs,
                      const int32_t* __restrict__ chunk_table, int chunk_pixels,
                      const double* __restrict__ poses, const double* __restrict__ exts,
@@ -200,19 +209,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
     for (int k = 0; k < 3; ++k)
       pu[k] = S.Ro[3 * k + 0] * ps[0] + S.Ro[3 * k + 1] * ps[1] + S.Ro[3 * k + 2] * ps[2] + S.to[k];
-    // g = R_j^T (R_i p_u + t_i - t_j);  p_bar = R_o^T (g - t_o)   (solver.py:235-236)
+    // p_bar = R_o^T (R_j^T (R_i p_u + t_i - t_j) - t_o) = M_i p_u + cpb  (solver.py:235-236)
     double pb[3];
-    {
-      double qv[3], g[3];
 #pragma unroll
-      for (int k = 0; k < 3; ++k)
-        qv[k] = S.Ri[3 * k + 0] * pu[0] + S.Ri[3 * k + 1] * pu[1] + S.Ri[3 * k + 2] * pu[2] + S.dt[k];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) g[k] = qv[0] * S.Rj[k] + qv[1] * S.Rj[3 + k] + qv[2] * S.Rj[6 + k];
-      const double a0 = g[0] - S.to[0], a1 = g[1] - S.to[1], a2 = g[2] - S.to[2];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) pb[k] = a0 * S.Ro[k] + a1 * S.Ro[3 + k] + a2 * S.Ro[6 + k];
-    }
+    for (int k = 0; k < 3; ++k)
+      pb[k] = S.Mi[3 * k + 0] * pu[0] + S.Mi[3 * k + 1] * pu[1] + S.Mi[3 * k + 2] * pu[2] + S.cpb[k];
 
     // ---- project into the destination (sensors.py:95-130) ----
     double u, v, dist;
@@ -242,14 +243,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                         __ldg(S.dst_mask + dp + dW) & __ldg(S.dst_mask + dp + dW + 1);
     if (!(mk & PBA_MASK_SAMP_CORE)) continue;  // core_ok
     const Texel* t00 = S.dst_tex + dp;
-    const Texel* t01 = t00 + 1;
     const Texel* t10 = t00 + dW;
-    const Texel* t11 = t10 + 1;
 
     const double2 a00 = __ldg(reinterpret_cast<const double2*>(t00));
-    const double2 a01 = __ldg(reinterpret_cast<const double2*>(t01));
+    const double2 a01 = __ldg(reinterpret_cast<const double2*>(t00 + 1));
     const double2 a10 = __ldg(reinterpret_cast<const double2*>(t10));
-    const double2 a11 = __ldg(reinterpret_cast<const double2*>(t11));
+    const double2 a11 = __ldg(reinterpret_cast<const double2*>(t10 + 1));
     const double Dd = bil(a00.y, a01.y, a10.y, a11.y, wx, wy);
     // zeta_d: range for spherical, z for pinhole (solver.py:240)
     const double zeta = dst_sph ? dist : pb[2];
@@ -260,30 +259,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       rho2 = pb[0] * pb[0] + pb[1] * pb[1];
       if (!(rho2 > 0.0)) continue;  // ok_jac (sensors.py:173-175; solver.py:262-263)
     }
-    const double Id = bil(a00.x, a01.x, a10.x, a11.x, wx, wy);
-    const double e0 = s_id.x - Id;
+    const double e0 = s_id.x - bil(a00.x, a01.x, a10.x, a11.x, wx, wy);
 
     const bool normal_on = (mk & PBA_MASK_SAMP_NORMAL) && (sm & PBA_MASK_NORMAL_VALID);
     double e2 = 0.0, e3 = 0.0, e4 = 0.0;
-    double ns[3] = {0.0, 0.0, 0.0};
+    double no[3] = {0.0, 0.0, 0.0};  // R_o n_src
     if (normal_on) {
       const double2 s_n01 = __ldg(st + 1);  // source nx, ny
-      ns[0] = s_n01.x;
-      ns[1] = s_n01.y;
-      ns[2] = __ldg(&S.src_tex[sp].v[4]);
+      const double ns2 = __ldg(&S.src_tex[sp].v[4]);
       const double2 b00 = __ldg(reinterpret_cast<const double2*>(t00) + 1);
-      const double2 b01 = __ldg(reinterpret_cast<const double2*>(t01) + 1);
+      const double2 b01 = __ldg(reinterpret_cast<const double2*>(t00 + 1) + 1);
       const double2 b10 = __ldg(reinterpret_cast<const double2*>(t10) + 1);
-      const double2 b11 = __ldg(reinterpret_cast<const double2*>(t11) + 1);
-      const double c00 = __ldg(&t00->v[4]), c01 = __ldg(&t01->v[4]);
-      const double c10 = __ldg(&t10->v[4]), c11 = __ldg(&t11->v[4]);
-      double mn[3];
+      const double2 b11 = __ldg(reinterpret_cast<const double2*>(t10 + 1) + 1);
+      const double c00 = __ldg(&t00->v[4]), c01 = __ldg(&t00[1].v[4]);
+      const double c10 = __ldg(&t10->v[4]), c11 = __ldg(&t10[1].v[4]);
+      // rot_n n_src (solver.py:241-248)
+      const double m0 = s_n01.x * S.rotn[0] + s_n01.y * S.rotn[1] + ns2 * S.rotn[2];
+      const double m1 = s_n01.x * S.rotn[3] + s_n01.y * S.rotn[4] + ns2 * S.rotn[5];
+      const double m2 = s_n01.x * S.rotn[6] + s_n01.y * S.rotn[7] + ns2 * S.rotn[8];
+      e2 = m0 - bil(b00.x, b01.x, b10.x, b11.x, wx, wy);
+      e3 = m1 - bil(b00.y, b01.y, b10.y, b11.y, wx, wy);
+      e4 = m2 - bil(c00, c01, c10, c11, wx, wy);
+      if (kJac) {
 #pragma unroll
-      for (int k = 0; k < 3; ++k)
-        mn[k] = ns[0] * S.rotn[3 * k + 0] + ns[1] * S.rotn[3 * k + 1] + ns[2] * S.rotn[3 * k + 2];
-      e2 = mn[0] - bil(b00.x, b01.x, b10.x, b11.x, wx, wy);
-      e3 = mn[1] - bil(b00.y, b01.y, b10.y, b11.y, wx, wy);
-      e4 = mn[2] - bil(c00, c01, c10, c11, wx, wy);
+        for (int k = 0; k < 3; ++k)
+          no[k] = S.Ro[3 * k + 0] * s_n01.x + S.Ro[3 * k + 1] * s_n01.y + S.Ro[3 * k + 2] * ns2;
+      }
     }
 
     // ---- per-cue Huber (solver.py:317-337) ----
@@ -296,78 +297,75 @@ __global__ void __launch_bounds__(kThreads, 1)
             (smN ? sN * sN : dN * (2.0 * sN - dN));
     ++count;
     if (!kJac) continue;
-    const double wI = smI ? 1.0 : dI / sI;
-    const double wD = smD ? 1.0 : dD / sD;
-    const double wN = smN ? 1.0 : dN / sN;
 
-    // ---- projective Jacobian (sensors.py:157-188) ----
-    double P0[3], P1[3];
+    // ---- projective Jacobian folded with M_i (sensors.py:157-188) ----
+    // MP0 = M_i^T P[0,:], MP1 = M_i^T P[1,:], ud = M_i^T (depth-cue direction)
+    double MP0[3], MP1[3], ud[3];
     if (dst_sph) {
       const double rho = sqrt(rho2);
       const double r2 = rho2 + pb[2] * pb[2];
-      P0[0] = S.dst_cam.fx * (-pb[1] / rho2);
-      P0[1] = S.dst_cam.fx * (pb[0] / rho2);
-      P0[2] = 0.0;
-      P1[0] = S.dst_cam.fy * (-pb[0] * pb[2] / (rho * r2));
-      P1[1] = S.dst_cam.fy * (-pb[1] * pb[2] / (rho * r2));
-      P1[2] = S.dst_cam.fy * (rho / r2);
+      const double f0 = S.dst_cam.fx / rho2;
+      const double f1 = S.dst_cam.fy / (rho * r2);
+      const double iz = 1.0 / zeta;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const double m0 = S.Mi[k], m1 = S.Mi[3 + k], m2 = S.Mi[6 + k];
+        MP0[k] = f0 * (pb[0] * m1 - pb[1] * m0);
+        MP1[k] = f1 * (rho2 * m2 - pb[2] * (pb[0] * m0 + pb[1] * m1));
+        ud[k] = iz * (pb[0] * m0 + pb[1] * m1 + pb[2] * m2);
+      }
     } else {
       const double iz = 1.0 / pb[2];
-      P0[0] = S.dst_cam.fx * iz;
-      P0[1] = 0.0;
-      P0[2] = -S.dst_cam.fx * pb[0] * iz * iz;
-      P1[0] = 0.0;
-      P1[1] = S.dst_cam.fy * iz;
-      P1[2] = -S.dst_cam.fy * pb[1] * iz * iz;
-    }
-    // normal-cue rotation terms m_k x (R_o n)  (solver.py:287-291, see header)
-    double xn[9];
-    if (normal_on) {
-      double no[3];
+      const double f0 = S.dst_cam.fx * iz, f1 = S.dst_cam.fy * iz;
+      const double xz = pb[0] * iz, yz = pb[1] * iz;
 #pragma unroll
-      for (int k = 0; k < 3; ++k)
-        no[k] = S.Ro[3 * k + 0] * ns[0] + S.Ro[3 * k + 1] * ns[1] + S.Ro[3 * k + 2] * ns[2];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) cross3(&S.Mi[3 * k], no, &xn[3 * k]);
+      for (int k = 0; k < 3; ++k) {
+        const double m2 = S.Mi[6 + k];
+        MP0[k] = f0 * (S.Mi[k] - xz * m2);
+        MP1[k] = f1 * (S.Mi[3 + k] - yz * m2);
+        ud[k] = m2;
+      }
     }
-    const double es[5] = {e0, e1, e2, e3, e4};
-    const double wwc[5] = {wI * cfg.omega[0], wD * cfg.omega[1], wN * cfg.omega[2],
-                           wN * cfg.omega[3], wN * cfg.omega[4]};
+    const double wI = smI ? cfg.omega[0] : cfg.omega[0] * (dI / sI);
+    const double wD = smD ? cfg.omega[1] : cfg.omega[1] * (dD / sD);
+    const double wN = smN ? 1.0 : dN / sN;
     const int n_ch = normal_on ? 5 : 2;
+#pragma unroll 1
     for (int c = 0; c < n_ch; ++c) {
       // bilinear gradient of channel c: the gradient images are interpolated
       // (cues.py:448-450), not differentiated
       const double2 g00 = __ldg(reinterpret_cast<const double2*>(&t00->g[2 * c]));
-      const double2 g01 = __ldg(reinterpret_cast<const double2*>(&t01->g[2 * c]));
+      const double2 g01 = __ldg(reinterpret_cast<const double2*>(&t00[1].g[2 * c]));
       const double2 g10 = __ldg(reinterpret_cast<const double2*>(&t10->g[2 * c]));
-      const double2 g11 = __ldg(reinterpret_cast<const double2*>(&t11->g[2 * c]));
+      const double2 g11 = __ldg(reinterpret_cast<const double2*>(&t10[1].g[2 * c]));
       const double gc = bil(g00.x, g01.x, g10.x, g11.x, wx, wy);
       const double gr_ = bil(g00.y, g01.y, g10.y, g11.y, wx, wy);
-      // v_c = -(grad . P) (+ depth cue direction: p_bar/|p_bar| or e_z)
-      double vv[3];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) vv[k] = -(gc * P0[k] + gr_ * P1[k]);
-      if (c == 1) {
-        if (dst_sph) {
-          vv[0] += pb[0] / zeta;
-          vv[1] += pb[1] / zeta;
-          vv[2] += pb[2] / zeta;
-        } else {
-          vv[2] += 1.0;
-        }
-      }
-      // q = [u; u x p_u (+ m_k x R_o n)],  u = M_i^T v
+      // q = [u; u x p_u (+ m_k x R_o n)],  u = M_i^T v_c,  v_c = -(grad P) (+ depth cue)
       double q[6];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) q[k] = vv[0] * S.Mi[k] + vv[1] * S.Mi[3 + k] + vv[2] * S.Mi[6 + k];
+      for (int k = 0; k < 3; ++k) q[k] = -(gc * MP0[k] + gr_ * MP1[k]);
+      double ww, ec;
+      if (c == 0) {
+        ww = wI;
+        ec = e0;
+      } else if (c == 1) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) q[k] += ud[k];
+        ww = wD;
+        ec = e1;
+      } else {
+        ww = wN * (c == 2 ? cfg.omega[2] : (c == 3 ? cfg.omega[3] : cfg.omega[4]));
+        ec = c == 2 ? e2 : (c == 3 ? e3 : e4);
+      }
       cross3(q, pu, &q[3]);
       if (c >= 2) {
-        q[3] += xn[3 * (c - 2) + 0];
-        q[4] += xn[3 * (c - 2) + 1];
-        q[5] += xn[3 * (c - 2) + 2];
+        double xn[3];
+        cross3(&S.Mi[3 * (c - 2)], no, xn);
+        q[3] += xn[0];
+        q[4] += xn[1];
+        q[5] += xn[2];
       }
-      const double ww = wwc[c];
-      const double we = ww * es[c];
+      const double we = ww * ec;
       double a[6];
 #pragma unroll
       for (int k = 0; k < 6; ++k) {
@@ -562,12 +560,25 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
                 "NULL buffer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (n_chunks > 0) {
-    if (want_jacobians)
-      linearize_kernel<true><<<(unsigned)n_chunks, kThreads, 0, st>>>(
-          frames, pairs, chunk_table, chunk_pixels, poses, extrinsics, *cfg, partials);
-    else
-      linearize_kernel<false><<<(unsigned)n_chunks, kThreads, 0, st>>>(
-          frames, pairs, chunk_table, chunk_pixels, poses, extrinsics, *cfg, partials);
+    // register/occupancy variant: 1 -> <=255 regs (8 warps/SM), 2 -> 128 regs
+    // (16 warps/SM), 3 -> 85 regs (24 warps/SM); PBA_LIN_MINB overrides
+    static int minb = -1;
+    if (minb < 0) {
+      const char* env = getenv("PBA_LIN_MINB");
+      minb = env ? atoi(env) : 2;
+      if (minb < 1 || minb > 3) minb = 2;
+    }
+    const unsigned grid = (unsigned)n_chunks;
+#define PBA_LAUNCH_LIN(J, M) \
+  linearize_kernel<J, M><<<grid, kThreads, 0, st>>>(frames, pairs, chunk_table, chunk_pixels, poses, extrinsics, *cfg, partials)
+    if (want_jacobians) {
+      if (minb == 1) PBA_LAUNCH_LIN(true, 1);
+      else if (minb == 2) PBA_LAUNCH_LIN(true, 2);
+      else PBA_LAUNCH_LIN(true, 3);
+    } else {
+      PBA_LAUNCH_LIN(false, 2);
+    }
+#undef PBA_LAUNCH_LIN
     PBA_LAUNCH_CHECK();
   }
   finalize_pairs_kernel<<<(unsigned)((n_pairs + 3) / 4), 128, 0, st>>>(
