@@ -44,8 +44,7 @@
 namespace pba {
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
+constexpr int kThreads = 256;  // default CTA size
 constexpr int kQ = 21;    // upper triangle of Q (6x6)
 constexpr int kPart = 32; // chunk partial: Q[21], beta[6], cost, count, pad
 
@@ -149,13 +148,14 @@ __device__ __forceinline__ void cross3(const double* a, const double* b, double*
 
 __device__ __forceinline__ int upper_idx(int k, int l) { return k * 6 - (k * (k - 1)) / 2 + (l - k); }
 
-template <bool kJac, int kMinBlocks>
-__global__ void __launch_bounds__(kThreads, kMinBlocks)
+template <bool kJac, int kT, int kMinBlocks>
+__global__ void __launch_bounds__(kT, kMinBlocks)
     linearize_kernel(const pba_frame* __restrict__ frames, const pba_pair* __restrict__ pairs,
                      const int32_t* __restrict__ chunk_table, int chunk_pixels,
                      const double* __restrict__ poses, const double* __restrict__ exts,
                      pba_config cfg, double* __restrict__ partials) {
   __shared__ PairSetup S;
+  constexpr int kWarps = kT / 32;
   __shared__ double red[kWarps][kPart];
 
   const long chunk = blockIdx.x;
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   const bool dst_sph = S.dst_cam.model == PBA_SPHERICAL;
   const double dWd = (double)dW, dHd = (double)dH;
 
-  for (int idx = first + (int)threadIdx.x; idx < last; idx += kThreads) {
+  for (int idx = first + (int)threadIdx.x; idx < last; idx += kT) {
     const int gr = idx / S.grid_w;
     const int row = gr * S.stride;
     const int col = (idx - gr * S.grid_w) * S.stride;
@@ -560,23 +560,29 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
                 "NULL buffer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (n_chunks > 0) {
-    // register/occupancy variant: 1 -> <=255 regs (8 warps/SM), 2 -> 128 regs
-    // (16 warps/SM), 3 -> 85 regs (24 warps/SM); PBA_LIN_MINB overrides
-    static int minb = -1;
-    if (minb < 0) {
-      const char* env = getenv("PBA_LIN_MINB");
-      minb = env ? atoi(env) : 2;
-      if (minb < 1 || minb > 3) minb = 2;
+    // CTA-size / occupancy variant (PBA_LIN_VARIANT overrides):
+    //   1: 256 thr, <=255 regs (8 warps/SM)    2: 256 thr, 128 regs (16 warps/SM)
+    //   3: 128 thr, 128 regs (16 warps/SM)     4: 128 thr, 168 regs (12 warps/SM)
+    //   5: 512 thr, 128 regs (16 warps/SM)
+    static int variant = -1;
+    if (variant < 0) {
+      const char* env = getenv("PBA_LIN_VARIANT");
+      variant = env ? atoi(env) : 2;
+      if (variant < 1 || variant > 5) variant = 2;
     }
     const unsigned grid = (unsigned)n_chunks;
-#define PBA_LAUNCH_LIN(J, M) \
-  linearize_kernel<J, M><<<grid, kThreads, 0, st>>>(frames, pairs, chunk_table, chunk_pixels, poses, extrinsics, *cfg, partials)
+#define PBA_LAUNCH_LIN(J, T, M) \
+  linearize_kernel<J, T, M><<<grid, T, 0, st>>>(frames, pairs, chunk_table, chunk_pixels, poses, extrinsics, *cfg, partials)
     if (want_jacobians) {
-      if (minb == 1) PBA_LAUNCH_LIN(true, 1);
-      else if (minb == 2) PBA_LAUNCH_LIN(true, 2);
-      else PBA_LAUNCH_LIN(true, 3);
+      switch (variant) {
+        case 1: PBA_LAUNCH_LIN(true, 256, 1); break;
+        case 3: PBA_LAUNCH_LIN(true, 128, 4); break;
+        case 4: PBA_LAUNCH_LIN(true, 128, 3); break;
+        case 5: PBA_LAUNCH_LIN(true, 512, 1); break;
+        default: PBA_LAUNCH_LIN(true, 256, 2); break;
+      }
     } else {
-      PBA_LAUNCH_LIN(false, 2);
+      PBA_LAUNCH_LIN(false, 256, 2);
     }
 #undef PBA_LAUNCH_LIN
     PBA_LAUNCH_CHECK();
