@@ -199,6 +199,12 @@ int pba_apply_step(const double* poses_in, const int32_t* gen_in, const double* 
                    int32_t n_poses, int32_t gauge, double* poses_out, int32_t* gen_out,
                    int32_t* status, void* stream);
 
+/* ---- diagnostics ------------------------------------------------------
+ * The table-corrected fp64 atan2 the spherical projection uses
+ * (csrc/fastmath.cuh), exposed so tests can bound its error against the
+ * library atan2 / numpy.arctan2 (sensors.py:120-121).  Device pointers. */
+int pba_atan2_batch(const double* y, const double* x, int64_t n, double* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

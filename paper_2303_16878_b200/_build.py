@@ -34,7 +34,7 @@ def _stale() -> bool:
     if not LIB.exists():
         return True
     mtime = LIB.stat().st_mtime
-    deps = [CSRC / s for s in SOURCES] + [CSRC / "pba_common.cuh", ROOT / "include" / "pba.h"]
+    deps = [CSRC / s for s in SOURCES] + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "pba.h"]
     return any(p.stat().st_mtime > mtime for p in deps)
 
 

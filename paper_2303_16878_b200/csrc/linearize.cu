@@ -39,10 +39,33 @@
 #include <math.h>
 #include <stdlib.h>
 
+#include "fastmath.cuh"
 #include "pba_common.cuh"
 
 namespace pba {
+
+int ensure_atan_table() {
+  static bool done[64] = {false};
+  int dev = 0;
+  PBA_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev >= 0 && dev < 64 && done[dev]) return PBA_OK;
+  static AtanEntry host[2 * kAtanHalf + 1];
+  const double h = 3.14159265358979323846 / kAtanHalf;
+  for (int k = -kAtanHalf; k <= kAtanHalf; ++k) {
+    const double th = k * h;  // the stored theta is exactly the angle of (c, s)
+    host[k + kAtanHalf] = AtanEntry{cos(th), sin(th), th, 0.0};
+  }
+  PBA_CUDA_TRY(cudaMemcpyToSymbol(g_atan_table, host, sizeof(host)));
+  if (dev >= 0 && dev < 64) done[dev] = true;
+  return PBA_OK;
+}
+
 namespace {
+
+__global__ void atan2_batch_kernel(const double* y, const double* x, int64_t n, double* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = atan2_tab(y[i], x[i]);
+}
 
 constexpr int kThreads = 256;  // default CTA size
 constexpr int kQ = 21;    // upper triangle of Q (6x6)
@@ -125,6 +148,11 @@ __device__ void build_setup(PairSetup& S, const pba_frame* frames, const pba_pai
 
 // numpy float modulus for a positive divisor (np.mod, sensors.py:122).
 __device__ __forceinline__ double py_mod(double a, double w) {
+  // |a| < 2w (always, for an azimuth in [-pi, pi] with the usual cx, fx):
+  // fmod is exact there, so this equals the general path bit for bit.
+  if (a >= 0.0 && a < w) return a;
+  if (a >= w && a < 2.0 * w) return a - w;
+  if (a < 0.0 && a > -w) return a + w;
   double m = fmod(a, w);
   if (m != 0.0) {
     if (m < 0.0) m += w;
@@ -144,6 +172,16 @@ __device__ __forceinline__ void cross3(const double* a, const double* b, double*
   c[0] = a[1] * b[2] - a[2] * b[1];
   c[1] = a[2] * b[0] - a[0] * b[2];
   c[2] = a[0] * b[1] - a[1] * b[0];
+}
+
+// Move a (row, col) position of the strided source grid forward by `step`
+// pixels in row-major order (replaces a per-pixel integer division).
+__device__ __forceinline__ void advance_pixel(int& row, int& col, int width, int step) {
+  col += step;
+  while (col >= width) {
+    col -= width;
+    ++row;
+  }
 }
 
 __device__ __forceinline__ int upper_idx(int k, int l) { return k * 6 - (k * (k - 1)) / 2 + (l - k); }
@@ -180,10 +218,13 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
   const bool dst_sph = S.dst_cam.model == PBA_SPHERICAL;
   const double dWd = (double)dW, dHd = (double)dH;
 
-  for (int idx = first + (int)threadIdx.x; idx < last; idx += kT) {
-    const int gr = idx / S.grid_w;
+  const int gw = S.grid_w;
+  int gr = (first + (int)threadIdx.x) / gw;             // strided-grid row / column of
+  int gcol = first + (int)threadIdx.x - gr * gw;        // this thread's current pixel
+  for (int idx = first + (int)threadIdx.x; idx < last;
+       idx += kT, advance_pixel(gr, gcol, gw, kT)) {
     const int row = gr * S.stride;
-    const int col = (idx - gr * S.grid_w) * S.stride;
+    const int col = gcol * S.stride;
     const int sp = row * sW + col;
     const uint32_t sm = __ldg(S.src_mask + sp);
     if (!(sm & PBA_MASK_DEPTH_VALID)) continue;  // PairContext.build: usable = depth_valid
@@ -218,11 +259,12 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     // ---- project into the destination (sensors.py:95-130) ----
     double u, v, dist;
     if (dst_sph) {
-      const double az = atan2(pb[1], pb[0]);
-      const double el = atan2(pb[2], hypot(pb[0], pb[1]));
+      const double rr = pb[0] * pb[0] + pb[1] * pb[1];
+      const double az = atan2_tab(pb[1], pb[0]);
+      const double el = atan2_tab(pb[2], sqrt(rr));  // hypot(x, y)
       u = py_mod(S.dst_cam.fx * az + S.dst_cam.cx, dWd);
       v = S.dst_cam.fy * el + S.dst_cam.cy;
-      dist = sqrt((pb[0] * pb[0] + pb[1] * pb[1]) + pb[2] * pb[2]);
+      dist = sqrt(rr + pb[2] * pb[2]);
     } else {
       if (!(pb[2] > 0.0)) continue;
       u = S.dst_cam.fx * pb[0] / pb[2] + S.dst_cam.cx;
@@ -559,6 +601,7 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
                     partials && records,
                 "NULL buffer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (int rc = ensure_atan_table()) return rc;
   if (n_chunks > 0) {
     // CTA-size / occupancy variant (PBA_LIN_VARIANT overrides):
     //   1: 256 thr, <=255 regs (8 warps/SM)    2: 256 thr, 128 regs (16 warps/SM)
@@ -589,6 +632,17 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
   }
   finalize_pairs_kernel<<<(unsigned)((n_pairs + 3) / 4), 128, 0, st>>>(
       partials, pair_chunk_offsets, pairs, poses, n_pairs, records);
+  PBA_LAUNCH_CHECK();
+  return PBA_OK;
+}
+
+extern "C" int pba_atan2_batch(const double* y, const double* x, int64_t n, double* out,
+                               void* stream) {
+  PBA_ARG_CHECK(n >= 0 && (n == 0 || (y && x && out)), "bad arguments");
+  if (int rc = ensure_atan_table()) return rc;
+  if (n == 0) return PBA_OK;
+  atan2_batch_kernel<<<(unsigned)((n + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      y, x, n, out);
   PBA_LAUNCH_CHECK();
   return PBA_OK;
 }

@@ -315,3 +315,29 @@ def test_smoke_entry():
     import __graft_entry__
 
     __graft_entry__.smoke()
+
+
+def test_table_atan2_within_one_ulp_of_numpy():
+    from paper_2303_16878_b200 import native as N
+
+    lib = N.load()
+    rng = np.random.default_rng(9)
+    n = 1 << 20
+    mag = 10.0 ** rng.uniform(-6, 3, n)
+    ang = rng.uniform(-math.pi, math.pi, n)
+    x = mag * np.cos(ang)
+    y = mag * np.sin(ang) * 10.0 ** rng.uniform(-3, 3, n)
+    special = np.array([[0.0, 1.0], [0.0, -1.0], [1.0, 0.0], [-1.0, 0.0], [-0.0, -1.0],
+                        [1e-300, -1.0], [-1e-300, -1.0], [0.0, 0.0], [-0.0, 0.0], [3.0, 1e-320]])
+    y = np.concatenate([y, special[:, 0]])
+    x = np.concatenate([x, special[:, 1]])
+    yt, xt = _rows(y), _rows(x)
+    out = torch.empty_like(yt)
+    N.check(lib.pba_atan2_batch(yt.data_ptr(), xt.data_ptr(), y.size, out.data_ptr(),
+                                torch.cuda.current_stream().cuda_stream), "atan2")
+    got = out.cpu().numpy()
+    ref = np.arctan2(y, x)
+    ulp = np.abs(got - ref) / np.spacing(np.abs(ref)).clip(min=np.finfo(float).tiny)
+    assert np.all(ulp[ref != 0] <= 1.0), float(ulp.max())
+    assert np.array_equal(np.signbit(got[-10:]), np.signbit(ref[-10:]))
+    assert np.array_equal(got[-10:], ref[-10:])

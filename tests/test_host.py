@@ -133,7 +133,7 @@ def test_check_connectivity_names_stranded_pose():
 
 def _header_functions():
     text = (ROOT / "include" / "pba.h").read_text()
-    return sorted(set(re.findall(r"\b(pba_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(pba_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_library_exports_every_header_symbol():
