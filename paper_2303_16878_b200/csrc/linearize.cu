@@ -186,90 +186,6 @@ __device__ __forceinline__ void advance_pixel(int& row, int& col, int width, int
 
 __device__ __forceinline__ int upper_idx(int k, int l) { return k * 6 - (k * (k - 1)) / 2 + (l - k); }
 
-// State of one source pixel between the two pipeline stages: geometry and
-// footprint from stage 1, destination corner loads (I, D and the
-// (nz, mask) word of each texel) already in flight.
-struct PixelState {
-  double pb[3];
-  double wx, wy, dist, isrc;
-  double2 a00, a01, a10, a11;  // (I, D) of the four corners (loads in flight)
-  int sp, dp;                   // source pixel, destination top-left texel
-  uint32_t smask;               // source mask bits; 0 = no work for this pixel
-};
-
-__device__ __forceinline__ uint32_t mask_of(const double2& v) {
-  return (uint32_t)(__double_as_longlong(v.y) & 0xffffffffu);
-}
-
-// Stage 1 (solver.py:200-237, sensors.py:95-154, cues.py:397-405): unproject
-// the source pixel, warp it, project it, check the projection and issue the
-// destination corner loads.  `src0`, `src2` are the already-loaded (I, D) and
-// (nz, mask) words of the source texel.
-__device__ __forceinline__ void stage1(const PairSetup& S, int row, int col, double2 src0,
-                                       double2 src2, PixelState& P) {
-  P.smask = 0;
-  const uint32_t sm = mask_of(src2);
-  if (!(sm & PBA_MASK_DEPTH_VALID)) return;  // PairContext.build: usable = depth_valid
-  const int sW = S.src_cam.width, sH = S.src_cam.height;
-  const int dW = S.dst_cam.width, dH = S.dst_cam.height;
-  const double dWd = (double)dW, dHd = (double)dH;
-  const double d = src0.y;
-  double ps[3];
-  if (S.src_cam.model == PBA_SPHERICAL) {
-    const double ca = __ldg(S.src_ray + col), sa = __ldg(S.src_ray + sW + col);
-    const double ce = __ldg(S.src_ray + 2 * sW + row), se = __ldg(S.src_ray + 2 * sW + sH + row);
-    ps[0] = (ce * ca) * d;
-    ps[1] = (ce * sa) * d;
-    ps[2] = se * d;
-  } else {
-    ps[0] = __ldg(S.src_ray + col) * d;
-    ps[1] = __ldg(S.src_ray + 2 * sW + row) * d;
-    ps[2] = d;
-  }
-  // p_u = R_o p + t_o (solver.py:215); p_bar = M_i p_u + cpb (solver.py:235-236)
-  double pu[3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k)
-    pu[k] = S.Ro[3 * k + 0] * ps[0] + S.Ro[3 * k + 1] * ps[1] + S.Ro[3 * k + 2] * ps[2] + S.to[k];
-#pragma unroll
-  for (int k = 0; k < 3; ++k)
-    P.pb[k] = S.Mi[3 * k + 0] * pu[0] + S.Mi[3 * k + 1] * pu[1] + S.Mi[3 * k + 2] * pu[2] +
-              S.cpb[k];
-  double u, v;
-  if (S.dst_cam.model == PBA_SPHERICAL) {
-    const double rr = P.pb[0] * P.pb[0] + P.pb[1] * P.pb[1];
-    const double az = atan2_tab(P.pb[1], P.pb[0]);
-    const double el = atan2_tab(P.pb[2], sqrt(rr));  // hypot(x, y)
-    u = py_mod(S.dst_cam.fx * az + S.dst_cam.cx, dWd);
-    v = S.dst_cam.fy * el + S.dst_cam.cy;
-    P.dist = sqrt(rr + P.pb[2] * P.pb[2]);
-  } else {
-    if (!(P.pb[2] > 0.0)) return;
-    u = S.dst_cam.fx * P.pb[0] / P.pb[2] + S.dst_cam.cx;
-    v = S.dst_cam.fy * P.pb[1] / P.pb[2] + S.dst_cam.cy;
-    P.dist = P.pb[2];
-  }
-  if (!(P.dist >= S.dst_cam.depth_min && P.dist <= S.dst_cam.depth_max)) return;
-  // project's strict bound, then sample's inclusive "inside" (cues.py:400)
-  if (!(u >= 0.0 && u < dWd && v >= 0.0 && v < dHd)) return;
-  if (!(u <= dWd - 1.0 && v <= dHd - 1.0)) return;
-  int x0 = (int)floor(u), y0 = (int)floor(v);
-  x0 = min(max(x0, 0), dW - 2);
-  y0 = min(max(y0, 0), dH - 2);
-  P.wx = u - x0;
-  P.wy = v - y0;
-  P.dp = y0 * dW + x0;
-  P.sp = row * sW + col;
-  P.isrc = src0.x;
-  const double2* t0 = reinterpret_cast<const double2*>(S.dst_tex + P.dp);
-  const double2* t1 = reinterpret_cast<const double2*>(S.dst_tex + P.dp + dW);
-  P.a00 = __ldg(t0);
-  P.a01 = __ldg(t0 + 8);
-  P.a10 = __ldg(t1);
-  P.a11 = __ldg(t1 + 8);
-  P.smask = sm | 0x100u;  // bit 8: reached the sampling stage
-}
-
 template <bool kJac, int kT, int kMinBlocks>
 __global__ void __launch_bounds__(kT, kMinBlocks)
     linearize_kernel(const pba_frame* __restrict__ frames, const pba_pair* __restrict__ pairs,
@@ -296,198 +212,213 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
   int count = 0;
 
   const int last = min(first + chunk_pixels, S.n_px);
-  const int sW = S.src_cam.width;
-  const int dW = S.dst_cam.width;
+  const int sW = S.src_cam.width, sH = S.src_cam.height;
+  const int dW = S.dst_cam.width, dH = S.dst_cam.height;
+  const bool src_sph = S.src_cam.model == PBA_SPHERICAL;
   const bool dst_sph = S.dst_cam.model == PBA_SPHERICAL;
-  const int gw = S.grid_w;
-  const int stride = S.stride;
+  const double dWd = (double)dW, dHd = (double)dH;
 
-  // software pipeline over this thread's pixels idx = first+tid, +kT, ...:
-  //   source texel of pixel k+2 loading | stage 1 of k+1 (dst loads in flight) | stage 2 of k
-  int gr = (first + (int)threadIdx.x) / gw;
-  int gcol = first + (int)threadIdx.x - gr * gw;
-  int idx = first + (int)threadIdx.x;
-  PixelState cur;
-  cur.smask = 0;
-  double2 nsrc0 = make_double2(0.0, 0.0), nsrc2 = make_double2(0.0, 0.0);
-  int nrow = gr * stride, ncol = gcol * stride;
-  if (idx < last) {
-    const double2* t = reinterpret_cast<const double2*>(S.src_tex + nrow * sW + ncol);
-    nsrc0 = __ldg(t);
-    nsrc2 = __ldg(t + 2);
-  }
-  bool have_cur = false;
-  while (true) {
-    // ---- stage 1 for the pixel whose source texel is loaded ----
-    PixelState nxt;
-    nxt.smask = 0;
-    const bool have_nxt = idx < last;
-    if (have_nxt) {
-      const double2 s0 = nsrc0, s2 = nsrc2;
-      const int row = nrow, col = ncol;
-      // prefetch the following pixel's source texel
-      idx += kT;
-      advance_pixel(gr, gcol, gw, kT);
-      nrow = gr * stride;
-      ncol = gcol * stride;
-      if (idx < last) {
-        const double2* t = reinterpret_cast<const double2*>(S.src_tex + nrow * sW + ncol);
-        nsrc0 = __ldg(t);
-        nsrc2 = __ldg(t + 2);
-      }
-      stage1(S, row, col, s0, s2, nxt);
+  const int gw = S.grid_w;
+  int gr = (first + (int)threadIdx.x) / gw;             // strided-grid row / column of
+  int gcol = first + (int)threadIdx.x - gr * gw;        // this thread's current pixel
+  for (int idx = first + (int)threadIdx.x; idx < last;
+       idx += kT, advance_pixel(gr, gcol, gw, kT)) {
+    const int row = gr * S.stride;
+    const int col = gcol * S.stride;
+    const int sp = row * sW + col;
+    const uint32_t sm = __ldg(S.src_mask + sp);
+    if (!(sm & PBA_MASK_DEPTH_VALID)) continue;  // PairContext.build: usable = depth_valid
+
+    // ---- source cue values and unprojection (sensors.py:133-154) ----
+    const double2* st = reinterpret_cast<const double2*>(S.src_tex + sp);
+    const double2 s_id = __ldg(st + 0);   // I, D
+    const double d = s_id.y;
+    double ps[3];
+    if (src_sph) {
+      const double ca = __ldg(S.src_ray + col), sa = __ldg(S.src_ray + sW + col);
+      const double ce = __ldg(S.src_ray + 2 * sW + row), se = __ldg(S.src_ray + 2 * sW + sH + row);
+      ps[0] = (ce * ca) * d;
+      ps[1] = (ce * sa) * d;
+      ps[2] = se * d;
+    } else {
+      ps[0] = __ldg(S.src_ray + col) * d;
+      ps[1] = __ldg(S.src_ray + 2 * sW + row) * d;
+      ps[2] = d;
     }
-    // ---- stage 2 (residuals, Huber, Jacobians, sums) for the previous pixel ----
-    if (have_cur && cur.smask) {
-      const PixelState& P = cur;
-      const Texel* t00 = S.dst_tex + P.dp;
-      const Texel* t10 = t00 + dW;
-      // corner masks and nz: same 128-byte lines as the (I, D) words -> L1 hits
-      const double2 m00 = __ldg(reinterpret_cast<const double2*>(t00) + 2);
-      const double2 m01 = __ldg(reinterpret_cast<const double2*>(t00 + 1) + 2);
-      const double2 m10 = __ldg(reinterpret_cast<const double2*>(t10) + 2);
-      const double2 m11 = __ldg(reinterpret_cast<const double2*>(t10 + 1) + 2);
-      const uint32_t mk = mask_of(m00) & mask_of(m01) & mask_of(m10) & mask_of(m11);
-      bool ok = (mk & PBA_MASK_SAMP_CORE) != 0;  // core_ok (cues.py:451-455)
-      const double wx = P.wx, wy = P.wy;
-      const double Dd = bil(P.a00.y, P.a01.y, P.a10.y, P.a11.y, wx, wy);
-      // zeta_d: range for spherical, z for pinhole (solver.py:240)
-      const double zeta = P.dist;
-      const double e1 = zeta - Dd;
-      ok = ok && !(e1 > S.occ_tol);  // occluded (solver.py:254-258)
-      double rho2 = 0.0;
-      if (kJac && dst_sph) {
-        rho2 = P.pb[0] * P.pb[0] + P.pb[1] * P.pb[1];
-        ok = ok && (rho2 > 0.0);  // ok_jac (sensors.py:173-175; solver.py:262-263)
+    // p_u = R_o p + t_o (solver.py:215)
+    double pu[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      pu[k] = S.Ro[3 * k + 0] * ps[0] + S.Ro[3 * k + 1] * ps[1] + S.Ro[3 * k + 2] * ps[2] + S.to[k];
+    // p_bar = R_o^T (R_j^T (R_i p_u + t_i - t_j) - t_o) = M_i p_u + cpb  (solver.py:235-236)
+    double pb[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      pb[k] = S.Mi[3 * k + 0] * pu[0] + S.Mi[3 * k + 1] * pu[1] + S.Mi[3 * k + 2] * pu[2] + S.cpb[k];
+
+    // ---- project into the destination (sensors.py:95-130) ----
+    double u, v, dist;
+    if (dst_sph) {
+      const double rr = pb[0] * pb[0] + pb[1] * pb[1];
+      const double az = atan2_tab(pb[1], pb[0]);
+      const double el = atan2_tab(pb[2], sqrt(rr));  // hypot(x, y)
+      u = py_mod(S.dst_cam.fx * az + S.dst_cam.cx, dWd);
+      v = S.dst_cam.fy * el + S.dst_cam.cy;
+      dist = sqrt(rr + pb[2] * pb[2]);
+    } else {
+      if (!(pb[2] > 0.0)) continue;
+      u = S.dst_cam.fx * pb[0] / pb[2] + S.dst_cam.cx;
+      v = S.dst_cam.fy * pb[1] / pb[2] + S.dst_cam.cy;
+      dist = pb[2];
+    }
+    if (!(dist >= S.dst_cam.depth_min && dist <= S.dst_cam.depth_max)) continue;
+    if (!(u >= 0.0 && u < dWd && v >= 0.0 && v < dHd)) continue;
+
+    // ---- bilinear footprint and validity (cues.py:397-409, 451-456) ----
+    if (!(u <= dWd - 1.0 && v <= dHd - 1.0)) continue;  // inside (u, v >= 0 already)
+    int x0 = (int)floor(u), y0 = (int)floor(v);
+    x0 = min(max(x0, 0), dW - 2);
+    y0 = min(max(y0, 0), dH - 2);
+    const double wx = u - x0, wy = v - y0;
+    const int dp = y0 * dW + x0;
+    const uint32_t mk = __ldg(S.dst_mask + dp) & __ldg(S.dst_mask + dp + 1) &
+                        __ldg(S.dst_mask + dp + dW) & __ldg(S.dst_mask + dp + dW + 1);
+    if (!(mk & PBA_MASK_SAMP_CORE)) continue;  // core_ok
+    const Texel* t00 = S.dst_tex + dp;
+    const Texel* t10 = t00 + dW;
+
+    const double2 a00 = __ldg(reinterpret_cast<const double2*>(t00));
+    const double2 a01 = __ldg(reinterpret_cast<const double2*>(t00 + 1));
+    const double2 a10 = __ldg(reinterpret_cast<const double2*>(t10));
+    const double2 a11 = __ldg(reinterpret_cast<const double2*>(t10 + 1));
+    const double Dd = bil(a00.y, a01.y, a10.y, a11.y, wx, wy);
+    // zeta_d: range for spherical, z for pinhole (solver.py:240)
+    const double zeta = dst_sph ? dist : pb[2];
+    const double e1 = zeta - Dd;
+    if (e1 > S.occ_tol) continue;  // occluded (solver.py:254-258)
+    double rho2 = 0.0;
+    if (kJac && dst_sph) {
+      rho2 = pb[0] * pb[0] + pb[1] * pb[1];
+      if (!(rho2 > 0.0)) continue;  // ok_jac (sensors.py:173-175; solver.py:262-263)
+    }
+    const double e0 = s_id.x - bil(a00.x, a01.x, a10.x, a11.x, wx, wy);
+
+    const bool normal_on = (mk & PBA_MASK_SAMP_NORMAL) && (sm & PBA_MASK_NORMAL_VALID);
+    double e2 = 0.0, e3 = 0.0, e4 = 0.0;
+    double no[3] = {0.0, 0.0, 0.0};  // R_o n_src
+    if (normal_on) {
+      const double2 s_n01 = __ldg(st + 1);  // source nx, ny
+      const double ns2 = __ldg(&S.src_tex[sp].v[4]);
+      const double2 b00 = __ldg(reinterpret_cast<const double2*>(t00) + 1);
+      const double2 b01 = __ldg(reinterpret_cast<const double2*>(t00 + 1) + 1);
+      const double2 b10 = __ldg(reinterpret_cast<const double2*>(t10) + 1);
+      const double2 b11 = __ldg(reinterpret_cast<const double2*>(t10 + 1) + 1);
+      const double c00 = __ldg(&t00->v[4]), c01 = __ldg(&t00[1].v[4]);
+      const double c10 = __ldg(&t10->v[4]), c11 = __ldg(&t10[1].v[4]);
+      // rot_n n_src (solver.py:241-248)
+      const double m0 = s_n01.x * S.rotn[0] + s_n01.y * S.rotn[1] + ns2 * S.rotn[2];
+      const double m1 = s_n01.x * S.rotn[3] + s_n01.y * S.rotn[4] + ns2 * S.rotn[5];
+      const double m2 = s_n01.x * S.rotn[6] + s_n01.y * S.rotn[7] + ns2 * S.rotn[8];
+      e2 = m0 - bil(b00.x, b01.x, b10.x, b11.x, wx, wy);
+      e3 = m1 - bil(b00.y, b01.y, b10.y, b11.y, wx, wy);
+      e4 = m2 - bil(c00, c01, c10, c11, wx, wy);
+      if (kJac) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+          no[k] = S.Ro[3 * k + 0] * s_n01.x + S.Ro[3 * k + 1] * s_n01.y + S.Ro[3 * k + 2] * ns2;
       }
-      if (ok) {
-        const double e0 = P.isrc - bil(P.a00.x, P.a01.x, P.a10.x, P.a11.x, wx, wy);
-        const bool normal_on = (mk & PBA_MASK_SAMP_NORMAL) && (P.smask & PBA_MASK_NORMAL_VALID);
-        double e2 = 0.0, e3 = 0.0, e4 = 0.0;
-        double no[3] = {0.0, 0.0, 0.0};  // R_o n_src
-        if (normal_on) {
-          const double2* st = reinterpret_cast<const double2*>(S.src_tex + P.sp);
-          const double2 s_n01 = __ldg(st + 1);  // source nx, ny
-          const double ns2 = __ldg(&S.src_tex[P.sp].v[4]);
-          const double2 b00 = __ldg(reinterpret_cast<const double2*>(t00) + 1);
-          const double2 b01 = __ldg(reinterpret_cast<const double2*>(t00 + 1) + 1);
-          const double2 b10 = __ldg(reinterpret_cast<const double2*>(t10) + 1);
-          const double2 b11 = __ldg(reinterpret_cast<const double2*>(t10 + 1) + 1);
-          // rot_n n_src (solver.py:241-248)
-          const double m0 = s_n01.x * S.rotn[0] + s_n01.y * S.rotn[1] + ns2 * S.rotn[2];
-          const double m1 = s_n01.x * S.rotn[3] + s_n01.y * S.rotn[4] + ns2 * S.rotn[5];
-          const double m2 = s_n01.x * S.rotn[6] + s_n01.y * S.rotn[7] + ns2 * S.rotn[8];
-          e2 = m0 - bil(b00.x, b01.x, b10.x, b11.x, wx, wy);
-          e3 = m1 - bil(b00.y, b01.y, b10.y, b11.y, wx, wy);
-          e4 = m2 - bil(m00.x, m01.x, m10.x, m11.x, wx, wy);
-          if (kJac) {
+    }
+
+    // ---- per-cue Huber (solver.py:317-337) ----
+    const double sI = sqrt(e0 * e0 * cfg.omega[0]);
+    const double sD = sqrt(e1 * e1 * cfg.omega[1]);
+    const double sN = sqrt((e2 * e2 * cfg.omega[2] + e3 * e3 * cfg.omega[3]) + e4 * e4 * cfg.omega[4]);
+    const double dI = cfg.huber_delta[0], dD = cfg.huber_delta[1], dN = cfg.huber_delta[2];
+    const bool smI = sI <= dI, smD = sD <= dD, smN = sN <= dN;
+    cost += (smI ? sI * sI : dI * (2.0 * sI - dI)) + (smD ? sD * sD : dD * (2.0 * sD - dD)) +
+            (smN ? sN * sN : dN * (2.0 * sN - dN));
+    ++count;
+    if (!kJac) continue;
+
+    // ---- projective Jacobian folded with M_i (sensors.py:157-188) ----
+    // MP0 = M_i^T P[0,:], MP1 = M_i^T P[1,:], ud = M_i^T (depth-cue direction)
+    double MP0[3], MP1[3], ud[3];
+    if (dst_sph) {
+      const double rho = sqrt(rho2);
+      const double r2 = rho2 + pb[2] * pb[2];
+      const double f0 = S.dst_cam.fx / rho2;
+      const double f1 = S.dst_cam.fy / (rho * r2);
+      const double iz = 1.0 / zeta;
 #pragma unroll
-            for (int k = 0; k < 3; ++k)
-              no[k] = S.Ro[3 * k + 0] * s_n01.x + S.Ro[3 * k + 1] * s_n01.y + S.Ro[3 * k + 2] * ns2;
-          }
-        }
-        // ---- per-cue Huber (solver.py:317-337) ----
-        const double sI = sqrt(e0 * e0 * cfg.omega[0]);
-        const double sD = sqrt(e1 * e1 * cfg.omega[1]);
-        const double sN =
-            sqrt((e2 * e2 * cfg.omega[2] + e3 * e3 * cfg.omega[3]) + e4 * e4 * cfg.omega[4]);
-        const double dI = cfg.huber_delta[0], dD = cfg.huber_delta[1], dN = cfg.huber_delta[2];
-        const bool smI = sI <= dI, smD = sD <= dD, smN = sN <= dN;
-        cost += (smI ? sI * sI : dI * (2.0 * sI - dI)) + (smD ? sD * sD : dD * (2.0 * sD - dD)) +
-                (smN ? sN * sN : dN * (2.0 * sN - dN));
-        ++count;
-        if (kJac) {
-          const double* pb = P.pb;
-          double pu[3];  // p_u = M_i^T (p_bar - cpb), cheaper than carrying it
-          {
-            const double q0 = pb[0] - S.cpb[0], q1 = pb[1] - S.cpb[1], q2 = pb[2] - S.cpb[2];
+      for (int k = 0; k < 3; ++k) {
+        const double m0 = S.Mi[k], m1 = S.Mi[3 + k], m2 = S.Mi[6 + k];
+        MP0[k] = f0 * (pb[0] * m1 - pb[1] * m0);
+        MP1[k] = f1 * (rho2 * m2 - pb[2] * (pb[0] * m0 + pb[1] * m1));
+        ud[k] = iz * (pb[0] * m0 + pb[1] * m1 + pb[2] * m2);
+      }
+    } else {
+      const double iz = 1.0 / pb[2];
+      const double f0 = S.dst_cam.fx * iz, f1 = S.dst_cam.fy * iz;
+      const double xz = pb[0] * iz, yz = pb[1] * iz;
 #pragma unroll
-            for (int k = 0; k < 3; ++k) pu[k] = q0 * S.Mi[k] + q1 * S.Mi[3 + k] + q2 * S.Mi[6 + k];
-          }
-          // ---- projective Jacobian folded with M_i (sensors.py:157-188) ----
-          double MP0[3], MP1[3], ud[3];
-          if (dst_sph) {
-            const double rho = sqrt(rho2);
-            const double r2 = rho2 + pb[2] * pb[2];
-            const double f0 = S.dst_cam.fx / rho2;
-            const double f1 = S.dst_cam.fy / (rho * r2);
-            const double iz = 1.0 / zeta;
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-              const double m0 = S.Mi[k], m1 = S.Mi[3 + k], m2 = S.Mi[6 + k];
-              MP0[k] = f0 * (pb[0] * m1 - pb[1] * m0);
-              MP1[k] = f1 * (rho2 * m2 - pb[2] * (pb[0] * m0 + pb[1] * m1));
-              ud[k] = iz * (pb[0] * m0 + pb[1] * m1 + pb[2] * m2);
-            }
-          } else {
-            const double iz = 1.0 / pb[2];
-            const double f0 = S.dst_cam.fx * iz, f1 = S.dst_cam.fy * iz;
-            const double xz = pb[0] * iz, yz = pb[1] * iz;
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-              const double m2 = S.Mi[6 + k];
-              MP0[k] = f0 * (S.Mi[k] - xz * m2);
-              MP1[k] = f1 * (S.Mi[3 + k] - yz * m2);
-              ud[k] = m2;
-            }
-          }
-          const double wI = smI ? cfg.omega[0] : cfg.omega[0] * (dI / sI);
-          const double wD = smD ? cfg.omega[1] : cfg.omega[1] * (dD / sD);
-          const double wN = smN ? 1.0 : dN / sN;
-          const int n_ch = normal_on ? 5 : 2;
+      for (int k = 0; k < 3; ++k) {
+        const double m2 = S.Mi[6 + k];
+        MP0[k] = f0 * (S.Mi[k] - xz * m2);
+        MP1[k] = f1 * (S.Mi[3 + k] - yz * m2);
+        ud[k] = m2;
+      }
+    }
+    const double wI = smI ? cfg.omega[0] : cfg.omega[0] * (dI / sI);
+    const double wD = smD ? cfg.omega[1] : cfg.omega[1] * (dD / sD);
+    const double wN = smN ? 1.0 : dN / sN;
+    const int n_ch = normal_on ? 5 : 2;
 #pragma unroll 1
-          for (int c = 0; c < n_ch; ++c) {
-            // bilinear gradient of channel c: the gradient images are interpolated
-            // (cues.py:448-450), not differentiated
-            const double2 g00 = __ldg(reinterpret_cast<const double2*>(&t00->g[2 * c]));
-            const double2 g01 = __ldg(reinterpret_cast<const double2*>(&t00[1].g[2 * c]));
-            const double2 g10 = __ldg(reinterpret_cast<const double2*>(&t10->g[2 * c]));
-            const double2 g11 = __ldg(reinterpret_cast<const double2*>(&t10[1].g[2 * c]));
-            const double gc = bil(g00.x, g01.x, g10.x, g11.x, wx, wy);
-            const double gr_ = bil(g00.y, g01.y, g10.y, g11.y, wx, wy);
-            // q = [u; u x p_u (+ m_k x R_o n)],  u = M_i^T v_c,  v_c = -(grad P) (+ depth cue)
-            double q[6];
+    for (int c = 0; c < n_ch; ++c) {
+      // bilinear gradient of channel c: the gradient images are interpolated
+      // (cues.py:448-450), not differentiated
+      const double2 g00 = __ldg(reinterpret_cast<const double2*>(&t00->g[2 * c]));
+      const double2 g01 = __ldg(reinterpret_cast<const double2*>(&t00[1].g[2 * c]));
+      const double2 g10 = __ldg(reinterpret_cast<const double2*>(&t10->g[2 * c]));
+      const double2 g11 = __ldg(reinterpret_cast<const double2*>(&t10[1].g[2 * c]));
+      const double gc = bil(g00.x, g01.x, g10.x, g11.x, wx, wy);
+      const double gr_ = bil(g00.y, g01.y, g10.y, g11.y, wx, wy);
+      // q = [u; u x p_u (+ m_k x R_o n)],  u = M_i^T v_c,  v_c = -(grad P) (+ depth cue)
+      double q[6];
 #pragma unroll
-            for (int k = 0; k < 3; ++k) q[k] = -(gc * MP0[k] + gr_ * MP1[k]);
-            double ww, ec;
-            if (c == 0) {
-              ww = wI;
-              ec = e0;
-            } else if (c == 1) {
+      for (int k = 0; k < 3; ++k) q[k] = -(gc * MP0[k] + gr_ * MP1[k]);
+      double ww, ec;
+      if (c == 0) {
+        ww = wI;
+        ec = e0;
+      } else if (c == 1) {
 #pragma unroll
-              for (int k = 0; k < 3; ++k) q[k] += ud[k];
-              ww = wD;
-              ec = e1;
-            } else {
-              ww = wN * (c == 2 ? cfg.omega[2] : (c == 3 ? cfg.omega[3] : cfg.omega[4]));
-              ec = c == 2 ? e2 : (c == 3 ? e3 : e4);
-            }
-            cross3(q, pu, &q[3]);
-            if (c >= 2) {
-              double xn[3];
-              cross3(&S.Mi[3 * (c - 2)], no, xn);
-              q[3] += xn[0];
-              q[4] += xn[1];
-              q[5] += xn[2];
-            }
-            const double we = ww * ec;
-            double a[6];
-#pragma unroll
-            for (int k = 0; k < 6; ++k) {
-              a[k] = ww * q[k];
-              beta[k] = fma(q[k], we, beta[k]);
-            }
-#pragma unroll
-            for (int k = 0; k < 6; ++k)
-#pragma unroll
-              for (int l = k; l < 6; ++l) Q[upper_idx(k, l)] = fma(a[k], q[l], Q[upper_idx(k, l)]);
-          }
-        }
+        for (int k = 0; k < 3; ++k) q[k] += ud[k];
+        ww = wD;
+        ec = e1;
+      } else {
+        ww = wN * (c == 2 ? cfg.omega[2] : (c == 3 ? cfg.omega[3] : cfg.omega[4]));
+        ec = c == 2 ? e2 : (c == 3 ? e3 : e4);
       }
+      cross3(q, pu, &q[3]);
+      if (c >= 2) {
+        double xn[3];
+        cross3(&S.Mi[3 * (c - 2)], no, xn);
+        q[3] += xn[0];
+        q[4] += xn[1];
+        q[5] += xn[2];
+      }
+      const double we = ww * ec;
+      double a[6];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        a[k] = ww * q[k];
+        beta[k] = fma(q[k], we, beta[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < 6; ++k)
+#pragma unroll
+        for (int l = k; l < 6; ++l) Q[upper_idx(k, l)] = fma(a[k], q[l], Q[upper_idx(k, l)]);
     }
-    if (!have_nxt) break;
-    cur = nxt;
-    have_cur = true;
   }
 
   // ---- fixed-order reduction: warp butterfly, then warps in order ----
@@ -679,8 +610,8 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
     static int variant = -1;
     if (variant < 0) {
       const char* env = getenv("PBA_LIN_VARIANT");
-      variant = env ? atoi(env) : 2;
-      if (variant < 1 || variant > 5) variant = 2;
+      variant = env ? atoi(env) : 4;
+      if (variant < 1 || variant > 5) variant = 4;
     }
     const unsigned grid = (unsigned)n_chunks;
 #define PBA_LAUNCH_LIN(J, T, M) \
@@ -689,12 +620,12 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
       switch (variant) {
         case 1: PBA_LAUNCH_LIN(true, 256, 1); break;
         case 3: PBA_LAUNCH_LIN(true, 128, 4); break;
-        case 4: PBA_LAUNCH_LIN(true, 128, 3); break;
         case 5: PBA_LAUNCH_LIN(true, 512, 1); break;
-        default: PBA_LAUNCH_LIN(true, 256, 2); break;
+        case 2: PBA_LAUNCH_LIN(true, 256, 2); break;
+        default: PBA_LAUNCH_LIN(true, 128, 3); break;
       }
     } else {
-      PBA_LAUNCH_LIN(false, 256, 2);
+      PBA_LAUNCH_LIN(false, 128, 3);
     }
 #undef PBA_LAUNCH_LIN
     PBA_LAUNCH_CHECK();
