@@ -401,7 +401,7 @@ def run_ours(args):
             "level": f"finest ({meta['cam'].height}x{meta['cam'].width})",
             "parallelism": f"pair-sharded x{world}" if world > 1 else "single GPU",
             "l2": "inputs larger than L2: %.1f GB of resident texels" % (store.texel_bytes() / 1e9),
-            "precision": "fp64 geometry/residuals/Jacobians/b/cost, fp32 per-thread H partials",
+            "precision": "fp64 throughout (geometry, residuals, Jacobians, H/b/cost sums)",
             "gn_iteration_ms": ms_per_step,
             "setup_seconds": round(t_setup, 2),
             "graph_seconds": round(meta["graph_seconds"], 2),
