@@ -307,6 +307,8 @@ def run_ours(args):
         step()
     stream = torch.cuda.current_stream(device)
     local_level.kernel_events = []
+    if getattr(local_level, "has_solver", False):
+        local_level.solve_events = []
     launches0 = lib.pba_kernel_launches()
     if world > 1:
         dist.barrier()
@@ -324,7 +326,9 @@ def run_ours(args):
     elapsed_ms = e0.elapsed_time(e1)
     launches = (lib.pba_kernel_launches() - launches0) / args.steps
     lin_ms = [a.elapsed_time(b) for a, b in local_level.kernel_events]
+    solve_ms = [a.elapsed_time(b) for a, b in (local_level.solve_events or [])]
     local_level.kernel_events = None
+    local_level.solve_events = None
     t = torch.tensor([elapsed_ms], dtype=torch.float64, device=device)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -419,6 +423,7 @@ def run_ours(args):
             "traffic": traffic,
             "linearize_ms": lin_avg_ms,
             "linearize_share_of_step": lin_avg_ms / ms_per_step,
+            "solve_ms": statistics.mean(solve_ms) if solve_ms else None,
             "algorithmic_bytes_per_launch": shard_pp * BYTES_PER_PIXEL_PAIR,
         },
         "e2e": e2e,

@@ -3,14 +3,20 @@
 //
 // The damped normal matrix is symmetric positive definite whenever the
 // reference's LU succeeds (H is a sum of J^T W J with W > 0 and lam > 0), so
-// the device path factors it with a tiled right-looking fp64 Cholesky:
-//   per 64-column panel k:  potrf(diagonal tile) -> trsm(panel) -> syrk/gemm(trailing)
-// A per-tile non-zero map (filled after damping, updated as fill-in appears)
-// lets every kernel skip structurally-zero tiles, so block-banded systems
-// (corridor trajectories) cost O(n * band^2) instead of
-// O(n^3) while general graphs get the full dense factorisation.  A status
-// word reports a non-positive pivot — the reference's LinAlgError path
-// (solver.py:513-522).
+// the device path factors it with a tiled right-looking fp64 Cholesky on
+// 64x64 tiles.  Per panel k:
+//   potrf_inv : factor the diagonal tile in shared memory (8-column warp
+//               panels, 16 CTA barriers) and form its explicit inverse
+//   panel     : L_ik = A_ik L_kk^-T as a 64x64x64 product with that inverse
+//   syrk      : trailing update A_ij -= L_ik L_jk^T
+// A per-tile non-zero map (filled after damping, updated on fill-in) lets
+// every kernel skip structurally zero tiles, so block-banded systems
+// (corridor trajectories: bandwidth ~20 poses) cost O(n * band^2) while
+// general graphs get the full factorisation.  The substitutions use the
+// tile inverses: one CTA walks the tile rows, each step a short dot-product
+// gather over the non-zero tiles plus a 64x64 mat-vec.
+// A status word reports a non-positive pivot — the reference's LinAlgError
+// path (solver.py:513-522).
 
 #include <math.h>
 
@@ -20,25 +26,28 @@ namespace pba {
 namespace {
 
 constexpr int NB = 64;  // tile size
-
-struct SolveWork {
-  double* A;      // dim x dim (lower triangle used)
-  double* y;      // dim
-  int32_t* nz;    // T x T tile non-zero flags
-};
+constexpr int LD = NB + 1;
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+struct SolveWork {
+  double* A;     // dim x dim (lower triangle used)
+  double* Linv;  // T x NB x NB inverses of the diagonal tiles
+  double* y;     // dim
+  int32_t* nz;   // T x T tile non-zero flags
+};
+
 SolveWork carve(void* work, int dim) {
-  const int T = (dim + NB - 1) / NB;
+  const size_t T = (dim + NB - 1) / NB;
   char* p = static_cast<char*>(work);
   SolveWork w;
   w.A = reinterpret_cast<double*>(p);
   p += align_up((size_t)dim * dim * sizeof(double), 256);
+  w.Linv = reinterpret_cast<double*>(p);
+  p += align_up(T * NB * NB * sizeof(double), 256);
   w.y = reinterpret_cast<double*>(p);
   p += align_up((size_t)dim * sizeof(double), 256);
   w.nz = reinterpret_cast<int32_t*>(p);
-  (void)T;
   return w;
 }
 
@@ -60,104 +69,159 @@ __global__ void tile_flags_kernel(const double* __restrict__ A, int dim, int T,
     if (threadIdx.x == 0) nz[bi * T + bj] = 0;
     return;
   }
-  __shared__ int any;
-  if (threadIdx.x == 0) any = 0;
-  __syncthreads();
   int mine = 0;
   for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
     const int r = bi * NB + e / NB, c = bj * NB + e % NB;
     if (r < dim && c < dim && c <= r && A[(long)r * dim + c] != 0.0) mine = 1;
   }
-  if (mine) any = 1;
-  __syncthreads();
+  const int any = __syncthreads_or(mine);
   if (threadIdx.x == 0) nz[bi * T + bj] = any || bi == bj;
 }
 
-// Unblocked Cholesky of diagonal tile k in shared memory (one CTA).
-__global__ void potrf_kernel(double* __restrict__ A, int dim, int k, int32_t* __restrict__ status) {
-  __shared__ double a[NB][NB + 1];
+// Factor diagonal tile k in shared memory and store L_kk and L_kk^{-1}.
+// 256 threads.  Columns are processed in panels of 8: warp 0 factors the
+// panel with warp-synchronous steps, then all threads apply the rank-8
+// update to the trailing part of the tile.
+__global__ void __launch_bounds__(256) potrf_inv_kernel(double* __restrict__ A, int dim, int k,
+                                                        double* __restrict__ Linv,
+                                                        int32_t* __restrict__ status) {
+  extern __shared__ double psm[];
+  double(*a)[LD] = reinterpret_cast<double(*)[LD]>(psm);
+  double(*x)[LD] = reinterpret_cast<double(*)[LD]>(psm + NB * LD);
   __shared__ int bad;
   if (*status) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k0 = k * NB;
   const int n = min(NB, dim - k0);
-  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
+  for (int e = tid; e < NB * NB; e += blockDim.x) {
     const int r = e / NB, c = e % NB;
-    a[r][c] = (r < n && c <= r) ? A[(long)(k0 + r) * dim + k0 + c] : 0.0;
+    a[r][c] = (r < n && c <= r) ? A[(long)(k0 + r) * dim + k0 + c] : (r == c ? 1.0 : 0.0);
   }
-  if (threadIdx.x == 0) bad = 0;
+  if (tid == 0) bad = 0;
   __syncthreads();
-  for (int j = 0; j < n; ++j) {
-    if (threadIdx.x == 0) {
-      const double d = a[j][j];
-      if (!(d > 0.0) || !isfinite(d)) bad = 1;
-      a[j][j] = sqrt(d);
+  for (int c0 = 0; c0 < n; c0 += 8) {
+    const int c1 = min(c0 + 8, n);
+    if (warp == 0) {
+      for (int j = c0; j < c1; ++j) {
+        const double d = a[j][j];
+        if (!(d > 0.0) || !isfinite(d)) {
+          if (lane == 0) bad = 1;
+        }
+        const double piv = sqrt(d);
+        __syncwarp();
+        if (lane == 0) a[j][j] = piv;
+        for (int r = j + 1 + lane; r < n; r += 32) a[r][j] /= piv;
+        __syncwarp();
+        // update the remaining columns of this panel
+        for (int r = j + 1 + lane; r < n; r += 32) {
+          const double arj = a[r][j];
+          for (int c = j + 1; c < c1 && c <= r; ++c) a[r][c] -= arj * a[c][j];
+        }
+        __syncwarp();
+      }
     }
     __syncthreads();
     if (bad) break;
-    const double piv = a[j][j];
-    for (int r = j + 1 + threadIdx.x; r < n; r += blockDim.x) a[r][j] /= piv;
-    __syncthreads();
-    const int m = n - j - 1;
-    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-      const int r = j + 1 + e / m, c = j + 1 + e % m;
-      if (c <= r) a[r][c] -= a[r][j] * a[c][j];
+    // rank-(c1-c0) update of the trailing tile: a[r][c] -= sum_j a[r][j] a[c][j], c1 <= c <= r
+    const int m = n - c1;
+    for (int e = tid; e < m * m; e += blockDim.x) {
+      const int r = c1 + e / m, c = c1 + e % m;
+      if (c <= r) {
+        double s = 0.0;
+        for (int j = c0; j < c1; ++j) s += a[r][j] * a[c][j];
+        a[r][c] -= s;
+      }
     }
     __syncthreads();
   }
   if (bad) {
-    if (threadIdx.x == 0) *status = 1;
+    if (tid == 0) *status = 1;
     return;
   }
-  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
+  // x = L^{-1} (lower triangular), one column per thread (64 threads active)
+  if (tid < NB) {
+    const int j = tid;
+    for (int i = 0; i < NB; ++i) x[i][j] = 0.0;
+    if (j < n) {
+      x[j][j] = 1.0 / a[j][j];
+      for (int i = j + 1; i < n; ++i) {
+        double s = 0.0;
+        for (int m2 = j; m2 < i; ++m2) s += a[i][m2] * x[m2][j];
+        x[i][j] = -s / a[i][i];
+      }
+    }
+  }
+  __syncthreads();
+  double* Li = Linv + (long)k * NB * NB;
+  for (int e = tid; e < NB * NB; e += blockDim.x) {
     const int r = e / NB, c = e % NB;
+    Li[e] = (c <= r) ? x[r][c] : 0.0;
     if (r < n && c <= r) A[(long)(k0 + r) * dim + k0 + c] = a[r][c];
   }
 }
 
-// L21 = A21 * L11^{-T} for row tiles bi > k with a non-zero (bi, k) tile.
-// One CTA per row tile; each thread owns one row and substitutes forward.
-__global__ void trsm_kernel(double* __restrict__ A, int dim, int k, int T,
-                            const int32_t* __restrict__ nz, const int32_t* __restrict__ status) {
-  if (*status) return;
-  const int bi = k + 1 + blockIdx.x;
-  if (!nz[bi * T + k]) return;
-  extern __shared__ double tsm[];
-  double(*L)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(tsm);
-  double(*X)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(tsm + NB * (NB + 1));
-  const int k0 = k * NB, r0 = bi * NB;
-  const int nk = min(NB, dim - k0), nr = min(NB, dim - r0);
-  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
-    const int r = e / NB, c = e % NB;
-    L[r][c] = (r < nk && c <= r) ? A[(long)(k0 + r) * dim + k0 + c] : 0.0;
-    X[r][c] = (r < nr && c < nk) ? A[(long)(r0 + r) * dim + k0 + c] : 0.0;
-  }
-  __syncthreads();
-  const int r = threadIdx.x;
-  if (r < nr) {
-    for (int j = 0; j < nk; ++j) {
-      double s = X[r][j];
-      for (int m = 0; m < j; ++m) s -= X[r][m] * L[j][m];
-      X[r][j] = s / L[j][j];
+// out(64x64) = P(64x64) * Q(64x64)^T with P, Q in shared memory (LD stride);
+// each of 256 threads owns a 4x4 block of outputs.
+__device__ __forceinline__ void tile_abt(const double* P, const double* Q, double acc[4][4]) {
+  const int tr = threadIdx.x / 16, tc = threadIdx.x % 16;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
+  for (int kk = 0; kk < NB; ++kk) {
+    double xv[4], yv[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      xv[a] = P[(tr + 16 * a) * LD + kk];
+      yv[a] = Q[(tc + 16 * a) * LD + kk];
     }
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
-    const int rr = e / NB, c = e % NB;
-    if (rr < nr && c < nk) A[(long)(r0 + rr) * dim + k0 + c] = X[rr][c];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[a][c] = fma(xv[a], yv[c], acc[a][c]);
   }
 }
 
-// Trailing update C(bi,bj) -= L(bi,k) L(bj,k)^T for bi >= bj > k.  One CTA
-// (256 threads, 4x4 outputs each) per lower tile; skipped when either panel
-// tile is zero.  Marks the target tile non-zero (fill-in).
+// L_ik = A_ik L_kk^{-T} for the non-zero tiles below diagonal tile k.
+__global__ void __launch_bounds__(256) panel_kernel(double* __restrict__ A, int dim, int k, int T,
+                                                    const int32_t* __restrict__ nz,
+                                                    const double* __restrict__ Linv,
+                                                    const int32_t* __restrict__ status) {
+  if (*status) return;
+  const int bi = k + 1 + blockIdx.x;
+  if (!nz[bi * T + k]) return;
+  extern __shared__ double smem[];
+  double* P = smem;
+  double* Q = smem + NB * LD;
+  const int k0 = k * NB, r0 = bi * NB;
+  const int nk = min(NB, dim - k0), nr = min(NB, dim - r0);
+  const double* Li = Linv + (long)k * NB * NB;
+  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
+    const int r = e / NB, c = e % NB;
+    P[r * LD + c] = (r < nr && c < nk) ? A[(long)(r0 + r) * dim + k0 + c] : 0.0;
+    Q[r * LD + c] = Li[e];
+  }
+  __syncthreads();
+  double acc[4][4];
+  tile_abt(P, Q, acc);
+  const int tr = threadIdx.x / 16, tc = threadIdx.x % 16;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int r = tr + 16 * a, col = tc + 16 * c;
+      if (r < nr && col < nk) A[(long)(r0 + r) * dim + k0 + col] = acc[a][c];
+    }
+}
+
+// Trailing update C(bi,bj) -= L(bi,k) L(bj,k)^T for bi >= bj > k, skipping
+// tiles whose panel factors are zero; marks fill-in.
 __global__ void __launch_bounds__(256) syrk_kernel(double* __restrict__ A, int dim, int k, int T,
                                                    int32_t* __restrict__ nz,
                                                    const int32_t* __restrict__ status) {
   if (*status) return;
-  // blockIdx.x enumerates lower tiles of the trailing (T-k-1)^2 matrix.
   const int m = T - k - 1;
   const int t = blockIdx.x;
-  // invert t = bi*(bi+1)/2 + bj with 0 <= bj <= bi < m
   int bi = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
   while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
   while (bi * (bi + 1) / 2 > t) --bi;
@@ -166,34 +230,19 @@ __global__ void __launch_bounds__(256) syrk_kernel(double* __restrict__ A, int d
   const int ti = k + 1 + bi, tj = k + 1 + bj;
   if (!nz[ti * T + k] || !nz[tj * T + k]) return;
   extern __shared__ double smem[];
-  double* Pi = smem;               // NB x (NB+1)
-  double* Pj = smem + NB * (NB + 1);
+  double* Pi = smem;
+  double* Pj = smem + NB * LD;
   const int k0 = k * NB, ri = ti * NB, rj = tj * NB;
   const int nk = min(NB, dim - k0);
   for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
     const int r = e / NB, c = e % NB;
-    Pi[r * (NB + 1) + c] = (ri + r < dim && c < nk) ? A[(long)(ri + r) * dim + k0 + c] : 0.0;
-    Pj[r * (NB + 1) + c] = (rj + r < dim && c < nk) ? A[(long)(rj + r) * dim + k0 + c] : 0.0;
+    Pi[r * LD + c] = (ri + r < dim && c < nk) ? A[(long)(ri + r) * dim + k0 + c] : 0.0;
+    Pj[r * LD + c] = (rj + r < dim && c < nk) ? A[(long)(rj + r) * dim + k0 + c] : 0.0;
   }
   __syncthreads();
-  const int tr = threadIdx.x / 16, tc = threadIdx.x % 16;
   double acc[4][4];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
-  for (int kk = 0; kk < NB; ++kk) {
-    double x[4], y[4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      x[a] = Pi[(tr + 16 * a) * (NB + 1) + kk];
-      y[a] = Pj[(tc + 16 * a) * (NB + 1) + kk];
-    }
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) acc[a][c] += x[a] * y[c];
-  }
+  tile_abt(Pi, Pj, acc);
+  const int tr = threadIdx.x / 16, tc = threadIdx.x % 16;
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -204,71 +253,65 @@ __global__ void __launch_bounds__(256) syrk_kernel(double* __restrict__ A, int d
   if (threadIdx.x == 0) nz[ti * T + tj] = 1;
 }
 
-// Forward (L y = -b) and backward (L^T x = y) substitution in one CTA,
-// tile by tile, skipping zero tiles.
+// Forward (L y = -b) and backward (L^T x = y) substitution in one CTA of 1024
+// threads with the tile inverses: per tile row a gather over the non-zero
+// tiles (16 threads per row, shuffle-reduced), then a 64x64 mat-vec.
 __global__ void __launch_bounds__(1024) trisolve_kernel(const double* __restrict__ A, int dim, int T,
                                                          const int32_t* __restrict__ nz,
+                                                         const double* __restrict__ Linv,
                                                          const double* __restrict__ b,
                                                          double* __restrict__ y,
                                                          double* __restrict__ x,
                                                          const int32_t* __restrict__ status) {
   if (*status) return;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
-  for (int i = tid; i < dim; i += blockDim.x) y[i] = -b[i];
-  __syncthreads();
-  // forward
+  __shared__ double r[NB];
+  const int tid = threadIdx.x;
+  const int row = tid >> 4, sub = tid & 15;  // 64 rows x 16 lanes
+  // forward: y_k = Linv_kk (-b_k - sum_{j<k} L_kj y_j)
   for (int k = 0; k < T; ++k) {
     const int k0 = k * NB, nk = min(NB, dim - k0);
-    if (warp == 0) {
-      for (int j = 0; j < nk; ++j) {
-        const double yj = y[k0 + j] / A[(long)(k0 + j) * dim + k0 + j];
-        __syncwarp();
-        if (lane == 0) y[k0 + j] = yj;
-        for (int r = j + 1 + lane; r < nk; r += 32) y[k0 + r] -= A[(long)(k0 + r) * dim + k0 + j] * yj;
-        __syncwarp();
+    double s = 0.0;
+    if (row < nk) {
+      for (int j = 0; j < k; ++j) {
+        if (!nz[k * T + j]) continue;
+        const double* Lr = A + (long)(k0 + row) * dim + j * NB;
+        const double* yj = y + j * NB;
+        for (int c = sub; c < NB; c += 16) s += Lr[c] * yj[c];
       }
     }
-    __syncthreads();
-    // update rows of non-zero tiles below
-    for (int bi = k + 1; bi < T; ++bi) {
-      if (!nz[bi * T + k]) continue;
-      const int r0 = bi * NB, nr = min(NB, dim - r0);
-      for (int r = warp; r < nr; r += nwarp) {
-        const double* row = A + (long)(r0 + r) * dim + k0;
-        double s = 0.0;
-        for (int c = lane; c < nk; c += 32) s += row[c] * y[k0 + c];
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-        if (lane == 0) y[r0 + r] -= s;
-      }
-    }
+    for (int off = 8; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (sub == 0) r[row] = (row < nk) ? -b[k0 + row] - s : 0.0;
+    __syncthreads();
+    const double* Li = Linv + (long)k * NB * NB;
+    double t = 0.0;
+    for (int c = sub; c <= row; c += 16) t += Li[row * NB + c] * r[c];
+#pragma unroll
+    for (int off = 8; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+    if (sub == 0 && row < nk) y[k0 + row] = t;
     __syncthreads();
   }
-  // backward: x = L^{-T} y
-  for (int i = tid; i < dim; i += blockDim.x) x[i] = y[i];
-  __syncthreads();
+  // backward: x_k = Linv_kk^T (y_k - sum_{i>k} L_ik^T x_i)
   for (int k = T - 1; k >= 0; --k) {
     const int k0 = k * NB, nk = min(NB, dim - k0);
-    // subtract contributions of already-solved tiles below: x_k -= L(bi,k)^T x_bi
-    for (int c = tid; c < nk; c += blockDim.x) {
-      double s = 0.0;
-      for (int bi = k + 1; bi < T; ++bi) {
-        if (!nz[bi * T + k]) continue;
-        const int r0 = bi * NB, nr = min(NB, dim - r0);
-        for (int r = 0; r < nr; ++r) s += A[(long)(r0 + r) * dim + k0 + c] * x[r0 + r];
+    double s = 0.0;
+    if (row < nk) {
+      for (int i = k + 1; i < T; ++i) {
+        if (!nz[i * T + k]) continue;
+        const int i0 = i * NB, ni = min(NB, dim - i0);
+        for (int rr = sub; rr < ni; rr += 16) s += A[(long)(i0 + rr) * dim + k0 + row] * x[i0 + rr];
       }
-      x[k0 + c] -= s;
     }
+#pragma unroll
+    for (int off = 8; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (sub == 0) r[row] = (row < nk) ? y[k0 + row] - s : 0.0;
     __syncthreads();
-    if (warp == 0) {
-      for (int j = nk - 1; j >= 0; --j) {
-        const double xj = x[k0 + j] / A[(long)(k0 + j) * dim + k0 + j];
-        __syncwarp();
-        if (lane == 0) x[k0 + j] = xj;
-        for (int r = lane; r < j; r += 32) x[k0 + r] -= A[(long)(k0 + j) * dim + k0 + r] * xj;
-        __syncwarp();
-      }
-    }
+    const double* Li = Linv + (long)k * NB * NB;
+    double t = 0.0;
+    for (int c = row + sub; c < NB; c += 16) t += Li[c * NB + row] * r[c];
+#pragma unroll
+    for (int off = 8; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+    if (sub == 0 && row < nk) x[k0 + row] = t;
     __syncthreads();
   }
 }
@@ -282,6 +325,7 @@ extern "C" size_t pba_solve_work_bytes(int32_t dim) {
   if (dim <= 0) return 0;
   const size_t T = (dim + NB - 1) / NB;
   return align_up((size_t)dim * dim * sizeof(double), 256) +
+         align_up(T * NB * NB * sizeof(double), 256) +
          align_up((size_t)dim * sizeof(double), 256) + align_up(T * T * sizeof(int32_t), 256);
 }
 
@@ -298,23 +342,25 @@ extern "C" int pba_solve_dense(const double* H, const double* b, int32_t dim, do
   PBA_LAUNCH_CHECK();
   tile_flags_kernel<<<dim3(T, T), 256, 0, st>>>(w.A, dim, T, w.nz);
   PBA_LAUNCH_CHECK();
-  const int syrk_smem = 2 * NB * (NB + 1) * sizeof(double);
+  const int tile_smem = 2 * NB * LD * sizeof(double);
   PBA_CUDA_TRY(cudaFuncSetAttribute(syrk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    syrk_smem));
-  PBA_CUDA_TRY(cudaFuncSetAttribute(trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    syrk_smem));
+                                    tile_smem));
+  PBA_CUDA_TRY(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    tile_smem));
+  PBA_CUDA_TRY(cudaFuncSetAttribute(potrf_inv_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));
   for (int k = 0; k < T; ++k) {
-    potrf_kernel<<<1, 256, 0, st>>>(w.A, dim, k, status);
+    potrf_inv_kernel<<<1, 256, tile_smem, st>>>(w.A, dim, k, w.Linv, status);
     PBA_LAUNCH_CHECK();
     const int m = T - k - 1;
     if (m > 0) {
-      trsm_kernel<<<m, NB, syrk_smem, st>>>(w.A, dim, k, T, w.nz, status);
+      panel_kernel<<<m, 256, tile_smem, st>>>(w.A, dim, k, T, w.nz, w.Linv, status);
       PBA_LAUNCH_CHECK();
-      syrk_kernel<<<m * (m + 1) / 2, 256, syrk_smem, st>>>(w.A, dim, k, T, w.nz, status);
+      syrk_kernel<<<m * (m + 1) / 2, 256, tile_smem, st>>>(w.A, dim, k, T, w.nz, status);
       PBA_LAUNCH_CHECK();
     }
   }
-  trisolve_kernel<<<1, 1024, 0, st>>>(w.A, dim, T, w.nz, b, w.y, delta, status);
+  trisolve_kernel<<<1, 1024, 0, st>>>(w.A, dim, T, w.nz, w.Linv, b, w.y, delta, status);
   PBA_LAUNCH_CHECK();
   return PBA_OK;
 }

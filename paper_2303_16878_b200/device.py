@@ -154,6 +154,7 @@ class DeviceLevel:
         self.cfg = cfg
         self.level = level
         self.kernel_events = None  # list -> (start, stop) CUDA events per pba_linearize call
+        self.solve_events = None   # same for pba_solve_dense
         self.n_poses = len(problems[0].graph.nodes)
         self.gauge = problems[0].gauge_index
         self.ccfg = config_struct(cfg)
@@ -301,10 +302,18 @@ class DeviceLevel:
                                         _stream_ptr(self.device)), "pba_sum_totals")
 
     def solve(self, which: int, lam: float, status_ptr: int) -> None:
+        ev = self.solve_events
+        if ev is not None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record(torch.cuda.current_stream(self.device))
         N.check(self.lib.pba_solve_dense(self.H[which].data_ptr(), self.b[which].data_ptr(),
                                          self.dim, float(lam), self.work.data_ptr(),
                                          self.delta.data_ptr(), status_ptr,
                                          _stream_ptr(self.device)), "pba_solve_dense")
+        if ev is not None:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record(torch.cuda.current_stream(self.device))
+            ev.append((e0, e1))
 
     def apply_step(self, src: int, dst: int, status_ptr: int) -> None:
         N.check(self.lib.pba_apply_step(self.poses[src].data_ptr(), self.gens[src].data_ptr(),
