@@ -181,13 +181,17 @@ int pba_assemble(const double* records, int32_t n_pairs, int32_t n_free, const i
 int pba_sum_totals(const double* records, int32_t n_pairs, double* totals, void* stream);
 
 /* ---- linear solve: np.linalg.solve(H + lam*diag(H), -b) (solver.py:510-512)
- * Dense fp64 Cholesky of the damped system.  H, b: device inputs (not
- * modified).  work: device, pba_solve_work_bytes(dim) bytes.  delta: device
- * output.  status: device int32 written 0 on success, 1 when the damped
- * matrix is not positive definite (the reference's LinAlgError). */
+ * Dense fp64 Cholesky of the damped system on 64x64 tiles.  H, b: device
+ * inputs (not modified).  tile_env: optional host array of ceil(dim/64)
+ * ints, tile_env[i] = first tile column that may be non-zero in tile row i
+ * (the matrix envelope; Cholesky fill-in never leaves it) — NULL means dense.
+ * work: device, pba_solve_work_bytes(dim) bytes.  delta: device output.
+ * status: device int32 written 0 on success, 1 when the damped matrix is
+ * not positive definite (the reference's LinAlgError). */
 size_t pba_solve_work_bytes(int32_t dim);
-int pba_solve_dense(const double* H, const double* b, int32_t dim, double lam, void* work,
-                    double* delta, int32_t* status, void* stream);
+int pba_solve_dense(const double* H, const double* b, int32_t dim, double lam,
+                    const int32_t* tile_env, void* work, double* delta, int32_t* status,
+                    void* stream);
 
 /* ---- pose update: _LevelProblem.apply_step (solver.py:451-460) --------
  * poses_out[k] = poses_in[k] * exp(delta[slot_k]) for every non-gauge pose

@@ -20,6 +20,8 @@
 
 #include <math.h>
 
+#include <vector>
+
 #include "pba_common.cuh"
 
 namespace pba {
@@ -52,20 +54,21 @@ SolveWork carve(void* work, int dim) {
 }
 
 __global__ void damp_copy_kernel(const double* __restrict__ H, int dim, double lam,
-                                 double* __restrict__ A) {
+                                 const int32_t* __restrict__ env, double* __restrict__ A) {
   const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (long)dim * dim) return;
   const int i = (int)(t / dim), j = (int)(t - (long)i * dim);
-  if (j > i) return;
+  if (j > i || j / NB < env[i / NB]) return;
   const double h = H[t];
   A[t] = (i == j) ? h + lam * h : h;  // h + lam * np.diag(np.diag(h))
 }
 
-// One CTA per lower tile: flag it if any entry is non-zero.
+// One CTA per lower tile: flag it if any entry is non-zero.  Tiles left of
+// the row's envelope are structurally zero and never touched.
 __global__ void tile_flags_kernel(const double* __restrict__ A, int dim, int T,
-                                  int32_t* __restrict__ nz) {
+                                  const int32_t* __restrict__ env, int32_t* __restrict__ nz) {
   const int bi = blockIdx.y, bj = blockIdx.x;
-  if (bj > bi) {
+  if (bj > bi || bj < env[bi]) {
     if (threadIdx.x == 0) nz[bi * T + bj] = 0;
     return;
   }
@@ -138,20 +141,36 @@ __global__ void __launch_bounds__(256) potrf_inv_kernel(double* __restrict__ A, 
     if (tid == 0) *status = 1;
     return;
   }
-  // x = L^{-1} (lower triangular), one column per thread (64 threads active)
-  if (tid < NB) {
-    const int j = tid;
-    for (int i = 0; i < NB; ++i) x[i][j] = 0.0;
-    if (j < n) {
-      x[j][j] = 1.0 / a[j][j];
-      for (int i = j + 1; i < n; ++i) {
-        double s = 0.0;
-        for (int m2 = j; m2 < i; ++m2) s += a[i][m2] * x[m2][j];
-        x[i][j] = -s / a[i][i];
-      }
-    }
+  // x = L^{-1} by a row sweep over 8-row blocks: the 64 column threads solve
+  // the 8x8 diagonal block of their column (no barrier), then all threads
+  // apply the rank-8 update to the rows below (one barrier per block).
+  for (int e = tid; e < NB * NB; e += blockDim.x) {
+    const int r = e / NB, c = e % NB;
+    x[r][c] = (r == c) ? 1.0 : 0.0;
   }
   __syncthreads();
+  for (int c0 = 0; c0 < n; c0 += 8) {
+    const int c1 = min(c0 + 8, n);
+    if (tid < NB) {
+      const int col = tid;
+      for (int j = c0; j < c1; ++j) {
+        const double xj = x[j][col] / a[j][j];
+        x[j][col] = xj;
+        for (int i = j + 1; i < c1; ++i) x[i][col] -= a[i][j] * xj;
+      }
+    }
+    __syncthreads();
+    const int m = n - c1;
+    for (int e = tid; e < m * NB; e += blockDim.x) {
+      const int i = c1 + e / NB, col = e % NB;
+      if (col <= i) {
+        double s = 0.0;
+        for (int j = c0; j < c1; ++j) s += a[i][j] * x[j][col];
+        x[i][col] -= s;
+      }
+    }
+    __syncthreads();
+  }
   double* Li = Linv + (long)k * NB * NB;
   for (int e = tid; e < NB * NB; e += blockDim.x) {
     const int r = e / NB, c = e % NB;
@@ -189,7 +208,7 @@ __global__ void __launch_bounds__(256) panel_kernel(double* __restrict__ A, int 
                                                     const int32_t* __restrict__ status) {
   if (*status) return;
   const int bi = k + 1 + blockIdx.x;
-  if (!nz[bi * T + k]) return;
+  if (bi >= T || !nz[bi * T + k]) return;
   extern __shared__ double smem[];
   double* P = smem;
   double* Q = smem + NB * LD;
@@ -257,6 +276,8 @@ __global__ void __launch_bounds__(256) syrk_kernel(double* __restrict__ A, int d
 // threads with the tile inverses: per tile row a gather over the non-zero
 // tiles (16 threads per row, shuffle-reduced), then a 64x64 mat-vec.
 __global__ void __launch_bounds__(1024) trisolve_kernel(const double* __restrict__ A, int dim, int T,
+                                                         const int32_t* __restrict__ env,
+                                                         const int32_t* __restrict__ last,
                                                          const int32_t* __restrict__ nz,
                                                          const double* __restrict__ Linv,
                                                          const double* __restrict__ b,
@@ -272,7 +293,7 @@ __global__ void __launch_bounds__(1024) trisolve_kernel(const double* __restrict
     const int k0 = k * NB, nk = min(NB, dim - k0);
     double s = 0.0;
     if (row < nk) {
-      for (int j = 0; j < k; ++j) {
+      for (int j = env[k]; j < k; ++j) {
         if (!nz[k * T + j]) continue;
         const double* Lr = A + (long)(k0 + row) * dim + j * NB;
         const double* yj = y + j * NB;
@@ -296,7 +317,7 @@ __global__ void __launch_bounds__(1024) trisolve_kernel(const double* __restrict
     const int k0 = k * NB, nk = min(NB, dim - k0);
     double s = 0.0;
     if (row < nk) {
-      for (int i = k + 1; i < T; ++i) {
+      for (int i = k + 1; i <= last[k]; ++i) {
         if (!nz[i * T + k]) continue;
         const int i0 = i * NB, ni = min(NB, dim - i0);
         for (int rr = sub; rr < ni; rr += 16) s += A[(long)(i0 + rr) * dim + k0 + row] * x[i0 + rr];
@@ -326,21 +347,46 @@ extern "C" size_t pba_solve_work_bytes(int32_t dim) {
   const size_t T = (dim + NB - 1) / NB;
   return align_up((size_t)dim * dim * sizeof(double), 256) +
          align_up(T * NB * NB * sizeof(double), 256) +
-         align_up((size_t)dim * sizeof(double), 256) + align_up(T * T * sizeof(int32_t), 256);
+         align_up((size_t)dim * sizeof(double), 256) + align_up(T * T * sizeof(int32_t), 256) +
+         align_up(2 * T * sizeof(int32_t), 256);
 }
 
 extern "C" int pba_solve_dense(const double* H, const double* b, int32_t dim, double lam,
-                               void* work, double* delta, int32_t* status, void* stream) {
+                               const int32_t* tile_env, void* work, double* delta,
+                               int32_t* status, void* stream) {
   PBA_ARG_CHECK(dim > 0, "dim must be positive");
   PBA_ARG_CHECK(H && b && work && delta && status, "NULL buffer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   SolveWork w = carve(work, dim);
   const int T = (dim + NB - 1) / NB;
+  // envelope: env[i] = first tile column that can be non-zero in tile row i
+  // (fill-in never leaves it); last[k] = last tile row whose envelope reaches k
+  std::vector<int32_t> env(T), last(T);
+  for (int i = 0; i < T; ++i) {
+    int e = tile_env ? tile_env[i] : 0;
+    PBA_ARG_CHECK(e >= 0 && e <= i, "tile_env[i] must lie in [0, i]");
+    env[i] = e;
+  }
+  for (int k = 0; k < T; ++k) {
+    int l = k;
+    for (int i = k + 1; i < T; ++i)
+      if (env[i] <= k) l = i;
+    last[k] = l;
+  }
+  int32_t* d_env = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(w.nz) +
+                                              align_up((size_t)T * T * sizeof(int32_t), 256));
+  int32_t* d_last = d_env + T;
+  // the tables are tiny; copy them with the stream so the call stays asynchronous
+  static thread_local std::vector<int32_t> staging;
+  staging.assign(env.begin(), env.end());
+  staging.insert(staging.end(), last.begin(), last.end());
+  PBA_CUDA_TRY(cudaMemcpyAsync(d_env, staging.data(), 2 * T * sizeof(int32_t),
+                               cudaMemcpyHostToDevice, st));
   PBA_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int32_t), st));
   const long n2 = (long)dim * dim;
-  damp_copy_kernel<<<(unsigned)((n2 + 255) / 256), 256, 0, st>>>(H, dim, lam, w.A);
+  damp_copy_kernel<<<(unsigned)((n2 + 255) / 256), 256, 0, st>>>(H, dim, lam, d_env, w.A);
   PBA_LAUNCH_CHECK();
-  tile_flags_kernel<<<dim3(T, T), 256, 0, st>>>(w.A, dim, T, w.nz);
+  tile_flags_kernel<<<dim3(T, T), 256, 0, st>>>(w.A, dim, T, d_env, w.nz);
   PBA_LAUNCH_CHECK();
   const int tile_smem = 2 * NB * LD * sizeof(double);
   PBA_CUDA_TRY(cudaFuncSetAttribute(syrk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -352,7 +398,7 @@ extern "C" int pba_solve_dense(const double* H, const double* b, int32_t dim, do
   for (int k = 0; k < T; ++k) {
     potrf_inv_kernel<<<1, 256, tile_smem, st>>>(w.A, dim, k, w.Linv, status);
     PBA_LAUNCH_CHECK();
-    const int m = T - k - 1;
+    const int m = last[k] - k;  // tile rows below k inside the envelope
     if (m > 0) {
       panel_kernel<<<m, 256, tile_smem, st>>>(w.A, dim, k, T, w.nz, w.Linv, status);
       PBA_LAUNCH_CHECK();
@@ -360,7 +406,8 @@ extern "C" int pba_solve_dense(const double* H, const double* b, int32_t dim, do
       PBA_LAUNCH_CHECK();
     }
   }
-  trisolve_kernel<<<1, 1024, 0, st>>>(w.A, dim, T, w.nz, w.Linv, b, w.y, delta, status);
+  trisolve_kernel<<<1, 1024, 0, st>>>(w.A, dim, T, d_env, d_last, w.nz, w.Linv, b, w.y, delta,
+                                      status);
   PBA_LAUNCH_CHECK();
   return PBA_OK;
 }

@@ -51,6 +51,27 @@ def chunk_pixels_for(total_pixels: int) -> int:
     return THREADS_PER_CHUNK * ppt
 
 
+def tile_envelope(slot_of_pose, pose_i, pose_j, dim, tile=64) -> np.ndarray:
+    """First possibly non-zero 64-wide tile column of every tile row of the
+    damped normal matrix: the envelope of its block sparsity (diagonal
+    blocks + one off-diagonal block per pair of free poses).  Cholesky
+    fill-in stays inside it, so the solver never touches the rest."""
+    n_free = int((slot_of_pose >= 0).sum())
+    first = np.arange(n_free, dtype=np.int64)  # first non-zero block column per block row
+    si = slot_of_pose[pose_i]
+    sj = slot_of_pose[pose_j]
+    both = (si >= 0) & (sj >= 0)
+    lo = np.minimum(si[both], sj[both])
+    hi = np.maximum(si[both], sj[both])
+    np.minimum.at(first, hi, lo)
+    T = (dim + tile - 1) // tile
+    env = np.arange(T, dtype=np.int32)
+    rows = np.arange(dim)
+    first_col = 6 * first[rows // 6]
+    np.minimum.at(env, rows // tile, (first_col // tile).astype(np.int32))
+    return np.ascontiguousarray(env, dtype=np.int32)
+
+
 class FrameStore:
     """Device-resident texel images, one per cue image object."""
 
@@ -266,6 +287,7 @@ class DeviceLevel:
         self.work = torch.empty(max(8, int(lib.pba_solve_work_bytes(d))), dtype=torch.uint8,
                                 device=dev)
         self.delta = torch.zeros(d, dtype=torch.float64, device=dev)
+        self.tile_env = tile_envelope(slot, self.pose_i, self.pose_j, self.dim)
         self.has_solver = True
 
     # ---- primitive steps -----------------------------------------------------
@@ -307,7 +329,8 @@ class DeviceLevel:
             e0 = torch.cuda.Event(enable_timing=True)
             e0.record(torch.cuda.current_stream(self.device))
         N.check(self.lib.pba_solve_dense(self.H[which].data_ptr(), self.b[which].data_ptr(),
-                                         self.dim, float(lam), self.work.data_ptr(),
+                                         self.dim, float(lam), self.tile_env.ctypes.data,
+                                         self.work.data_ptr(),
                                          self.delta.data_ptr(), status_ptr,
                                          _stream_ptr(self.device)), "pba_solve_dense")
         if ev is not None:

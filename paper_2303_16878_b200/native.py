@@ -83,7 +83,7 @@ _SIGNATURES = {
                                     _vp, _vp]),
     "pba_sum_totals": (ctypes.c_int, [_vp, _i32, _vp, _vp]),
     "pba_solve_work_bytes": (_sz, [_i32]),
-    "pba_solve_dense": (ctypes.c_int, [_vp, _vp, _i32, _dbl, _vp, _vp, _vp, _vp]),
+    "pba_solve_dense": (ctypes.c_int, [_vp, _vp, _i32, _dbl, _vp, _vp, _vp, _vp, _vp]),
     "pba_apply_step": (ctypes.c_int, [_vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp]),
     "pba_atan2_batch": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp]),
 }

@@ -234,7 +234,7 @@ def test_under_constrained_raises():
 # ---------------------------------------------------------------------------
 # K3 / K4 kernels in isolation
 # ---------------------------------------------------------------------------
-def _dense_solve(H, b, lam):
+def _dense_solve(H, b, lam, env=None):
     from paper_2303_16878_b200 import native as N
 
     lib = N.load()
@@ -243,7 +243,8 @@ def _dense_solve(H, b, lam):
     work = torch.empty(int(lib.pba_solve_work_bytes(dim)), dtype=torch.uint8, device="cuda")
     delta = torch.zeros(dim, dtype=torch.float64, device="cuda")
     status = torch.zeros(1, dtype=torch.int32, device="cuda")
-    N.check(lib.pba_solve_dense(Ht.data_ptr(), bt.data_ptr(), dim, lam, work.data_ptr(),
+    env_p = None if env is None else env.ctypes.data
+    N.check(lib.pba_solve_dense(Ht.data_ptr(), bt.data_ptr(), dim, lam, env_p, work.data_ptr(),
                                 delta.data_ptr(), status.data_ptr(),
                                 torch.cuda.current_stream().cuda_stream), "solve")
     return delta.cpu().numpy(), int(status.item())
@@ -258,10 +259,17 @@ def test_dense_cholesky_matches_numpy_solve(dim, band):
     H = A @ A.T + 1e-3 * np.eye(dim)
     b = rng.normal(size=dim)
     lam = 1e-3
+    ref = np.linalg.solve(H + lam * np.diag(np.diag(H)), -b)
     x, st = _dense_solve(H, b, lam)
     assert st == 0
-    ref = np.linalg.solve(H + lam * np.diag(np.diag(H)), -b)
     assert np.max(np.abs(x - ref)) <= 1e-8 * np.max(np.abs(ref))
+    if band is not None:  # envelope-restricted factorisation gives the same answer
+        T = (dim + 63) // 64
+        first = np.array([np.nonzero(H[r, : r + 1])[0][0] for r in range(dim)])
+        env = np.array([first[t * 64: (t + 1) * 64].min() // 64 for t in range(T)], np.int32)
+        x2, st = _dense_solve(H, b, lam, env)
+        assert st == 0
+        assert np.max(np.abs(x2 - ref)) <= 1e-8 * np.max(np.abs(ref))
 
 
 def test_dense_cholesky_reports_singular():

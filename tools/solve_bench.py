@@ -33,13 +33,19 @@ def run(dim, band, reps):
     delta = torch.zeros(dim, dtype=torch.float64, device="cuda")
     st = torch.zeros(1, dtype=torch.int32, device="cuda")
     stream = torch.cuda.current_stream().cuda_stream
+    T = (dim + 63) // 64
+    if band is None or band >= dim:
+        env = np.zeros(T, np.int32)
+    else:
+        env = np.array([max(0, (t * 64 - band) // 64) for t in range(T)], np.int32)
     times = []
     for r in range(reps + 2):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        N.check(lib.pba_solve_dense(H.data_ptr(), b.data_ptr(), dim, 1e-3, work.data_ptr(),
-                                    delta.data_ptr(), st.data_ptr(), stream), "solve")
+        N.check(lib.pba_solve_dense(H.data_ptr(), b.data_ptr(), dim, 1e-3, env.ctypes.data,
+                                    work.data_ptr(), delta.data_ptr(), st.data_ptr(), stream),
+                "solve")
         e1.record()
         torch.cuda.synchronize()
         if r >= 2:
