@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(256) potrf_inv_kernel(double* __restrict__ A, 
   double(*x)[LD] = reinterpret_cast<double(*)[LD]>(psm + NB * LD);
   __shared__ int bad;
   if (*status) return;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const int k0 = k * NB;
   const int n = min(NB, dim - k0);
   for (int e = tid; e < NB * NB; e += blockDim.x) {
@@ -102,25 +102,29 @@ __global__ void __launch_bounds__(256) potrf_inv_kernel(double* __restrict__ A, 
   }
   if (tid == 0) bad = 0;
   __syncthreads();
+  __shared__ double rdiag[NB];
   for (int c0 = 0; c0 < n; c0 += 8) {
     const int c1 = min(c0 + 8, n);
-    if (warp == 0) {
+    if (tid < NB) {
+      // panel of 8 columns: thread r owns row r; steps are separated by a
+      // 64-thread named barrier (warps 0-1 only)
+      const int r = tid;
       for (int j = c0; j < c1; ++j) {
-        const double d = a[j][j];
-        if (!(d > 0.0) || !isfinite(d)) {
-          if (lane == 0) bad = 1;
+        if (r == j) {
+          const double d = a[j][j];
+          if (!(d > 0.0) || !isfinite(d)) bad = 1;
+          const double piv = sqrt(d);
+          a[j][j] = piv;
+          rdiag[j] = 1.0 / piv;
         }
-        const double piv = sqrt(d);
-        __syncwarp();
-        if (lane == 0) a[j][j] = piv;
-        for (int r = j + 1 + lane; r < n; r += 32) a[r][j] /= piv;
-        __syncwarp();
-        // update the remaining columns of this panel
-        for (int r = j + 1 + lane; r < n; r += 32) {
-          const double arj = a[r][j];
-          for (int c = j + 1; c < c1 && c <= r; ++c) a[r][c] -= arj * a[c][j];
+        asm volatile("bar.sync 1, 64;");
+        if (r > j && r < n) {
+          const double arj = a[r][j] * rdiag[j];
+          a[r][j] = arj;
+          const int cmax = min(c1, r + 1);
+          for (int c = j + 1; c < cmax; ++c) a[r][c] -= arj * a[c][j];
         }
-        __syncwarp();
+        asm volatile("bar.sync 1, 64;");
       }
     }
     __syncthreads();
@@ -154,7 +158,7 @@ __global__ void __launch_bounds__(256) potrf_inv_kernel(double* __restrict__ A, 
     if (tid < NB) {
       const int col = tid;
       for (int j = c0; j < c1; ++j) {
-        const double xj = x[j][col] / a[j][j];
+        const double xj = x[j][col] * rdiag[j];
         x[j][col] = xj;
         for (int i = j + 1; i < c1; ++i) x[i][col] -= a[i][j] * xj;
       }
