@@ -82,10 +82,10 @@ __global__ void tile_flags_kernel(const double* __restrict__ A, int dim, int T,
 }
 
 // Factor diagonal tile k in shared memory and store L_kk and L_kk^{-1}.
-// 256 threads.  Columns are processed in panels of 8: warp 0 factors the
-// panel with warp-synchronous steps, then all threads apply the rank-8
-// update to the trailing part of the tile.
-__global__ void __launch_bounds__(256) potrf_inv_kernel(double* __restrict__ A, int dim, int k,
+// 1024 threads.  Columns are processed in panels of 8: 64 threads (one row
+// each) factor the panel between named barriers, then all threads apply the
+// rank-8 update to the trailing part of the tile.
+__global__ void __launch_bounds__(1024) potrf_inv_kernel(double* __restrict__ A, int dim, int k,
                                                         double* __restrict__ Linv,
                                                         int32_t* __restrict__ status) {
   extern __shared__ double psm[];
@@ -131,12 +131,17 @@ __global__ void __launch_bounds__(256) potrf_inv_kernel(double* __restrict__ A, 
     if (bad) break;
     // rank-(c1-c0) update of the trailing tile: a[r][c] -= sum_j a[r][j] a[c][j], c1 <= c <= r
     const int m = n - c1;
-    for (int e = tid; e < m * m; e += blockDim.x) {
-      const int r = c1 + e / m, c = c1 + e % m;
-      if (c <= r) {
-        double s = 0.0;
-        for (int j = c0; j < c1; ++j) s += a[r][j] * a[c][j];
-        a[r][c] -= s;
+    for (int e = tid; e < m * NB; e += blockDim.x) {
+      const int r = c1 + (e >> 6), c = e & (NB - 1);
+      if (c >= c1 && c <= r) {
+        double s0 = 0.0, s1 = 0.0;
+        int j = c0;
+        for (; j + 1 < c1; j += 2) {  // two independent chains
+          s0 = fma(a[r][j], a[c][j], s0);
+          s1 = fma(a[r][j + 1], a[c][j + 1], s1);
+        }
+        if (j < c1) s0 = fma(a[r][j], a[c][j], s0);
+        a[r][c] -= s0 + s1;
       }
     }
     __syncthreads();
@@ -166,11 +171,16 @@ __global__ void __launch_bounds__(256) potrf_inv_kernel(double* __restrict__ A, 
     __syncthreads();
     const int m = n - c1;
     for (int e = tid; e < m * NB; e += blockDim.x) {
-      const int i = c1 + e / NB, col = e % NB;
+      const int i = c1 + (e >> 6), col = e & (NB - 1);
       if (col <= i) {
-        double s = 0.0;
-        for (int j = c0; j < c1; ++j) s += a[i][j] * x[j][col];
-        x[i][col] -= s;
+        double s0 = 0.0, s1 = 0.0;
+        int j = c0;
+        for (; j + 1 < c1; j += 2) {
+          s0 = fma(a[i][j], x[j][col], s0);
+          s1 = fma(a[i][j + 1], x[j + 1][col], s1);
+        }
+        if (j < c1) s0 = fma(a[i][j], x[j][col], s0);
+        x[i][col] -= s0 + s1;
       }
     }
     __syncthreads();
@@ -400,7 +410,7 @@ extern "C" int pba_solve_dense(const double* H, const double* b, int32_t dim, do
   PBA_CUDA_TRY(cudaFuncSetAttribute(potrf_inv_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));
   for (int k = 0; k < T; ++k) {
-    potrf_inv_kernel<<<1, 256, tile_smem, st>>>(w.A, dim, k, w.Linv, status);
+    potrf_inv_kernel<<<1, 1024, tile_smem, st>>>(w.A, dim, k, w.Linv, status);
     PBA_LAUNCH_CHECK();
     const int m = last[k] - k;  // tile rows below k inside the envelope
     if (m > 0) {
