@@ -468,332 +468,6 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
   }
 }
 
-// ---------------------------------------------------------------------------
-// Asynchronous-copy variant.  Stage 1 of pixel k+1 (unproject, warp, project,
-// footprint) issues cp.async copies of the first 48 bytes — (I, D), (nx, ny),
-// (nz, mask) — of its four destination texels into a per-thread shared-memory
-// slot, then stage 2 of pixel k runs from the other slot.  No registers are
-// held for the in-flight gather, so the L2 latency of the destination texels
-// overlaps the Jacobian/accumulation work of the previous pixel.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
-
-struct Pending {
-  double pb[3];
-  double wx, wy, dist, isrc;
-  int sp, dp;
-  uint32_t smask;  // 0: nothing staged for this pixel
-};
-
-// stage 1: returns the pending record; issues the copies when the pixel projects
-template <int kT>
-__device__ __forceinline__ void stage1_async(const PairSetup& S, int row, int col,
-                                             double2* slot /* [12][kT] */, Pending& P) {
-  P.smask = 0;
-  const int sW = S.src_cam.width, sH = S.src_cam.height;
-  const int sp = row * sW + col;
-  const uint32_t sm = __ldg(S.src_mask + sp);
-  if (!(sm & PBA_MASK_DEPTH_VALID)) return;
-  const double2 s_id = __ldg(reinterpret_cast<const double2*>(S.src_tex + sp));
-  const double d = s_id.y;
-  double ps[3];
-  if (S.src_cam.model == PBA_SPHERICAL) {
-    const double ca = __ldg(S.src_ray + col), sa = __ldg(S.src_ray + sW + col);
-    const double ce = __ldg(S.src_ray + 2 * sW + row), se = __ldg(S.src_ray + 2 * sW + sH + row);
-    ps[0] = (ce * ca) * d;
-    ps[1] = (ce * sa) * d;
-    ps[2] = se * d;
-  } else {
-    ps[0] = __ldg(S.src_ray + col) * d;
-    ps[1] = __ldg(S.src_ray + 2 * sW + row) * d;
-    ps[2] = d;
-  }
-  double pu[3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k)
-    pu[k] = S.Ro[3 * k + 0] * ps[0] + S.Ro[3 * k + 1] * ps[1] + S.Ro[3 * k + 2] * ps[2] + S.to[k];
-#pragma unroll
-  for (int k = 0; k < 3; ++k)
-    P.pb[k] = S.Mi[3 * k + 0] * pu[0] + S.Mi[3 * k + 1] * pu[1] + S.Mi[3 * k + 2] * pu[2] + S.cpb[k];
-  const int dW = S.dst_cam.width, dH = S.dst_cam.height;
-  const double dWd = (double)dW, dHd = (double)dH;
-  double u, v;
-  if (S.dst_cam.model == PBA_SPHERICAL) {
-    const double rr = P.pb[0] * P.pb[0] + P.pb[1] * P.pb[1];
-    const double az = atan2_tab(P.pb[1], P.pb[0]);
-    const double el = atan2_tab(P.pb[2], sqrt(rr));  // hypot(x, y)
-    u = py_mod(S.dst_cam.fx * az + S.dst_cam.cx, dWd);
-    v = S.dst_cam.fy * el + S.dst_cam.cy;
-    P.dist = sqrt(rr + P.pb[2] * P.pb[2]);
-  } else {
-    if (!(P.pb[2] > 0.0)) return;
-    u = S.dst_cam.fx * P.pb[0] / P.pb[2] + S.dst_cam.cx;
-    v = S.dst_cam.fy * P.pb[1] / P.pb[2] + S.dst_cam.cy;
-    P.dist = P.pb[2];
-  }
-  if (!(P.dist >= S.dst_cam.depth_min && P.dist <= S.dst_cam.depth_max)) return;
-  if (!(u >= 0.0 && u < dWd && v >= 0.0 && v < dHd)) return;
-  if (!(u <= dWd - 1.0 && v <= dHd - 1.0)) return;  // sample's inclusive "inside"
-  int x0 = (int)floor(u), y0 = (int)floor(v);
-  x0 = min(max(x0, 0), dW - 2);
-  y0 = min(max(y0, 0), dH - 2);
-  P.wx = u - x0;
-  P.wy = v - y0;
-  P.dp = y0 * dW + x0;
-  P.sp = sp;
-  P.isrc = s_id.x;
-  P.smask = sm | 0x100u;
-  const char* t00 = reinterpret_cast<const char*>(S.dst_tex + P.dp);
-  const char* t10 = reinterpret_cast<const char*>(S.dst_tex + P.dp + dW);
-  const int tid = threadIdx.x;
-#pragma unroll
-  for (int f = 0; f < 3; ++f) {
-    cp_async16(&slot[(0 * 3 + f) * kT + tid], t00 + 16 * f);
-    cp_async16(&slot[(1 * 3 + f) * kT + tid], t00 + 128 + 16 * f);
-    cp_async16(&slot[(2 * 3 + f) * kT + tid], t10 + 16 * f);
-    cp_async16(&slot[(3 * 3 + f) * kT + tid], t10 + 128 + 16 * f);
-  }
-}
-
-template <bool kJac, int kT, int kMinBlocks>
-__global__ void __launch_bounds__(kT, kMinBlocks)
-    linearize_async_kernel(const pba_frame* __restrict__ frames, const pba_pair* __restrict__ pairs,
-                           const int32_t* __restrict__ chunk_table, int chunk_pixels,
-                           const double* __restrict__ poses, const double* __restrict__ exts,
-                           pba_config cfg, double* __restrict__ partials) {
-  __shared__ PairSetup S;
-  constexpr int kWarps = kT / 32;
-  __shared__ double red[kWarps][kPart];
-  extern __shared__ double2 stage_buf[];  // [2][12][kT]
-
-  const long chunk = blockIdx.x;
-  const int pair = chunk_table[2 * chunk];
-  const int first = chunk_table[2 * chunk + 1];
-  if (threadIdx.x == 0) build_setup(S, frames, pairs[pair], poses, exts, cfg.pixel_stride);
-  __syncthreads();
-
-  double Q[kQ];
-#pragma unroll
-  for (int k = 0; k < kQ; ++k) Q[k] = 0.0;
-  double beta[6];
-#pragma unroll
-  for (int k = 0; k < 6; ++k) beta[k] = 0.0;
-  double cost = 0.0;
-  int count = 0;
-
-  const int last = min(first + chunk_pixels, S.n_px);
-  const int dW = S.dst_cam.width;
-  const bool dst_sph = S.dst_cam.model == PBA_SPHERICAL;
-  const int gw = S.grid_w;
-  const int tid = threadIdx.x;
-  int gr = (first + tid) / gw;
-  int gcol = first + tid - gr * gw;
-  int idx = first + tid;
-
-  Pending cur;
-  cur.smask = 0;
-  int buf = 0;
-  bool have_cur = false;
-  while (true) {
-    Pending nxt;
-    nxt.smask = 0;
-    const bool have_nxt = idx < last;
-    if (have_nxt) {
-      stage1_async<kT>(S, gr * S.stride, gcol * S.stride, stage_buf + (buf ^ 1) * 12 * kT, nxt);
-      idx += kT;
-      advance_pixel(gr, gcol, gw, kT);
-    }
-    cp_async_commit();
-    cp_async_wait1();  // the group of `cur` (committed one iteration ago) has landed
-    if (have_cur && cur.smask) {
-      const Pending& P = cur;
-      const double2* sl = stage_buf + buf * 12 * kT + tid;
-      const double2 a00 = sl[0 * kT], b00 = sl[1 * kT], m00 = sl[2 * kT];
-      const double2 a01 = sl[3 * kT], b01 = sl[4 * kT], m01 = sl[5 * kT];
-      const double2 a10 = sl[6 * kT], b10 = sl[7 * kT], m10 = sl[8 * kT];
-      const double2 a11 = sl[9 * kT], b11 = sl[10 * kT], m11 = sl[11 * kT];
-      const uint32_t mk = mask_of_d2(m00) & mask_of_d2(m01) & mask_of_d2(m10) & mask_of_d2(m11);
-      const double wx = P.wx, wy = P.wy;
-      const double Dd = bil(a00.y, a01.y, a10.y, a11.y, wx, wy);
-      const double zeta = P.dist;  // range (spherical) or z (pinhole), solver.py:240
-      const double e1 = zeta - Dd;
-      bool ok = (mk & PBA_MASK_SAMP_CORE) && !(e1 > S.occ_tol);  // core_ok, occlusion
-      double rho2 = 0.0;
-      if (kJac && dst_sph) {
-        rho2 = P.pb[0] * P.pb[0] + P.pb[1] * P.pb[1];
-        ok = ok && (rho2 > 0.0);  // ok_jac
-      }
-      if (ok) {
-        const double e0 = P.isrc - bil(a00.x, a01.x, a10.x, a11.x, wx, wy);
-        const bool normal_on = (mk & PBA_MASK_SAMP_NORMAL) && (P.smask & PBA_MASK_NORMAL_VALID);
-        double e2 = 0.0, e3 = 0.0, e4 = 0.0;
-        double no[3] = {0.0, 0.0, 0.0};
-        if (normal_on) {
-          const double2* st = reinterpret_cast<const double2*>(S.src_tex + P.sp);
-          const double2 s_n01 = __ldg(st + 1);
-          const double ns2 = __ldg(&S.src_tex[P.sp].v[4]);
-          const double m0 = s_n01.x * S.rotn[0] + s_n01.y * S.rotn[1] + ns2 * S.rotn[2];
-          const double m1 = s_n01.x * S.rotn[3] + s_n01.y * S.rotn[4] + ns2 * S.rotn[5];
-          const double m2 = s_n01.x * S.rotn[6] + s_n01.y * S.rotn[7] + ns2 * S.rotn[8];
-          e2 = m0 - bil(b00.x, b01.x, b10.x, b11.x, wx, wy);
-          e3 = m1 - bil(b00.y, b01.y, b10.y, b11.y, wx, wy);
-          e4 = m2 - bil(m00.x, m01.x, m10.x, m11.x, wx, wy);
-          if (kJac) {
-#pragma unroll
-            for (int k = 0; k < 3; ++k)
-              no[k] = S.Ro[3 * k + 0] * s_n01.x + S.Ro[3 * k + 1] * s_n01.y + S.Ro[3 * k + 2] * ns2;
-          }
-        }
-        const double sI = sqrt(e0 * e0 * cfg.omega[0]);
-        const double sD = sqrt(e1 * e1 * cfg.omega[1]);
-        const double sN =
-            sqrt((e2 * e2 * cfg.omega[2] + e3 * e3 * cfg.omega[3]) + e4 * e4 * cfg.omega[4]);
-        const double dI = cfg.huber_delta[0], dD = cfg.huber_delta[1], dN = cfg.huber_delta[2];
-        const bool smI = sI <= dI, smD = sD <= dD, smN = sN <= dN;
-        cost += (smI ? sI * sI : dI * (2.0 * sI - dI)) + (smD ? sD * sD : dD * (2.0 * sD - dD)) +
-                (smN ? sN * sN : dN * (2.0 * sN - dN));
-        ++count;
-        if (kJac) {
-          const double* pb = P.pb;
-          double pu[3];
-          {
-            const double q0 = pb[0] - S.cpb[0], q1 = pb[1] - S.cpb[1], q2 = pb[2] - S.cpb[2];
-#pragma unroll
-            for (int k = 0; k < 3; ++k) pu[k] = q0 * S.Mi[k] + q1 * S.Mi[3 + k] + q2 * S.Mi[6 + k];
-          }
-          double MP0[3], MP1[3], ud[3];
-          if (dst_sph) {
-            const double rho = sqrt(rho2);
-            const double r2 = rho2 + pb[2] * pb[2];
-            const double f0 = S.dst_cam.fx / rho2;
-            const double f1 = S.dst_cam.fy / (rho * r2);
-            const double iz = 1.0 / zeta;
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-              const double m0 = S.Mi[k], m1 = S.Mi[3 + k], m2 = S.Mi[6 + k];
-              MP0[k] = f0 * (pb[0] * m1 - pb[1] * m0);
-              MP1[k] = f1 * (rho2 * m2 - pb[2] * (pb[0] * m0 + pb[1] * m1));
-              ud[k] = iz * (pb[0] * m0 + pb[1] * m1 + pb[2] * m2);
-            }
-          } else {
-            const double iz = 1.0 / pb[2];
-            const double f0 = S.dst_cam.fx * iz, f1 = S.dst_cam.fy * iz;
-            const double xz = pb[0] * iz, yz = pb[1] * iz;
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-              const double m2 = S.Mi[6 + k];
-              MP0[k] = f0 * (S.Mi[k] - xz * m2);
-              MP1[k] = f1 * (S.Mi[3 + k] - yz * m2);
-              ud[k] = m2;
-            }
-          }
-          const double wI = smI ? cfg.omega[0] : cfg.omega[0] * (dI / sI);
-          const double wD = smD ? cfg.omega[1] : cfg.omega[1] * (dD / sD);
-          const double wN = smN ? 1.0 : dN / sN;
-          const int n_ch = normal_on ? 5 : 2;
-          const Texel* t00 = S.dst_tex + P.dp;
-          const Texel* t10 = t00 + dW;
-#pragma unroll 1
-          for (int c = 0; c < n_ch; ++c) {
-            const double2 g00 = __ldg(reinterpret_cast<const double2*>(&t00->g[2 * c]));
-            const double2 g01 = __ldg(reinterpret_cast<const double2*>(&t00[1].g[2 * c]));
-            const double2 g10 = __ldg(reinterpret_cast<const double2*>(&t10->g[2 * c]));
-            const double2 g11 = __ldg(reinterpret_cast<const double2*>(&t10[1].g[2 * c]));
-            const double gc = bil(g00.x, g01.x, g10.x, g11.x, wx, wy);
-            const double gr_ = bil(g00.y, g01.y, g10.y, g11.y, wx, wy);
-            double q[6];
-#pragma unroll
-            for (int k = 0; k < 3; ++k) q[k] = -(gc * MP0[k] + gr_ * MP1[k]);
-            double ww, ec;
-            if (c == 0) {
-              ww = wI;
-              ec = e0;
-            } else if (c == 1) {
-#pragma unroll
-              for (int k = 0; k < 3; ++k) q[k] += ud[k];
-              ww = wD;
-              ec = e1;
-            } else {
-              ww = wN * (c == 2 ? cfg.omega[2] : (c == 3 ? cfg.omega[3] : cfg.omega[4]));
-              ec = c == 2 ? e2 : (c == 3 ? e3 : e4);
-            }
-            cross3(q, pu, &q[3]);
-            if (c >= 2) {
-              double xn[3];
-              cross3(&S.Mi[3 * (c - 2)], no, xn);
-              q[3] += xn[0];
-              q[4] += xn[1];
-              q[5] += xn[2];
-            }
-            const double we = ww * ec;
-            double a[6];
-#pragma unroll
-            for (int k = 0; k < 6; ++k) {
-              a[k] = ww * q[k];
-              beta[k] = fma(q[k], we, beta[k]);
-            }
-#pragma unroll
-            for (int k = 0; k < 6; ++k)
-#pragma unroll
-              for (int l = k; l < 6; ++l) Q[upper_idx(k, l)] = fma(a[k], q[l], Q[upper_idx(k, l)]);
-          }
-        }
-      }
-    }
-    if (!have_nxt) break;
-    cur = nxt;
-    have_cur = true;
-    buf ^= 1;
-  }
-  asm volatile("cp.async.wait_all;\n" ::);
-
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double cnt = (double)count;
-  if (kJac) {
-#pragma unroll
-    for (int k = 0; k < kQ; ++k) {
-      double x = Q[k];
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
-      Q[k] = x;
-    }
-#pragma unroll
-    for (int k = 0; k < 6; ++k) {
-      double x = beta[k];
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
-      beta[k] = x;
-    }
-  }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    cost += __shfl_xor_sync(0xffffffffu, cost, off);
-    cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
-  }
-  if (lane == 0) {
-    double* r = red[warp];
-#pragma unroll
-    for (int k = 0; k < kQ; ++k) r[k] = kJac ? Q[k] : 0.0;
-#pragma unroll
-    for (int k = 0; k < 6; ++k) r[kQ + k] = kJac ? beta[k] : 0.0;
-    r[27] = cost;
-    r[28] = cnt;
-    r[29] = r[30] = r[31] = 0.0;
-  }
-  __syncthreads();
-  if (threadIdx.x < kPart) {
-    double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) s += red[w][threadIdx.x];
-    partials[chunk * kPart + threadIdx.x] = s;
-  }
-}
-
 // One warp per pair: sum the pair's chunk partials in chunk order, then
 // expand (Q, beta) into the reference _EdgeTerm blocks:
 //   H_ii = D Q D, H_jj = L Q L^T, H_ij = D Q L^T, b_i = D beta, b_j = L beta.
@@ -941,18 +615,9 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
     if (variant < 0) {
       const char* env = getenv("PBA_LIN_VARIANT");
       variant = env ? atoi(env) : 4;
-      if (variant < 1 || variant > 8) variant = 4;
+      if (variant < 1 || variant > 5) variant = 4;
     }
     const unsigned grid = (unsigned)n_chunks;
-#define PBA_LAUNCH_ASYNC(J, T, M)                                                              \
-  do {                                                                                         \
-    const int smem = 2 * 12 * T * (int)sizeof(double2);                                        \
-    cudaFuncSetAttribute(linearize_async_kernel<J, T, M>,                                      \
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);                   \
-    linearize_async_kernel<J, T, M><<<grid, T, smem, st>>>(frames, pairs, chunk_table,         \
-                                                         chunk_pixels, poses, extrinsics, *cfg, \
-                                                         partials);                            \
-  } while (0)
 #define PBA_LAUNCH_LIN(J, T, M) \
   linearize_kernel<J, T, M><<<grid, T, 0, st>>>(frames, pairs, chunk_table, chunk_pixels, poses, extrinsics, *cfg, partials)
     if (want_jacobians) {
@@ -961,16 +626,12 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
         case 3: PBA_LAUNCH_LIN(true, 128, 4); break;
         case 5: PBA_LAUNCH_LIN(true, 512, 1); break;
         case 2: PBA_LAUNCH_LIN(true, 256, 2); break;
-        case 6: PBA_LAUNCH_ASYNC(true, 128, 3); break;
-        case 7: PBA_LAUNCH_ASYNC(true, 128, 2); break;
-        case 8: PBA_LAUNCH_ASYNC(true, 256, 1); break;
         default: PBA_LAUNCH_LIN(true, 128, 3); break;
       }
     } else {
       PBA_LAUNCH_LIN(false, 128, 3);
     }
 #undef PBA_LAUNCH_LIN
-#undef PBA_LAUNCH_ASYNC
     PBA_LAUNCH_CHECK();
   }
   finalize_pairs_kernel<<<(unsigned)((n_pairs + 3) / 4), 128, 0, st>>>(
