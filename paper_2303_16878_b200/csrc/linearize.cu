@@ -190,7 +190,7 @@ __device__ __forceinline__ uint32_t mask_of_d2(const double2& v) {
 
 __device__ __forceinline__ int upper_idx(int k, int l) { return k * 6 - (k * (k - 1)) / 2 + (l - k); }
 
-template <bool kJac, int kT, int kMinBlocks>
+template <bool kJac, int kT, int kMinBlocks, int kProbe = 0>
 __global__ void __launch_bounds__(kT, kMinBlocks)
     linearize_kernel(const pba_frame* __restrict__ frames, const pba_pair* __restrict__ pairs,
                      const int32_t* __restrict__ chunk_table, int chunk_pixels,
@@ -284,7 +284,8 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     x0 = min(max(x0, 0), dW - 2);
     y0 = min(max(y0, 0), dH - 2);
     const double wx = u - x0, wy = v - y0;
-    const int dp = y0 * dW + x0;
+    // kProbe 1 (diagnostics only): every sample reads the same texel block
+    const int dp = kProbe == 1 ? (dH / 2) * dW + dW / 2 : y0 * dW + x0;
     const uint32_t mk = __ldg(S.dst_mask + dp) & __ldg(S.dst_mask + dp + 1) &
                         __ldg(S.dst_mask + dp + dW) & __ldg(S.dst_mask + dp + dW + 1);
     if (!(mk & PBA_MASK_SAMP_CORE)) continue;  // core_ok
@@ -615,7 +616,7 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
     if (variant < 0) {
       const char* env = getenv("PBA_LIN_VARIANT");
       variant = env ? atoi(env) : 4;
-      if (variant < 1 || variant > 5) variant = 4;
+      if (variant < 1 || variant > 9) variant = 4;
     }
     const unsigned grid = (unsigned)n_chunks;
 #define PBA_LAUNCH_LIN(J, T, M) \
@@ -626,6 +627,11 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
         case 3: PBA_LAUNCH_LIN(true, 128, 4); break;
         case 5: PBA_LAUNCH_LIN(true, 512, 1); break;
         case 2: PBA_LAUNCH_LIN(true, 256, 2); break;
+        case 9:  // diagnostics: destination gather replaced by a fixed texel
+          linearize_kernel<true, 128, 3, 1><<<grid, 128, 0, st>>>(frames, pairs, chunk_table,
+                                                                chunk_pixels, poses, extrinsics,
+                                                                *cfg, partials);
+          break;
         default: PBA_LAUNCH_LIN(true, 128, 3); break;
       }
     } else {
