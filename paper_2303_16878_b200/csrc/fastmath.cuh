@@ -27,9 +27,33 @@ __device__ AtanEntry g_atan_table[2 * kAtanHalf + 1];
 // Host: fill the table for the current device (idempotent per device).
 int ensure_atan_table();
 
+// fp64 reciprocal: fp32 seed + 3 Newton steps (relative error < 1e-17 before
+// the final rounding), ~8 instructions instead of the IEEE division sequence.
+__device__ __forceinline__ double rcp_nr(double x) {
+  const double ax = fabs(x);
+  if (!(ax > 1e-30 && ax < 1e30)) return 1.0 / x;  // outside the fp32 seed's range
+  double r = (double)__frcp_rn((float)x);
+  r = fma(r, fma(-x, r, 1.0), r);
+  r = fma(r, fma(-x, r, 1.0), r);
+  r = fma(r, fma(-x, r, 1.0), r);
+  return r;
+}
+
+// Cheap fp32 atan2 (max error ~1e-5 rad): only has to pick the table slot.
+__device__ __forceinline__ float atan2_guess(float y, float x) {
+  const float ax = fabsf(x), ay = fabsf(y);
+  const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+  const float a = mn * __frcp_rn(mx);
+  const float s = a * a;
+  float r = fmaf(fmaf(fmaf(-0.0464964749f, s, 0.15931422f), s, -0.327622764f), s * a, a);
+  if (ay > ax) r = 1.57079637f - r;
+  if (x < 0.0f) r = 3.14159274f - r;
+  return (y < 0.0f) ? -r : r;
+}
+
 __device__ __forceinline__ double atan2_tab(double y, double x) {
   if (x == 0.0 && y == 0.0) return atan2(y, x);  // signed-zero semantics
-  const float tf = atan2f((float)y, (float)x);
+  const float tf = atan2_guess((float)y, (float)x);
   int k = __float2int_rn(tf * (float)(kAtanHalf / 3.14159265358979323846));
   k = min(max(k, -kAtanHalf), kAtanHalf);
   const AtanEntry* e = &g_atan_table[k + kAtanHalf];
@@ -37,7 +61,7 @@ __device__ __forceinline__ double atan2_tab(double y, double x) {
   const double th = __ldg(&e->theta);
   const double num = y * cs.x - x * cs.y;
   const double den = x * cs.x + y * cs.y;
-  const double d = num / den;
+  const double d = num * rcp_nr(den);  // den ~ |(x, y)| > 0
   const double d2 = d * d;
   double p = fma(d2, 1.0 / 9.0, -1.0 / 7.0);
   p = fma(p, d2, 1.0 / 5.0);

@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
   const bool src_sph = S.src_cam.model == PBA_SPHERICAL;
   const bool dst_sph = S.dst_cam.model == PBA_SPHERICAL;
   const double dWd = (double)dW, dHd = (double)dH;
+  const double sqw0 = sqrt(cfg.omega[0]), sqw1 = sqrt(cfg.omega[1]);
 
   const int gw = S.grid_w;
   int gr = (first + (int)threadIdx.x) / gw;             // strided-grid row / column of
@@ -261,11 +262,12 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
       pb[k] = S.Mi[3 * k + 0] * pu[0] + S.Mi[3 * k + 1] * pu[1] + S.Mi[3 * k + 2] * pu[2] + S.cpb[k];
 
     // ---- project into the destination (sensors.py:95-130) ----
-    double u, v, dist;
+    double u, v, dist, rho = 0.0;
     if (dst_sph) {
       const double rr = pb[0] * pb[0] + pb[1] * pb[1];
+      rho = sqrt(rr);
       const double az = atan2_tab(pb[1], pb[0]);
-      const double el = atan2_tab(pb[2], sqrt(rr));  // hypot(x, y)
+      const double el = atan2_tab(pb[2], rho);  // hypot(x, y)
       u = py_mod(S.dst_cam.fx * az + S.dst_cam.cx, dWd);
       v = S.dst_cam.fy * el + S.dst_cam.cy;
       dist = sqrt(rr + pb[2] * pb[2]);
@@ -335,8 +337,8 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     }
 
     // ---- per-cue Huber (solver.py:317-337) ----
-    const double sI = sqrt(e0 * e0 * cfg.omega[0]);
-    const double sD = sqrt(e1 * e1 * cfg.omega[1]);
+    const double sI = fabs(e0) * sqw0;  // = sqrt(e0^2 w0) up to one rounding
+    const double sD = fabs(e1) * sqw1;
     const double sN = sqrt((e2 * e2 * cfg.omega[2] + e3 * e3 * cfg.omega[3]) + e4 * e4 * cfg.omega[4]);
     const double dI = cfg.huber_delta[0], dD = cfg.huber_delta[1], dN = cfg.huber_delta[2];
     const bool smI = sI <= dI, smD = sD <= dD, smN = sN <= dN;
@@ -349,11 +351,11 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     // MP0 = M_i^T P[0,:], MP1 = M_i^T P[1,:], ud = M_i^T (depth-cue direction)
     double MP0[3], MP1[3], ud[3];
     if (dst_sph) {
-      const double rho = sqrt(rho2);
       const double r2 = rho2 + pb[2] * pb[2];
-      const double f0 = S.dst_cam.fx / rho2;
-      const double f1 = S.dst_cam.fy / (rho * r2);
-      const double iz = 1.0 / zeta;
+      const double irho2 = rcp_nr(rho2);
+      const double f0 = S.dst_cam.fx * irho2;
+      const double f1 = S.dst_cam.fy * rcp_nr(rho * r2);
+      const double iz = rcp_nr(zeta);
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
         const double m0 = S.Mi[k], m1 = S.Mi[3 + k], m2 = S.Mi[6 + k];
@@ -362,7 +364,7 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
         ud[k] = iz * (pb[0] * m0 + pb[1] * m1 + pb[2] * m2);
       }
     } else {
-      const double iz = 1.0 / pb[2];
+      const double iz = rcp_nr(pb[2]);
       const double f0 = S.dst_cam.fx * iz, f1 = S.dst_cam.fy * iz;
       const double xz = pb[0] * iz, yz = pb[1] * iz;
 #pragma unroll
@@ -373,9 +375,9 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
         ud[k] = m2;
       }
     }
-    const double wI = smI ? cfg.omega[0] : cfg.omega[0] * (dI / sI);
-    const double wD = smD ? cfg.omega[1] : cfg.omega[1] * (dD / sD);
-    const double wN = smN ? 1.0 : dN / sN;
+    const double wI = smI ? cfg.omega[0] : cfg.omega[0] * (dI * rcp_nr(sI));
+    const double wD = smD ? cfg.omega[1] : cfg.omega[1] * (dD * rcp_nr(sD));
+    const double wN = smN ? 1.0 : dN * rcp_nr(sN);
     const int n_ch = normal_on ? 5 : 2;
 #pragma unroll 1
     for (int c = 0; c < n_ch; ++c) {
