@@ -40,7 +40,9 @@ __device__ __forceinline__ double rcp_nr(double x) {
 }
 
 // Cheap fp32 atan2 (max error ~1e-5 rad): only has to pick the table slot.
-__device__ __forceinline__ float atan2_guess(float y, float x) {
+// The sign comes from the fp64 y (signbit) so that y = -0 or a negative y
+// that underflows in fp32 still selects the -pi side of the branch cut.
+__device__ __forceinline__ float atan2_guess(float y, float x, bool y_negative) {
   const float ax = fabsf(x), ay = fabsf(y);
   const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
   const float a = mn * __frcp_rn(mx);
@@ -48,12 +50,12 @@ __device__ __forceinline__ float atan2_guess(float y, float x) {
   float r = fmaf(fmaf(fmaf(-0.0464964749f, s, 0.15931422f), s, -0.327622764f), s * a, a);
   if (ay > ax) r = 1.57079637f - r;
   if (x < 0.0f) r = 3.14159274f - r;
-  return (y < 0.0f) ? -r : r;
+  return y_negative ? -r : r;
 }
 
 __device__ __forceinline__ double atan2_tab(double y, double x) {
   if (x == 0.0 && y == 0.0) return atan2(y, x);  // signed-zero semantics
-  const float tf = atan2_guess((float)y, (float)x);
+  const float tf = atan2_guess((float)y, (float)x, signbit(y));
   int k = __float2int_rn(tf * (float)(kAtanHalf / 3.14159265358979323846));
   k = min(max(k, -kAtanHalf), kAtanHalf);
   const AtanEntry* e = &g_atan_table[k + kAtanHalf];
