@@ -184,7 +184,7 @@ __device__ __forceinline__ void advance_pixel(int& row, int& col, int width, int
   }
 }
 
-__device__ __forceinline__ uint32_t mask_of_d2(const double2& v) {
+__device__ __forceinline__ uint32_t mask_word(const double2& v) {
   return (uint32_t)(__double_as_longlong(v.y) & 0xffffffffu);
 }
 
@@ -224,19 +224,40 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
   const double sqw0 = sqrt(cfg.omega[0]), sqw1 = sqrt(cfg.omega[1]);
 
   const int gw = S.grid_w;
-  int gr = (first + (int)threadIdx.x) / gw;             // strided-grid row / column of
-  int gcol = first + (int)threadIdx.x - gr * gw;        // this thread's current pixel
-  for (int idx = first + (int)threadIdx.x; idx < last;
-       idx += kT, advance_pixel(gr, gcol, gw, kT)) {
-    const int row = gr * S.stride;
-    const int col = gcol * S.stride;
+  const int stride = S.stride;
+  int gr = (first + (int)threadIdx.x) / gw;       // strided-grid row / column of
+  int gcol = first + (int)threadIdx.x - gr * gw;  // this thread's current pixel
+  // The source texel of the next pixel is always in flight one iteration
+  // ahead: (I, D) and (nz, mask) words, 2 x 16 B.  Masks come from the texel
+  // lines themselves, so a pixel costs two dependent L2 round trips (source
+  // texel, destination texels) instead of four.
+  double2 nx0 = make_double2(0.0, 0.0), nx2 = make_double2(0.0, 0.0);
+  if (first + (int)threadIdx.x < last) {
+    const double2* t = reinterpret_cast<const double2*>(S.src_tex + gr * stride * sW + gcol * stride);
+    nx0 = __ldg(t);
+    nx2 = __ldg(t + 2);
+  }
+  int ngr = gr, ngcol = gcol;
+  for (int idx = first + (int)threadIdx.x; idx < last; idx += kT, gr = ngr, gcol = ngcol) {
+    const int row = gr * stride;
+    const int col = gcol * stride;
     const int sp = row * sW + col;
-    const uint32_t sm = __ldg(S.src_mask + sp);
+    const double2 s_id = nx0;  // I, D
+    const uint32_t sm = mask_word(nx2);
+    const double mask_src_nz = nx2.x;
+    ngr = gr;
+    ngcol = gcol;
+    advance_pixel(ngr, ngcol, gw, kT);
+    if (idx + kT < last) {
+      const double2* t =
+          reinterpret_cast<const double2*>(S.src_tex + ngr * stride * sW + ngcol * stride);
+      nx0 = __ldg(t);
+      nx2 = __ldg(t + 2);
+    }
     if (!(sm & PBA_MASK_DEPTH_VALID)) continue;  // PairContext.build: usable = depth_valid
 
     // ---- source cue values and unprojection (sensors.py:133-154) ----
     const double2* st = reinterpret_cast<const double2*>(S.src_tex + sp);
-    const double2 s_id = __ldg(st + 0);   // I, D
     const double d = s_id.y;
     double ps[3];
     if (src_sph) {
@@ -288,16 +309,19 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     const double wx = u - x0, wy = v - y0;
     // kProbe 1 (diagnostics only): every sample reads the same texel block
     const int dp = kProbe == 1 ? (dH / 2) * dW + dW / 2 : y0 * dW + x0;
-    const uint32_t mk = __ldg(S.dst_mask + dp) & __ldg(S.dst_mask + dp + 1) &
-                        __ldg(S.dst_mask + dp + dW) & __ldg(S.dst_mask + dp + dW + 1);
-    if (!(mk & PBA_MASK_SAMP_CORE)) continue;  // core_ok
     const Texel* t00 = S.dst_tex + dp;
     const Texel* t10 = t00 + dW;
-
+    // (I, D) and (nz, mask) of the four corners in one round trip
     const double2 a00 = __ldg(reinterpret_cast<const double2*>(t00));
     const double2 a01 = __ldg(reinterpret_cast<const double2*>(t00 + 1));
     const double2 a10 = __ldg(reinterpret_cast<const double2*>(t10));
     const double2 a11 = __ldg(reinterpret_cast<const double2*>(t10 + 1));
+    const double2 m00 = __ldg(reinterpret_cast<const double2*>(t00) + 2);
+    const double2 m01 = __ldg(reinterpret_cast<const double2*>(t00 + 1) + 2);
+    const double2 m10 = __ldg(reinterpret_cast<const double2*>(t10) + 2);
+    const double2 m11 = __ldg(reinterpret_cast<const double2*>(t10 + 1) + 2);
+    const uint32_t mk = mask_word(m00) & mask_word(m01) & mask_word(m10) & mask_word(m11);
+    if (!(mk & PBA_MASK_SAMP_CORE)) continue;  // core_ok
     const double Dd = bil(a00.y, a01.y, a10.y, a11.y, wx, wy);
     // zeta_d: range for spherical, z for pinhole (solver.py:240)
     const double zeta = dst_sph ? dist : pb[2];
@@ -314,21 +338,19 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     double e2 = 0.0, e3 = 0.0, e4 = 0.0;
     double no[3] = {0.0, 0.0, 0.0};  // R_o n_src
     if (normal_on) {
-      const double2 s_n01 = __ldg(st + 1);  // source nx, ny
-      const double ns2 = __ldg(&S.src_tex[sp].v[4]);
+      const double2 s_n01 = __ldg(st + 1);  // source nx, ny (same line: L1 hit)
+      const double ns2 = mask_src_nz;
       const double2 b00 = __ldg(reinterpret_cast<const double2*>(t00) + 1);
       const double2 b01 = __ldg(reinterpret_cast<const double2*>(t00 + 1) + 1);
       const double2 b10 = __ldg(reinterpret_cast<const double2*>(t10) + 1);
       const double2 b11 = __ldg(reinterpret_cast<const double2*>(t10 + 1) + 1);
-      const double c00 = __ldg(&t00->v[4]), c01 = __ldg(&t00[1].v[4]);
-      const double c10 = __ldg(&t10->v[4]), c11 = __ldg(&t10[1].v[4]);
       // rot_n n_src (solver.py:241-248)
       const double m0 = s_n01.x * S.rotn[0] + s_n01.y * S.rotn[1] + ns2 * S.rotn[2];
       const double m1 = s_n01.x * S.rotn[3] + s_n01.y * S.rotn[4] + ns2 * S.rotn[5];
       const double m2 = s_n01.x * S.rotn[6] + s_n01.y * S.rotn[7] + ns2 * S.rotn[8];
       e2 = m0 - bil(b00.x, b01.x, b10.x, b11.x, wx, wy);
       e3 = m1 - bil(b00.y, b01.y, b10.y, b11.y, wx, wy);
-      e4 = m2 - bil(c00, c01, c10, c11, wx, wy);
+      e4 = m2 - bil(m00.x, m01.x, m10.x, m11.x, wx, wy);
       if (kJac) {
 #pragma unroll
         for (int k = 0; k < 3; ++k)
