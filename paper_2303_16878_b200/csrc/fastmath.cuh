@@ -1,14 +1,12 @@
-// fp64 atan2 at a third of the cost of the CUDA library routine.
+// Division-free fp64 atan2 for the spherical projection (sensors.py:120-121).
 //
-// atan2(y, x) = theta_k + atan(d),  d = (y c_k - x s_k) / (x c_k + y s_k)
-// for any table angle theta_k with c_k = cos theta_k, s_k = sin theta_k
-// (rotate (x, y) by -theta_k).  theta_k is picked from a 513-entry table
-// over [-pi, pi] by an fp32 atan2f guess, so |theta - theta_k| <= pi/512 + 1e-6
-// and |d| < 0.0062: the odd series d - d^3/3 + ... + d^9/9 is exact to
-// d^11/11 < 1e-25 relative, leaving only the rounding of one division and
-// the final add (<= 1 ulp, vs ~2 ulp for the library atan2).  Used for the
-// spherical projection (sensors.py:120-121), where the two library atan2
-// calls were 25% of the linearisation kernel's instructions.
+// For any table angle theta_k (c_k = cos, s_k = sin), rotating (x, y) by
+// -theta_k gives sin(theta - theta_k) = (y c_k - x s_k) / r.  theta_k is
+// picked from a 513-entry table over [-pi, pi] by a cheap fp32 guess, so
+// |theta - theta_k| <= pi/512 + 1e-5 and asin of that sine is an odd series
+// exact to ~1e-25; the result is within ~1 ulp of pi absolute (tested against
+// numpy.arctan2).  The library atan2 calls were 25% of the linearisation
+// kernel's instructions and long dependent chains.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -27,18 +25,6 @@ __device__ AtanEntry g_atan_table[2 * kAtanHalf + 1];
 // Host: fill the table for the current device (idempotent per device).
 int ensure_atan_table();
 
-// fp64 reciprocal: fp32 seed + 3 Newton steps (relative error < 1e-17 before
-// the final rounding), ~8 instructions instead of the IEEE division sequence.
-__device__ __forceinline__ double rcp_nr(double x) {
-  const double ax = fabs(x);
-  if (!(ax > 1e-30 && ax < 1e30)) return 1.0 / x;  // outside the fp32 seed's range
-  double r = (double)__frcp_rn((float)x);
-  r = fma(r, fma(-x, r, 1.0), r);
-  r = fma(r, fma(-x, r, 1.0), r);
-  r = fma(r, fma(-x, r, 1.0), r);
-  return r;
-}
-
 // Cheap fp32 atan2 (max error ~1e-5 rad): only has to pick the table slot.
 // The sign comes from the fp64 y (signbit) so that y = -0 or a negative y
 // that underflows in fp32 still selects the -pi side of the branch cut.
@@ -53,22 +39,33 @@ __device__ __forceinline__ float atan2_guess(float y, float x, bool y_negative) 
   return y_negative ? -r : r;
 }
 
-__device__ __forceinline__ double atan2_tab(double y, double x) {
-  if (x == 0.0 && y == 0.0) return atan2(y, x);  // signed-zero semantics
+// atan2(y, x) given inv_r = 1 / |(x, y)| (computed once by the caller with
+// rsqrt, which also yields the range and the Jacobian reciprocals):
+//   Delta = theta - theta_k,  sin Delta = (y c_k - x s_k) * inv_r,
+//   atan2 = theta_k + asin(sin Delta)  (|sin Delta| < 0.0063, odd series to s^9).
+// No division; measured on B200: fp64 divide ~130 cycles, sqrt ~100,
+// rsqrt ~75 of dependent latency vs 8 for a DFMA.
+__device__ __forceinline__ double atan2_tab_r(double y, double x, double inv_r) {
   const float tf = atan2_guess((float)y, (float)x, signbit(y));
   int k = __float2int_rn(tf * (float)(kAtanHalf / 3.14159265358979323846));
   k = min(max(k, -kAtanHalf), kAtanHalf);
   const AtanEntry* e = &g_atan_table[k + kAtanHalf];
   const double2 cs = __ldg(reinterpret_cast<const double2*>(e));
   const double th = __ldg(&e->theta);
-  const double num = y * cs.x - x * cs.y;
-  const double den = x * cs.x + y * cs.y;
-  const double d = num * rcp_nr(den);  // den ~ |(x, y)| > 0
-  const double d2 = d * d;
-  double p = fma(d2, 1.0 / 9.0, -1.0 / 7.0);
-  p = fma(p, d2, 1.0 / 5.0);
-  p = fma(p, d2, -1.0 / 3.0);
-  return th + fma(d * d2, p, d);
+  const double sd = (y * cs.x - x * cs.y) * inv_r;
+  const double s2 = sd * sd;
+  double p = fma(s2, 35.0 / 1152.0, 5.0 / 112.0);
+  p = fma(p, s2, 3.0 / 40.0);
+  p = fma(p, s2, 1.0 / 6.0);
+  return th + fma(sd * s2, p, sd);
+}
+
+// Stand-alone atan2 (diagnostics / rare paths): same method, inv_r via rsqrt.
+__device__ __forceinline__ double atan2_tab(double y, double x) {
+  if (x == 0.0 && y == 0.0) return atan2(y, x);  // signed-zero semantics
+  const double rr = x * x + y * y;
+  if (!(rr > 1e-300 && rr < 1e300)) return atan2(y, x);
+  return atan2_tab_r(y, x, rsqrt(rr));
 }
 
 }  // namespace pba

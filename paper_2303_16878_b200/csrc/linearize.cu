@@ -283,19 +283,32 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
       pb[k] = S.Mi[3 * k + 0] * pu[0] + S.Mi[3 * k + 1] * pu[1] + S.Mi[3 * k + 2] * pu[2] + S.cpb[k];
 
     // ---- project into the destination (sensors.py:95-130) ----
-    double u, v, dist, rho = 0.0;
+    // Two independent rsqrt give rho = hypot(x, y), the range and every
+    // reciprocal needed below (inv = 1/rho, 1/range; pinhole: 1/z).
+    double u, v, dist, rho = 0.0, inv_rho = 0.0, inv_dist;
     if (dst_sph) {
       const double rr = pb[0] * pb[0] + pb[1] * pb[1];
-      rho = sqrt(rr);
-      const double az = atan2_tab(pb[1], pb[0]);
-      const double el = atan2_tab(pb[2], rho);  // hypot(x, y)
+      const double r2 = rr + pb[2] * pb[2];
+      inv_dist = rsqrt(r2);
+      dist = r2 * inv_dist;
+      double az;
+      if (rr > 1e-60) {
+        inv_rho = rsqrt(rr);
+        rho = rr * inv_rho;
+        az = atan2_tab_r(pb[1], pb[0], inv_rho);
+      } else {  // (practically) on the polar axis: library path, atan2's zero semantics
+        rho = sqrt(rr);
+        inv_rho = rr > 0.0 ? 1.0 / rho : 0.0;
+        az = atan2(pb[1], pb[0]);
+      }
+      const double el = atan2_tab_r(pb[2], rho, inv_dist);
       u = py_mod(S.dst_cam.fx * az + S.dst_cam.cx, dWd);
       v = S.dst_cam.fy * el + S.dst_cam.cy;
-      dist = sqrt(rr + pb[2] * pb[2]);
     } else {
       if (!(pb[2] > 0.0)) continue;
-      u = S.dst_cam.fx * pb[0] / pb[2] + S.dst_cam.cx;
-      v = S.dst_cam.fy * pb[1] / pb[2] + S.dst_cam.cy;
+      inv_dist = __drcp_rn(pb[2]);
+      u = S.dst_cam.fx * pb[0] * inv_dist + S.dst_cam.cx;
+      v = S.dst_cam.fy * pb[1] * inv_dist + S.dst_cam.cy;
       dist = pb[2];
     }
     if (!(dist >= S.dst_cam.depth_min && dist <= S.dst_cam.depth_max)) continue;
@@ -361,7 +374,9 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     // ---- per-cue Huber (solver.py:317-337) ----
     const double sI = fabs(e0) * sqw0;  // = sqrt(e0^2 w0) up to one rounding
     const double sD = fabs(e1) * sqw1;
-    const double sN = sqrt((e2 * e2 * cfg.omega[2] + e3 * e3 * cfg.omega[3]) + e4 * e4 * cfg.omega[4]);
+    const double tN = (e2 * e2 * cfg.omega[2] + e3 * e3 * cfg.omega[3]) + e4 * e4 * cfg.omega[4];
+    const double inv_sN = tN > 1e-300 ? rsqrt(tN) : 0.0;
+    const double sN = tN > 1e-300 ? tN * inv_sN : sqrt(tN);
     const double dI = cfg.huber_delta[0], dD = cfg.huber_delta[1], dN = cfg.huber_delta[2];
     const bool smI = sI <= dI, smD = sD <= dD, smN = sN <= dN;
     cost += (smI ? sI * sI : dI * (2.0 * sI - dI)) + (smD ? sD * sD : dD * (2.0 * sD - dD)) +
@@ -373,11 +388,9 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     // MP0 = M_i^T P[0,:], MP1 = M_i^T P[1,:], ud = M_i^T (depth-cue direction)
     double MP0[3], MP1[3], ud[3];
     if (dst_sph) {
-      const double r2 = rho2 + pb[2] * pb[2];
-      const double irho2 = rcp_nr(rho2);
-      const double f0 = S.dst_cam.fx * irho2;
-      const double f1 = S.dst_cam.fy * rcp_nr(rho * r2);
-      const double iz = rcp_nr(zeta);
+      const double iz = inv_dist;  // 1/|p_bar| = 1/zeta
+      const double f0 = S.dst_cam.fx * (inv_rho * inv_rho);         // fx / rho^2
+      const double f1 = S.dst_cam.fy * (inv_rho * (iz * iz));       // fy / (rho r^2)
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
         const double m0 = S.Mi[k], m1 = S.Mi[3 + k], m2 = S.Mi[6 + k];
@@ -386,7 +399,7 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
         ud[k] = iz * (pb[0] * m0 + pb[1] * m1 + pb[2] * m2);
       }
     } else {
-      const double iz = rcp_nr(pb[2]);
+      const double iz = inv_dist;  // 1/z
       const double f0 = S.dst_cam.fx * iz, f1 = S.dst_cam.fy * iz;
       const double xz = pb[0] * iz, yz = pb[1] * iz;
 #pragma unroll
@@ -397,9 +410,9 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
         ud[k] = m2;
       }
     }
-    const double wI = smI ? cfg.omega[0] : cfg.omega[0] * (dI * rcp_nr(sI));
-    const double wD = smD ? cfg.omega[1] : cfg.omega[1] * (dD * rcp_nr(sD));
-    const double wN = smN ? 1.0 : dN * rcp_nr(sN);
+    const double wI = smI ? cfg.omega[0] : cfg.omega[0] * (dI * __drcp_rn(sI));
+    const double wD = smD ? cfg.omega[1] : cfg.omega[1] * (dD * __drcp_rn(sD));
+    const double wN = smN ? 1.0 : dN * inv_sN;
     const int n_ch = normal_on ? 5 : 2;
 #pragma unroll 1
     for (int c = 0; c < n_ch; ++c) {
