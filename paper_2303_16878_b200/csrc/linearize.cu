@@ -190,6 +190,48 @@ __device__ __forceinline__ uint32_t mask_word(const double2& v) {
 
 __device__ __forceinline__ int upper_idx(int k, int l) { return k * 6 - (k * (k - 1)) / 2 + (l - k); }
 
+// Bilinear interpolation of a (d/dcol, d/drow) gradient pair with corner weights.
+__device__ __forceinline__ double2 bil4(double2 g00, double2 g01, double2 g10, double2 g11,
+                                        double w00, double w01, double w10, double w11) {
+  double2 r;
+  r.x = fma(w11, g11.x, fma(w10, g10.x, fma(w01, g01.x, w00 * g00.x)));
+  r.y = fma(w11, g11.y, fma(w10, g10.y, fma(w01, g01.y, w00 * g00.y)));
+  return r;
+}
+
+// One cue channel's contribution in the q-basis (see the file header):
+//   q = [u; u x p_u (+ xn)],  u = -(g . P) M_i (+ extra_u),
+//   Q += ww q q^T,  beta += q ww e.
+__device__ __forceinline__ void accumulate_channel(double* Q, double* beta, double2 g,
+                                                   const double* MP0, const double* MP1,
+                                                   const double* extra_u, const double* pu,
+                                                   const double* xn, double ww, double ec) {
+  double q[6];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) q[k] = -(g.x * MP0[k] + g.y * MP1[k]);
+  if (extra_u) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) q[k] += extra_u[k];
+  }
+  cross3(q, pu, &q[3]);
+  if (xn) {
+    q[3] += xn[0];
+    q[4] += xn[1];
+    q[5] += xn[2];
+  }
+  const double we = ww * ec;
+  double a[6];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    a[k] = ww * q[k];
+    beta[k] = fma(q[k], we, beta[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < 6; ++k)
+#pragma unroll
+    for (int l = k; l < 6; ++l) Q[upper_idx(k, l)] = fma(a[k], q[l], Q[upper_idx(k, l)]);
+}
+
 template <bool kJac, int kT, int kMinBlocks, int kProbe = 0>
 __global__ void __launch_bounds__(kT, kMinBlocks)
     linearize_kernel(const pba_frame* __restrict__ frames, const pba_pair* __restrict__ pairs,
@@ -413,53 +455,38 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     const double wI = smI ? cfg.omega[0] : cfg.omega[0] * (dI * __drcp_rn(sI));
     const double wD = smD ? cfg.omega[1] : cfg.omega[1] * (dD * __drcp_rn(sD));
     const double wN = smN ? 1.0 : dN * inv_sN;
-    const int n_ch = normal_on ? 5 : 2;
-#pragma unroll 1
-    for (int c = 0; c < n_ch; ++c) {
-      // bilinear gradient of channel c: the gradient images are interpolated
-      // (cues.py:448-450), not differentiated
-      const double2 g00 = __ldg(reinterpret_cast<const double2*>(&t00->g[2 * c]));
-      const double2 g01 = __ldg(reinterpret_cast<const double2*>(&t00[1].g[2 * c]));
-      const double2 g10 = __ldg(reinterpret_cast<const double2*>(&t10->g[2 * c]));
-      const double2 g11 = __ldg(reinterpret_cast<const double2*>(&t10[1].g[2 * c]));
-      const double gc = bil(g00.x, g01.x, g10.x, g11.x, wx, wy);
-      const double gr_ = bil(g00.y, g01.y, g10.y, g11.y, wx, wy);
-      // q = [u; u x p_u (+ m_k x R_o n)],  u = M_i^T v_c,  v_c = -(grad P) (+ depth cue)
-      double q[6];
+    // Gradients of the four corners, fetched in two batches (the lines are in
+    // L1 after the value loads) and interpolated with the corner weights;
+    // the gradient images are interpolated, not differentiated (cues.py:448-450).
+    const double w00 = (1.0 - wx) * (1.0 - wy), w01 = wx * (1.0 - wy);
+    const double w10 = (1.0 - wx) * wy, w11 = wx * wy;
+    const double2* g00p = reinterpret_cast<const double2*>(t00->g);
+    const double2* g01p = reinterpret_cast<const double2*>(t00[1].g);
+    const double2* g10p = reinterpret_cast<const double2*>(t10->g);
+    const double2* g11p = reinterpret_cast<const double2*>(t10[1].g);
+    double2 gI, gD;
+    {
+      const double2 i00 = __ldg(g00p), i01 = __ldg(g01p), i10 = __ldg(g10p), i11 = __ldg(g11p);
+      const double2 d00 = __ldg(g00p + 1), d01 = __ldg(g01p + 1), d10 = __ldg(g10p + 1),
+                    d11 = __ldg(g11p + 1);
+      gI = bil4(i00, i01, i10, i11, w00, w01, w10, w11);
+      gD = bil4(d00, d01, d10, d11, w00, w01, w10, w11);
+    }
+    accumulate_channel(Q, beta, gI, MP0, MP1, nullptr, pu, nullptr, wI, e0);
+    accumulate_channel(Q, beta, gD, MP0, MP1, ud, pu, nullptr, wD, e1);
+    if (normal_on) {
+      double2 gN[3];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) q[k] = -(gc * MP0[k] + gr_ * MP1[k]);
-      double ww, ec;
-      if (c == 0) {
-        ww = wI;
-        ec = e0;
-      } else if (c == 1) {
-#pragma unroll
-        for (int k = 0; k < 3; ++k) q[k] += ud[k];
-        ww = wD;
-        ec = e1;
-      } else {
-        ww = wN * (c == 2 ? cfg.omega[2] : (c == 3 ? cfg.omega[3] : cfg.omega[4]));
-        ec = c == 2 ? e2 : (c == 3 ? e3 : e4);
-      }
-      cross3(q, pu, &q[3]);
-      if (c >= 2) {
-        double xn[3];
-        cross3(&S.Mi[3 * (c - 2)], no, xn);
-        q[3] += xn[0];
-        q[4] += xn[1];
-        q[5] += xn[2];
-      }
-      const double we = ww * ec;
-      double a[6];
-#pragma unroll
-      for (int k = 0; k < 6; ++k) {
-        a[k] = ww * q[k];
-        beta[k] = fma(q[k], we, beta[k]);
-      }
-#pragma unroll
-      for (int k = 0; k < 6; ++k)
-#pragma unroll
-        for (int l = k; l < 6; ++l) Q[upper_idx(k, l)] = fma(a[k], q[l], Q[upper_idx(k, l)]);
+      for (int k = 0; k < 3; ++k)
+        gN[k] = bil4(__ldg(g00p + 2 + k), __ldg(g01p + 2 + k), __ldg(g10p + 2 + k),
+                     __ldg(g11p + 2 + k), w00, w01, w10, w11);
+      double xn[3];
+      cross3(&S.Mi[0], no, xn);
+      accumulate_channel(Q, beta, gN[0], MP0, MP1, nullptr, pu, xn, wN * cfg.omega[2], e2);
+      cross3(&S.Mi[3], no, xn);
+      accumulate_channel(Q, beta, gN[1], MP0, MP1, nullptr, pu, xn, wN * cfg.omega[3], e3);
+      cross3(&S.Mi[6], no, xn);
+      accumulate_channel(Q, beta, gN[2], MP0, MP1, nullptr, pu, xn, wN * cfg.omega[4], e4);
     }
   }
 
