@@ -232,101 +232,6 @@ __device__ __forceinline__ void accumulate_channel(double* Q, double* beta, doub
     for (int l = k; l < 6; ++l) Q[upper_idx(k, l)] = fma(a[k], q[l], Q[upper_idx(k, l)]);
 }
 
-// Projection of one source pixel (stage 1 of the pixel pipeline): everything
-// from the source texel up to the bilinear footprint, plus an L1 prefetch of
-// the four destination texel lines, so that by the time the pixel is
-// processed (one iteration later) its gather hits L1.
-struct Proj {
-  double pb[3];
-  double wx, wy, dist, inv_rho, inv_dist, isrc, nzs;
-  int dp, sp;
-  uint32_t sm;  // source mask bits; 0 = pixel produces no residual
-};
-
-__device__ __forceinline__ void prefetch_l1(const void* p) {
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-}
-
-__device__ __forceinline__ void project_pixel(const PairSetup& S, int row, int col, double2 s_id,
-                                              double2 s2, Proj& P) {
-  P.sm = 0;
-  const uint32_t sm = mask_word(s2);
-  if (!(sm & PBA_MASK_DEPTH_VALID)) return;  // PairContext.build: usable = depth_valid
-  const int sW = S.src_cam.width, sH = S.src_cam.height;
-  const int dW = S.dst_cam.width, dH = S.dst_cam.height;
-  const double dWd = (double)dW, dHd = (double)dH;
-  // ---- unprojection (sensors.py:133-154) ----
-  const double d = s_id.y;
-  double ps[3];
-  if (S.src_cam.model == PBA_SPHERICAL) {
-    const double ca = __ldg(S.src_ray + col), sa = __ldg(S.src_ray + sW + col);
-    const double ce = __ldg(S.src_ray + 2 * sW + row), se = __ldg(S.src_ray + 2 * sW + sH + row);
-    ps[0] = (ce * ca) * d;
-    ps[1] = (ce * sa) * d;
-    ps[2] = se * d;
-  } else {
-    ps[0] = __ldg(S.src_ray + col) * d;
-    ps[1] = __ldg(S.src_ray + 2 * sW + row) * d;
-    ps[2] = d;
-  }
-  // p_u = R_o p + t_o (solver.py:215); p_bar = M_i p_u + cpb (solver.py:235-236)
-  double pu[3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k)
-    pu[k] = S.Ro[3 * k + 0] * ps[0] + S.Ro[3 * k + 1] * ps[1] + S.Ro[3 * k + 2] * ps[2] + S.to[k];
-#pragma unroll
-  for (int k = 0; k < 3; ++k)
-    P.pb[k] = S.Mi[3 * k + 0] * pu[0] + S.Mi[3 * k + 1] * pu[1] + S.Mi[3 * k + 2] * pu[2] + S.cpb[k];
-  const double* pb = P.pb;
-  // ---- projection (sensors.py:95-130): two rsqrt, no division ----
-  double u, v;
-  P.inv_rho = 0.0;
-  if (S.dst_cam.model == PBA_SPHERICAL) {
-    const double rr = pb[0] * pb[0] + pb[1] * pb[1];
-    const double r2 = rr + pb[2] * pb[2];
-    P.inv_dist = rsqrt(r2);
-    P.dist = r2 * P.inv_dist;
-    double az, rho;
-    if (rr > 1e-60) {
-      P.inv_rho = rsqrt(rr);
-      rho = rr * P.inv_rho;
-      az = atan2_tab_r(pb[1], pb[0], P.inv_rho);
-    } else {  // (practically) on the polar axis: library path, atan2's zero semantics
-      rho = sqrt(rr);
-      P.inv_rho = rr > 0.0 ? 1.0 / rho : 0.0;
-      az = atan2(pb[1], pb[0]);
-    }
-    const double el = atan2_tab_r(pb[2], rho, P.inv_dist);
-    u = py_mod(S.dst_cam.fx * az + S.dst_cam.cx, dWd);
-    v = S.dst_cam.fy * el + S.dst_cam.cy;
-  } else {
-    if (!(pb[2] > 0.0)) return;
-    P.inv_dist = __drcp_rn(pb[2]);
-    u = S.dst_cam.fx * pb[0] * P.inv_dist + S.dst_cam.cx;
-    v = S.dst_cam.fy * pb[1] * P.inv_dist + S.dst_cam.cy;
-    P.dist = pb[2];
-  }
-  if (!(P.dist >= S.dst_cam.depth_min && P.dist <= S.dst_cam.depth_max)) return;
-  if (!(u >= 0.0 && u < dWd && v >= 0.0 && v < dHd)) return;
-  // ---- bilinear footprint (cues.py:397-405): inclusive "inside" ----
-  if (!(u <= dWd - 1.0 && v <= dHd - 1.0)) return;
-  int x0 = (int)floor(u), y0 = (int)floor(v);
-  x0 = min(max(x0, 0), dW - 2);
-  y0 = min(max(y0, 0), dH - 2);
-  P.wx = u - x0;
-  P.wy = v - y0;
-  P.dp = y0 * dW + x0;
-  P.sp = row * sW + col;
-  P.isrc = s_id.x;
-  P.nzs = s2.x;
-  P.sm = sm;
-  const Texel* t00 = S.dst_tex + P.dp;
-  prefetch_l1(t00);
-  prefetch_l1(t00 + 1);
-  prefetch_l1(t00 + dW);
-  prefetch_l1(t00 + dW + 1);
-}
-
 template <bool kJac, int kT, int kMinBlocks, int kProbe = 0>
 __global__ void __launch_bounds__(kT, kMinBlocks)
     linearize_kernel(const pba_frame* __restrict__ frames, const pba_pair* __restrict__ pairs,
@@ -364,44 +269,101 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
   const int stride = S.stride;
   int gr = (first + (int)threadIdx.x) / gw;       // strided-grid row / column of
   int gcol = first + (int)threadIdx.x - gr * gw;  // this thread's current pixel
-  // Pixel pipeline per thread: the source texel of pixel k+2 is loading and
-  // pixel k+1 is projected (its destination lines prefetched into L1) while
-  // pixel k is sampled and accumulated.
-  auto load_src = [&](int r, int c, double2& t0, double2& t2) {
-    const double2* t = reinterpret_cast<const double2*>(S.src_tex + r * stride * sW + c * stride);
-    t0 = __ldg(t);
-    t2 = __ldg(t + 2);
-  };
+  // The source texel of the next pixel is always in flight one iteration
+  // ahead: (I, D) and (nz, mask) words, 2 x 16 B.  Masks come from the texel
+  // lines themselves, so a pixel costs two dependent L2 round trips (source
+  // texel, destination texels) instead of four.
   double2 nx0 = make_double2(0.0, 0.0), nx2 = make_double2(0.0, 0.0);
-  Proj cur;
-  cur.sm = 0;
-  int idx = first + (int)threadIdx.x;
-  if (idx < last) {
-    double2 c0, c2;
-    load_src(gr, gcol, c0, c2);
-    project_pixel(S, gr * stride, gcol * stride, c0, c2, cur);
-    advance_pixel(gr, gcol, gw, kT);
-    if (idx + kT < last) load_src(gr, gcol, nx0, nx2);
+  if (first + (int)threadIdx.x < last) {
+    const double2* t = reinterpret_cast<const double2*>(S.src_tex + gr * stride * sW + gcol * stride);
+    nx0 = __ldg(t);
+    nx2 = __ldg(t + 2);
   }
-  for (; idx < last; idx += kT) {
-    Proj nxt;
-    nxt.sm = 0;
-    if (idx + kT < last) {  // project pixel k+1, start loading pixel k+2's source texel
-      const double2 s0 = nx0, s2 = nx2;
-      const int r1 = gr, c1 = gcol;
-      advance_pixel(gr, gcol, gw, kT);
-      if (idx + 2 * kT < last) load_src(gr, gcol, nx0, nx2);
-      project_pixel(S, r1 * stride, c1 * stride, s0, s2, nxt);
+  int ngr = gr, ngcol = gcol;
+  for (int idx = first + (int)threadIdx.x; idx < last; idx += kT, gr = ngr, gcol = ngcol) {
+    const int row = gr * stride;
+    const int col = gcol * stride;
+    const int sp = row * sW + col;
+    const double2 s_id = nx0;  // I, D
+    const uint32_t sm = mask_word(nx2);
+    const double mask_src_nz = nx2.x;
+    ngr = gr;
+    ngcol = gcol;
+    advance_pixel(ngr, ngcol, gw, kT);
+    if (idx + kT < last) {
+      const double2* t =
+          reinterpret_cast<const double2*>(S.src_tex + ngr * stride * sW + ngcol * stride);
+      nx0 = __ldg(t);
+      nx2 = __ldg(t + 2);
     }
-    const Proj P = cur;
-    cur = nxt;
-    if (!P.sm) continue;
-    const double* pb = P.pb;
-    const double wx = P.wx, wy = P.wy, dist = P.dist, inv_rho = P.inv_rho, inv_dist = P.inv_dist;
-    const int dp = P.dp, sp = P.sp;
-    const uint32_t sm = P.sm;
-    const double2 s_id = make_double2(P.isrc, 0.0);
-    const double mask_src_nz = P.nzs;
+    if (!(sm & PBA_MASK_DEPTH_VALID)) continue;  // PairContext.build: usable = depth_valid
+
+    // ---- source cue values and unprojection (sensors.py:133-154) ----
+    const double2* st = reinterpret_cast<const double2*>(S.src_tex + sp);
+    const double d = s_id.y;
+    double ps[3];
+    if (src_sph) {
+      const double ca = __ldg(S.src_ray + col), sa = __ldg(S.src_ray + sW + col);
+      const double ce = __ldg(S.src_ray + 2 * sW + row), se = __ldg(S.src_ray + 2 * sW + sH + row);
+      ps[0] = (ce * ca) * d;
+      ps[1] = (ce * sa) * d;
+      ps[2] = se * d;
+    } else {
+      ps[0] = __ldg(S.src_ray + col) * d;
+      ps[1] = __ldg(S.src_ray + 2 * sW + row) * d;
+      ps[2] = d;
+    }
+    // p_u = R_o p + t_o (solver.py:215)
+    double pu[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      pu[k] = S.Ro[3 * k + 0] * ps[0] + S.Ro[3 * k + 1] * ps[1] + S.Ro[3 * k + 2] * ps[2] + S.to[k];
+    // p_bar = R_o^T (R_j^T (R_i p_u + t_i - t_j) - t_o) = M_i p_u + cpb  (solver.py:235-236)
+    double pb[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      pb[k] = S.Mi[3 * k + 0] * pu[0] + S.Mi[3 * k + 1] * pu[1] + S.Mi[3 * k + 2] * pu[2] + S.cpb[k];
+
+    // ---- project into the destination (sensors.py:95-130) ----
+    // Two independent rsqrt give rho = hypot(x, y), the range and every
+    // reciprocal needed below (inv = 1/rho, 1/range; pinhole: 1/z).
+    double u, v, dist, rho = 0.0, inv_rho = 0.0, inv_dist;
+    if (dst_sph) {
+      const double rr = pb[0] * pb[0] + pb[1] * pb[1];
+      const double r2 = rr + pb[2] * pb[2];
+      inv_dist = rsqrt(r2);
+      dist = r2 * inv_dist;
+      double az;
+      if (rr > 1e-60) {
+        inv_rho = rsqrt(rr);
+        rho = rr * inv_rho;
+        az = atan2_tab_r(pb[1], pb[0], inv_rho);
+      } else {  // (practically) on the polar axis: library path, atan2's zero semantics
+        rho = sqrt(rr);
+        inv_rho = rr > 0.0 ? 1.0 / rho : 0.0;
+        az = atan2(pb[1], pb[0]);
+      }
+      const double el = atan2_tab_r(pb[2], rho, inv_dist);
+      u = py_mod(S.dst_cam.fx * az + S.dst_cam.cx, dWd);
+      v = S.dst_cam.fy * el + S.dst_cam.cy;
+    } else {
+      if (!(pb[2] > 0.0)) continue;
+      inv_dist = __drcp_rn(pb[2]);
+      u = S.dst_cam.fx * pb[0] * inv_dist + S.dst_cam.cx;
+      v = S.dst_cam.fy * pb[1] * inv_dist + S.dst_cam.cy;
+      dist = pb[2];
+    }
+    if (!(dist >= S.dst_cam.depth_min && dist <= S.dst_cam.depth_max)) continue;
+    if (!(u >= 0.0 && u < dWd && v >= 0.0 && v < dHd)) continue;
+
+    // ---- bilinear footprint and validity (cues.py:397-409, 451-456) ----
+    if (!(u <= dWd - 1.0 && v <= dHd - 1.0)) continue;  // inside (u, v >= 0 already)
+    int x0 = (int)floor(u), y0 = (int)floor(v);
+    x0 = min(max(x0, 0), dW - 2);
+    y0 = min(max(y0, 0), dH - 2);
+    const double wx = u - x0, wy = v - y0;
+    // kProbe 1 (diagnostics only): every sample reads the same texel block
+    const int dp = kProbe == 1 ? (dH / 2) * dW + dW / 2 : y0 * dW + x0;
     const Texel* t00 = S.dst_tex + dp;
     const Texel* t10 = t00 + dW;
     // (I, D) and (nz, mask) of the four corners in one round trip
@@ -431,7 +393,7 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     double e2 = 0.0, e3 = 0.0, e4 = 0.0;
     double no[3] = {0.0, 0.0, 0.0};  // R_o n_src
     if (normal_on) {
-      const double2 s_n01 = __ldg(reinterpret_cast<const double2*>(S.src_tex + sp) + 1);  // nx, ny
+      const double2 s_n01 = __ldg(st + 1);  // source nx, ny (same line: L1 hit)
       const double ns2 = mask_src_nz;
       const double2 b00 = __ldg(reinterpret_cast<const double2*>(t00) + 1);
       const double2 b01 = __ldg(reinterpret_cast<const double2*>(t00 + 1) + 1);
@@ -464,13 +426,6 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     ++count;
     if (!kJac) continue;
 
-    // p_u = M_i^T (p_bar - cpb): recomputed, cheaper than carrying it
-    double pu[3];
-    {
-      const double q0 = pb[0] - S.cpb[0], q1 = pb[1] - S.cpb[1], q2 = pb[2] - S.cpb[2];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) pu[k] = q0 * S.Mi[k] + q1 * S.Mi[3 + k] + q2 * S.Mi[6 + k];
-    }
     // ---- projective Jacobian folded with M_i (sensors.py:157-188) ----
     // MP0 = M_i^T P[0,:], MP1 = M_i^T P[1,:], ud = M_i^T (depth-cue direction)
     double MP0[3], MP1[3], ud[3];
