@@ -333,6 +333,8 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
       const double r2 = rr + pb[2] * pb[2];
       inv_dist = rsqrt(r2);
       dist = r2 * inv_dist;
+      // range gate first: it does not depend on the angles (sensors.py:126)
+      if (!(dist >= S.dst_cam.depth_min && dist <= S.dst_cam.depth_max)) continue;
       double az;
       if (rr > 1e-60) {
         inv_rho = rsqrt(rr);
