@@ -232,99 +232,6 @@ __device__ __forceinline__ void accumulate_channel(double* Q, double* beta, doub
     for (int l = k; l < 6; ++l) Q[upper_idx(k, l)] = fma(a[k], q[l], Q[upper_idx(k, l)]);
 }
 
-// Per-warp queue of valid pixels between the two halves of the pixel work.
-// About half of the pixel-pairs are rejected by the occlusion test after the
-// full projection/gather (SURVEY App. C corridor, perturbed poses), so doing
-// the Jacobian/accumulation inline would run it with half the lanes idle.
-// Valid pixels are appended (in lane order) to a 64-entry ring in shared
-// memory and the back half runs on full warps of 32 queued pixels; the order
-// is fixed, so sums stay deterministic.
-constexpr int kQueue = 64;
-enum RecField { R_PB0, R_PB1, R_PB2, R_WX, R_WY, R_IRHO, R_IDIST, R_E0, R_E1, R_E2, R_E3, R_E4,
-                R_WI, R_WD, R_WN, R_NO0, R_NO1, R_NO2, R_NFIELDS };
-struct WarpQueue {
-  double f[R_NFIELDS][kQueue];
-  int dp[kQueue];
-  int normal_on[kQueue];
-};
-
-// Back half for one queued pixel: projective Jacobian folded with M_i, the
-// five cue channels in the q-basis, Q += w q q^T, beta += q w e.
-__device__ __forceinline__ void back_half(const PairSetup& S, const WarpQueue& W, int slot,
-                                          const pba_config& cfg, double* Q, double* beta) {
-  const double pb[3] = {W.f[R_PB0][slot], W.f[R_PB1][slot], W.f[R_PB2][slot]};
-  const double wx = W.f[R_WX][slot], wy = W.f[R_WY][slot];
-  const double inv_rho = W.f[R_IRHO][slot], iz = W.f[R_IDIST][slot];
-  const int dW = S.dst_cam.width;
-  // p_u = M_i^T (p_bar - cpb)
-  double pu[3];
-  {
-    const double q0 = pb[0] - S.cpb[0], q1 = pb[1] - S.cpb[1], q2 = pb[2] - S.cpb[2];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) pu[k] = q0 * S.Mi[k] + q1 * S.Mi[3 + k] + q2 * S.Mi[6 + k];
-  }
-  // MP0 = M_i^T P[0,:], MP1 = M_i^T P[1,:], ud = M_i^T (depth-cue direction)
-  double MP0[3], MP1[3], ud[3];
-  if (S.dst_cam.model == PBA_SPHERICAL) {
-    const double rho2 = pb[0] * pb[0] + pb[1] * pb[1];
-    const double f0 = S.dst_cam.fx * (inv_rho * inv_rho);    // fx / rho^2
-    const double f1 = S.dst_cam.fy * (inv_rho * (iz * iz));  // fy / (rho r^2)
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const double m0 = S.Mi[k], m1 = S.Mi[3 + k], m2 = S.Mi[6 + k];
-      MP0[k] = f0 * (pb[0] * m1 - pb[1] * m0);
-      MP1[k] = f1 * (rho2 * m2 - pb[2] * (pb[0] * m0 + pb[1] * m1));
-      ud[k] = iz * (pb[0] * m0 + pb[1] * m1 + pb[2] * m2);
-    }
-  } else {
-    const double f0 = S.dst_cam.fx * iz, f1 = S.dst_cam.fy * iz;
-    const double xz = pb[0] * iz, yz = pb[1] * iz;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const double m2 = S.Mi[6 + k];
-      MP0[k] = f0 * (S.Mi[k] - xz * m2);
-      MP1[k] = f1 * (S.Mi[3 + k] - yz * m2);
-      ud[k] = m2;
-    }
-  }
-  // gradients of the four corners (lines still in L1), corner-weight interpolation;
-  // the gradient images are interpolated, not differentiated (cues.py:448-450)
-  const double w00 = (1.0 - wx) * (1.0 - wy), w01 = wx * (1.0 - wy);
-  const double w10 = (1.0 - wx) * wy, w11 = wx * wy;
-  const Texel* t00 = S.dst_tex + W.dp[slot];
-  const Texel* t10 = t00 + dW;
-  const double2* g00p = reinterpret_cast<const double2*>(t00->g);
-  const double2* g01p = reinterpret_cast<const double2*>(t00[1].g);
-  const double2* g10p = reinterpret_cast<const double2*>(t10->g);
-  const double2* g11p = reinterpret_cast<const double2*>(t10[1].g);
-  double2 gI, gD;
-  {
-    const double2 i00 = __ldg(g00p), i01 = __ldg(g01p), i10 = __ldg(g10p), i11 = __ldg(g11p);
-    const double2 d00 = __ldg(g00p + 1), d01 = __ldg(g01p + 1), d10 = __ldg(g10p + 1),
-                  d11 = __ldg(g11p + 1);
-    gI = bil4(i00, i01, i10, i11, w00, w01, w10, w11);
-    gD = bil4(d00, d01, d10, d11, w00, w01, w10, w11);
-  }
-  accumulate_channel(Q, beta, gI, MP0, MP1, nullptr, pu, nullptr, W.f[R_WI][slot], W.f[R_E0][slot]);
-  accumulate_channel(Q, beta, gD, MP0, MP1, ud, pu, nullptr, W.f[R_WD][slot], W.f[R_E1][slot]);
-  if (W.normal_on[slot]) {
-    const double no[3] = {W.f[R_NO0][slot], W.f[R_NO1][slot], W.f[R_NO2][slot]};
-    const double wN = W.f[R_WN][slot];
-    double2 gN[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k)
-      gN[k] = bil4(__ldg(g00p + 2 + k), __ldg(g01p + 2 + k), __ldg(g10p + 2 + k),
-                   __ldg(g11p + 2 + k), w00, w01, w10, w11);
-    double xn[3];
-    cross3(&S.Mi[0], no, xn);
-    accumulate_channel(Q, beta, gN[0], MP0, MP1, nullptr, pu, xn, wN * cfg.omega[2], W.f[R_E2][slot]);
-    cross3(&S.Mi[3], no, xn);
-    accumulate_channel(Q, beta, gN[1], MP0, MP1, nullptr, pu, xn, wN * cfg.omega[3], W.f[R_E3][slot]);
-    cross3(&S.Mi[6], no, xn);
-    accumulate_channel(Q, beta, gN[2], MP0, MP1, nullptr, pu, xn, wN * cfg.omega[4], W.f[R_E4][slot]);
-  }
-}
-
 template <bool kJac, int kT, int kMinBlocks, int kProbe = 0>
 __global__ void __launch_bounds__(kT, kMinBlocks)
     linearize_kernel(const pba_frame* __restrict__ frames, const pba_pair* __restrict__ pairs,
@@ -334,7 +241,6 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
   __shared__ PairSetup S;
   constexpr int kWarps = kT / 32;
   __shared__ double red[kWarps][kPart];
-  extern __shared__ __align__(16) unsigned char queue_mem[];
 
   const long chunk = blockIdx.x;
   const int pair = chunk_table[2 * chunk];
@@ -351,10 +257,6 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
   double cost = 0.0;
   int count = 0;
 
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  WarpQueue& W = reinterpret_cast<WarpQueue*>(queue_mem)[warp];
-  int q_head = 0, q_n = 0;  // warp-uniform ring state
-
   const int last = min(first + chunk_pixels, S.n_px);
   const int sW = S.src_cam.width, sH = S.src_cam.height;
   const int dW = S.dst_cam.width, dH = S.dst_cam.height;
@@ -362,200 +264,236 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
   const bool dst_sph = S.dst_cam.model == PBA_SPHERICAL;
   const double dWd = (double)dW, dHd = (double)dH;
   const double sqw0 = sqrt(cfg.omega[0]), sqw1 = sqrt(cfg.omega[1]);
+
   const int gw = S.grid_w;
   const int stride = S.stride;
-  const unsigned lane_lt = (1u << lane) - 1u;
-
   int gr = (first + (int)threadIdx.x) / gw;       // strided-grid row / column of
   int gcol = first + (int)threadIdx.x - gr * gw;  // this thread's current pixel
-  // the next pixel's source texel ((I, D) and (nz, mask) words) is in flight
+  // The source texel of the next pixel is always in flight one iteration
+  // ahead: (I, D) and (nz, mask) words, 2 x 16 B.  Masks come from the texel
+  // lines themselves, so a pixel costs two dependent L2 round trips (source
+  // texel, destination texels) instead of four.
   double2 nx0 = make_double2(0.0, 0.0), nx2 = make_double2(0.0, 0.0);
   if (first + (int)threadIdx.x < last) {
     const double2* t = reinterpret_cast<const double2*>(S.src_tex + gr * stride * sW + gcol * stride);
     nx0 = __ldg(t);
     nx2 = __ldg(t + 2);
   }
-  // warp-uniform loop: lanes past the end of the chunk ride along inactive
-  for (int base = first + warp * 32; base < last; base += kT) {
-    const int idx = base + lane;
-    const bool active = idx < last;
-    const int row = gr * stride, col = gcol * stride;
+  int ngr = gr, ngcol = gcol;
+  for (int idx = first + (int)threadIdx.x; idx < last; idx += kT, gr = ngr, gcol = ngcol) {
+    const int row = gr * stride;
+    const int col = gcol * stride;
     const int sp = row * sW + col;
     const double2 s_id = nx0;  // I, D
     const uint32_t sm = mask_word(nx2);
-    const double src_nz = nx2.x;
-    advance_pixel(gr, gcol, gw, kT);
+    const double mask_src_nz = nx2.x;
+    ngr = gr;
+    ngcol = gcol;
+    advance_pixel(ngr, ngcol, gw, kT);
     if (idx + kT < last) {
-      const double2* t = reinterpret_cast<const double2*>(S.src_tex + gr * stride * sW + gcol * stride);
+      const double2* t =
+          reinterpret_cast<const double2*>(S.src_tex + ngr * stride * sW + ngcol * stride);
       nx0 = __ldg(t);
       nx2 = __ldg(t + 2);
     }
-    bool valid = false;
-    // record fields of this lane's pixel (written to the queue if valid)
-    double pb[3], wx = 0.0, wy = 0.0, inv_rho = 0.0, inv_dist = 0.0;
-    double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0, e4 = 0.0, wI = 0.0, wD = 0.0, wN = 0.0;
-    double no[3] = {0.0, 0.0, 0.0};
-    int dp = 0;
-    bool normal_on = false;
-    do {  // front half; `break` = this pixel contributes nothing
-      if (!active || !(sm & PBA_MASK_DEPTH_VALID)) break;  // usable = depth_valid (solver.py:200)
-      // ---- unprojection (sensors.py:133-154) ----
-      const double d = s_id.y;
-      double ps[3];
-      if (src_sph) {
-        const double ca = __ldg(S.src_ray + col), sa = __ldg(S.src_ray + sW + col);
-        const double ce = __ldg(S.src_ray + 2 * sW + row), se = __ldg(S.src_ray + 2 * sW + sH + row);
-        ps[0] = (ce * ca) * d;
-        ps[1] = (ce * sa) * d;
-        ps[2] = se * d;
-      } else {
-        ps[0] = __ldg(S.src_ray + col) * d;
-        ps[1] = __ldg(S.src_ray + 2 * sW + row) * d;
-        ps[2] = d;
-      }
-      // p_u = R_o p + t_o (solver.py:215); p_bar = M_i p_u + cpb (solver.py:235-236)
-      double pu[3];
-#pragma unroll
-      for (int k = 0; k < 3; ++k)
-        pu[k] = S.Ro[3 * k + 0] * ps[0] + S.Ro[3 * k + 1] * ps[1] + S.Ro[3 * k + 2] * ps[2] + S.to[k];
-#pragma unroll
-      for (int k = 0; k < 3; ++k)
-        pb[k] = S.Mi[3 * k + 0] * pu[0] + S.Mi[3 * k + 1] * pu[1] + S.Mi[3 * k + 2] * pu[2] + S.cpb[k];
-      // ---- projection (sensors.py:95-130): two rsqrt, no division ----
-      double u, v, dist;
-      if (dst_sph) {
-        const double rr = pb[0] * pb[0] + pb[1] * pb[1];
-        const double r2 = rr + pb[2] * pb[2];
-        inv_dist = rsqrt(r2);
-        dist = r2 * inv_dist;
-        if (!(dist >= S.dst_cam.depth_min && dist <= S.dst_cam.depth_max)) break;
-        double az, rho;
-        if (rr > 1e-60) {
-          inv_rho = rsqrt(rr);
-          rho = rr * inv_rho;
-          az = atan2_tab_r(pb[1], pb[0], inv_rho);
-        } else {  // (practically) on the polar axis: library path, atan2's zero semantics
-          rho = sqrt(rr);
-          inv_rho = rr > 0.0 ? 1.0 / rho : 0.0;
-          az = atan2(pb[1], pb[0]);
-        }
-        const double el = atan2_tab_r(pb[2], rho, inv_dist);
-        u = py_mod(S.dst_cam.fx * az + S.dst_cam.cx, dWd);
-        v = S.dst_cam.fy * el + S.dst_cam.cy;
-      } else {
-        if (!(pb[2] > 0.0)) break;
-        inv_dist = __drcp_rn(pb[2]);
-        u = S.dst_cam.fx * pb[0] * inv_dist + S.dst_cam.cx;
-        v = S.dst_cam.fy * pb[1] * inv_dist + S.dst_cam.cy;
-        dist = pb[2];
-      }
-      if (!(dist >= S.dst_cam.depth_min && dist <= S.dst_cam.depth_max)) break;
-      if (!(u >= 0.0 && u < dWd && v >= 0.0 && v < dHd)) break;
-      // ---- bilinear footprint and validity (cues.py:397-409, 451-456) ----
-      if (!(u <= dWd - 1.0 && v <= dHd - 1.0)) break;  // inclusive "inside"
-      int x0 = (int)floor(u), y0 = (int)floor(v);
-      x0 = min(max(x0, 0), dW - 2);
-      y0 = min(max(y0, 0), dH - 2);
-      wx = u - x0;
-      wy = v - y0;
-      dp = kProbe == 1 ? (dH / 2) * dW + dW / 2 : y0 * dW + x0;
-      const Texel* t00 = S.dst_tex + dp;
-      const Texel* t10 = t00 + dW;
-      // (I, D) and (nz, mask) of the four corners in one round trip
-      const double2 a00 = __ldg(reinterpret_cast<const double2*>(t00));
-      const double2 a01 = __ldg(reinterpret_cast<const double2*>(t00 + 1));
-      const double2 a10 = __ldg(reinterpret_cast<const double2*>(t10));
-      const double2 a11 = __ldg(reinterpret_cast<const double2*>(t10 + 1));
-      const double2 m00 = __ldg(reinterpret_cast<const double2*>(t00) + 2);
-      const double2 m01 = __ldg(reinterpret_cast<const double2*>(t00 + 1) + 2);
-      const double2 m10 = __ldg(reinterpret_cast<const double2*>(t10) + 2);
-      const double2 m11 = __ldg(reinterpret_cast<const double2*>(t10 + 1) + 2);
-      const uint32_t mk = mask_word(m00) & mask_word(m01) & mask_word(m10) & mask_word(m11);
-      if (!(mk & PBA_MASK_SAMP_CORE)) break;  // core_ok
-      const double Dd = bil(a00.y, a01.y, a10.y, a11.y, wx, wy);
-      // zeta_d: range for spherical, z for pinhole (solver.py:240)
-      e1 = dist - Dd;
-      if (e1 > S.occ_tol) break;  // occluded (solver.py:254-258)
-      if (kJac && dst_sph && !(pb[0] * pb[0] + pb[1] * pb[1] > 0.0)) break;  // ok_jac
-      e0 = s_id.x - bil(a00.x, a01.x, a10.x, a11.x, wx, wy);
-      normal_on = (mk & PBA_MASK_SAMP_NORMAL) && (sm & PBA_MASK_NORMAL_VALID);
-      if (normal_on) {
-        const double2 s_n01 = __ldg(reinterpret_cast<const double2*>(S.src_tex + sp) + 1);
-        const double ns2 = src_nz;
-        const double2 b00 = __ldg(reinterpret_cast<const double2*>(t00) + 1);
-        const double2 b01 = __ldg(reinterpret_cast<const double2*>(t00 + 1) + 1);
-        const double2 b10 = __ldg(reinterpret_cast<const double2*>(t10) + 1);
-        const double2 b11 = __ldg(reinterpret_cast<const double2*>(t10 + 1) + 1);
-        // rot_n n_src (solver.py:241-248)
-        const double m0 = s_n01.x * S.rotn[0] + s_n01.y * S.rotn[1] + ns2 * S.rotn[2];
-        const double m1 = s_n01.x * S.rotn[3] + s_n01.y * S.rotn[4] + ns2 * S.rotn[5];
-        const double m2 = s_n01.x * S.rotn[6] + s_n01.y * S.rotn[7] + ns2 * S.rotn[8];
-        e2 = m0 - bil(b00.x, b01.x, b10.x, b11.x, wx, wy);
-        e3 = m1 - bil(b00.y, b01.y, b10.y, b11.y, wx, wy);
-        e4 = m2 - bil(m00.x, m01.x, m10.x, m11.x, wx, wy);
-        if (kJac) {
-#pragma unroll
-          for (int k = 0; k < 3; ++k)
-            no[k] = S.Ro[3 * k + 0] * s_n01.x + S.Ro[3 * k + 1] * s_n01.y + S.Ro[3 * k + 2] * ns2;
-        }
-      }
-      // ---- per-cue Huber (solver.py:317-337) ----
-      const double sI = fabs(e0) * sqw0;  // = sqrt(e0^2 w0) up to one rounding
-      const double sD = fabs(e1) * sqw1;
-      const double tN = (e2 * e2 * cfg.omega[2] + e3 * e3 * cfg.omega[3]) + e4 * e4 * cfg.omega[4];
-      const double inv_sN = tN > 1e-300 ? rsqrt(tN) : 0.0;
-      const double sN = tN > 1e-300 ? tN * inv_sN : sqrt(tN);
-      const double dI = cfg.huber_delta[0], dD = cfg.huber_delta[1], dN = cfg.huber_delta[2];
-      const bool smI = sI <= dI, smD = sD <= dD, smN = sN <= dN;
-      cost += (smI ? sI * sI : dI * (2.0 * sI - dI)) + (smD ? sD * sD : dD * (2.0 * sD - dD)) +
-              (smN ? sN * sN : dN * (2.0 * sN - dN));
-      ++count;
-      if (kJac) {
-        wI = smI ? cfg.omega[0] : cfg.omega[0] * (dI * __drcp_rn(sI));
-        wD = smD ? cfg.omega[1] : cfg.omega[1] * (dD * __drcp_rn(sD));
-        wN = smN ? 1.0 : dN * inv_sN;
-        valid = true;
-      }
-    } while (false);
-    if (!kJac) continue;
-    // ---- enqueue valid pixels in lane order; drain full warps ----
-    const unsigned vm = __ballot_sync(0xffffffffu, valid);
-    if (valid) {
-      const int slot = (q_head + q_n + __popc(vm & lane_lt)) & (kQueue - 1);
-      W.f[R_PB0][slot] = pb[0];
-      W.f[R_PB1][slot] = pb[1];
-      W.f[R_PB2][slot] = pb[2];
-      W.f[R_WX][slot] = wx;
-      W.f[R_WY][slot] = wy;
-      W.f[R_IRHO][slot] = inv_rho;
-      W.f[R_IDIST][slot] = inv_dist;
-      W.f[R_E0][slot] = e0;
-      W.f[R_E1][slot] = e1;
-      W.f[R_E2][slot] = e2;
-      W.f[R_E3][slot] = e3;
-      W.f[R_E4][slot] = e4;
-      W.f[R_WI][slot] = wI;
-      W.f[R_WD][slot] = wD;
-      W.f[R_WN][slot] = wN;
-      W.f[R_NO0][slot] = no[0];
-      W.f[R_NO1][slot] = no[1];
-      W.f[R_NO2][slot] = no[2];
-      W.dp[slot] = dp;
-      W.normal_on[slot] = normal_on;
+    if (!(sm & PBA_MASK_DEPTH_VALID)) continue;  // PairContext.build: usable = depth_valid
+
+    // ---- source cue values and unprojection (sensors.py:133-154) ----
+    const double2* st = reinterpret_cast<const double2*>(S.src_tex + sp);
+    const double d = s_id.y;
+    double ps[3];
+    if (src_sph) {
+      const double ca = __ldg(S.src_ray + col), sa = __ldg(S.src_ray + sW + col);
+      const double ce = __ldg(S.src_ray + 2 * sW + row), se = __ldg(S.src_ray + 2 * sW + sH + row);
+      ps[0] = (ce * ca) * d;
+      ps[1] = (ce * sa) * d;
+      ps[2] = se * d;
+    } else {
+      ps[0] = __ldg(S.src_ray + col) * d;
+      ps[1] = __ldg(S.src_ray + 2 * sW + row) * d;
+      ps[2] = d;
     }
-    q_n += __popc(vm);
-    __syncwarp();
-    if (q_n >= 32) {
-      back_half(S, W, (q_head + lane) & (kQueue - 1), cfg, Q, beta);
-      q_head = (q_head + 32) & (kQueue - 1);
-      q_n -= 32;
-      __syncwarp();
+    // p_u = R_o p + t_o (solver.py:215)
+    double pu[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      pu[k] = S.Ro[3 * k + 0] * ps[0] + S.Ro[3 * k + 1] * ps[1] + S.Ro[3 * k + 2] * ps[2] + S.to[k];
+    // p_bar = R_o^T (R_j^T (R_i p_u + t_i - t_j) - t_o) = M_i p_u + cpb  (solver.py:235-236)
+    double pb[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      pb[k] = S.Mi[3 * k + 0] * pu[0] + S.Mi[3 * k + 1] * pu[1] + S.Mi[3 * k + 2] * pu[2] + S.cpb[k];
+
+    // ---- project into the destination (sensors.py:95-130) ----
+    // Two independent rsqrt give rho = hypot(x, y), the range and every
+    // reciprocal needed below (inv = 1/rho, 1/range; pinhole: 1/z).
+    double u, v, dist, rho = 0.0, inv_rho = 0.0, inv_dist;
+    if (dst_sph) {
+      const double rr = pb[0] * pb[0] + pb[1] * pb[1];
+      const double r2 = rr + pb[2] * pb[2];
+      inv_dist = rsqrt(r2);
+      dist = r2 * inv_dist;
+      // range gate first: it does not depend on the angles (sensors.py:126)
+      if (!(dist >= S.dst_cam.depth_min && dist <= S.dst_cam.depth_max)) continue;
+      double az;
+      if (rr > 1e-60) {
+        inv_rho = rsqrt(rr);
+        rho = rr * inv_rho;
+        az = atan2_tab_r(pb[1], pb[0], inv_rho);
+      } else {  // (practically) on the polar axis: library path, atan2's zero semantics
+        rho = sqrt(rr);
+        inv_rho = rr > 0.0 ? 1.0 / rho : 0.0;
+        az = atan2(pb[1], pb[0]);
+      }
+      const double el = atan2_tab_r(pb[2], rho, inv_dist);
+      u = py_mod(S.dst_cam.fx * az + S.dst_cam.cx, dWd);
+      v = S.dst_cam.fy * el + S.dst_cam.cy;
+    } else {
+      if (!(pb[2] > 0.0)) continue;
+      inv_dist = __drcp_rn(pb[2]);
+      u = S.dst_cam.fx * pb[0] * inv_dist + S.dst_cam.cx;
+      v = S.dst_cam.fy * pb[1] * inv_dist + S.dst_cam.cy;
+      dist = pb[2];
+    }
+    if (!(dist >= S.dst_cam.depth_min && dist <= S.dst_cam.depth_max)) continue;
+    if (!(u >= 0.0 && u < dWd && v >= 0.0 && v < dHd)) continue;
+
+    // ---- bilinear footprint and validity (cues.py:397-409, 451-456) ----
+    if (!(u <= dWd - 1.0 && v <= dHd - 1.0)) continue;  // inside (u, v >= 0 already)
+    int x0 = (int)floor(u), y0 = (int)floor(v);
+    x0 = min(max(x0, 0), dW - 2);
+    y0 = min(max(y0, 0), dH - 2);
+    const double wx = u - x0, wy = v - y0;
+    // kProbe 1 (diagnostics only): every sample reads the same texel block
+    const int dp = kProbe == 1 ? (dH / 2) * dW + dW / 2 : y0 * dW + x0;
+    const Texel* t00 = S.dst_tex + dp;
+    const Texel* t10 = t00 + dW;
+    // (I, D) and (nz, mask) of the four corners in one round trip
+    const double2 a00 = __ldg(reinterpret_cast<const double2*>(t00));
+    const double2 a01 = __ldg(reinterpret_cast<const double2*>(t00 + 1));
+    const double2 a10 = __ldg(reinterpret_cast<const double2*>(t10));
+    const double2 a11 = __ldg(reinterpret_cast<const double2*>(t10 + 1));
+    const double2 m00 = __ldg(reinterpret_cast<const double2*>(t00) + 2);
+    const double2 m01 = __ldg(reinterpret_cast<const double2*>(t00 + 1) + 2);
+    const double2 m10 = __ldg(reinterpret_cast<const double2*>(t10) + 2);
+    const double2 m11 = __ldg(reinterpret_cast<const double2*>(t10 + 1) + 2);
+    const uint32_t mk = mask_word(m00) & mask_word(m01) & mask_word(m10) & mask_word(m11);
+    if (!(mk & PBA_MASK_SAMP_CORE)) continue;  // core_ok
+    const double Dd = bil(a00.y, a01.y, a10.y, a11.y, wx, wy);
+    // zeta_d: range for spherical, z for pinhole (solver.py:240)
+    const double zeta = dst_sph ? dist : pb[2];
+    const double e1 = zeta - Dd;
+    if (e1 > S.occ_tol) continue;  // occluded (solver.py:254-258)
+    double rho2 = 0.0;
+    if (kJac && dst_sph) {
+      rho2 = pb[0] * pb[0] + pb[1] * pb[1];
+      if (!(rho2 > 0.0)) continue;  // ok_jac (sensors.py:173-175; solver.py:262-263)
+    }
+    const double e0 = s_id.x - bil(a00.x, a01.x, a10.x, a11.x, wx, wy);
+
+    const bool normal_on = (mk & PBA_MASK_SAMP_NORMAL) && (sm & PBA_MASK_NORMAL_VALID);
+    double e2 = 0.0, e3 = 0.0, e4 = 0.0;
+    double no[3] = {0.0, 0.0, 0.0};  // R_o n_src
+    if (normal_on) {
+      const double2 s_n01 = __ldg(st + 1);  // source nx, ny (same line: L1 hit)
+      const double ns2 = mask_src_nz;
+      const double2 b00 = __ldg(reinterpret_cast<const double2*>(t00) + 1);
+      const double2 b01 = __ldg(reinterpret_cast<const double2*>(t00 + 1) + 1);
+      const double2 b10 = __ldg(reinterpret_cast<const double2*>(t10) + 1);
+      const double2 b11 = __ldg(reinterpret_cast<const double2*>(t10 + 1) + 1);
+      // rot_n n_src (solver.py:241-248)
+      const double m0 = s_n01.x * S.rotn[0] + s_n01.y * S.rotn[1] + ns2 * S.rotn[2];
+      const double m1 = s_n01.x * S.rotn[3] + s_n01.y * S.rotn[4] + ns2 * S.rotn[5];
+      const double m2 = s_n01.x * S.rotn[6] + s_n01.y * S.rotn[7] + ns2 * S.rotn[8];
+      e2 = m0 - bil(b00.x, b01.x, b10.x, b11.x, wx, wy);
+      e3 = m1 - bil(b00.y, b01.y, b10.y, b11.y, wx, wy);
+      e4 = m2 - bil(m00.x, m01.x, m10.x, m11.x, wx, wy);
+      if (kJac) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+          no[k] = S.Ro[3 * k + 0] * s_n01.x + S.Ro[3 * k + 1] * s_n01.y + S.Ro[3 * k + 2] * ns2;
+      }
+    }
+
+    // ---- per-cue Huber (solver.py:317-337) ----
+    const double sI = fabs(e0) * sqw0;  // = sqrt(e0^2 w0) up to one rounding
+    const double sD = fabs(e1) * sqw1;
+    const double tN = (e2 * e2 * cfg.omega[2] + e3 * e3 * cfg.omega[3]) + e4 * e4 * cfg.omega[4];
+    const double inv_sN = tN > 1e-300 ? rsqrt(tN) : 0.0;
+    const double sN = tN > 1e-300 ? tN * inv_sN : sqrt(tN);
+    const double dI = cfg.huber_delta[0], dD = cfg.huber_delta[1], dN = cfg.huber_delta[2];
+    const bool smI = sI <= dI, smD = sD <= dD, smN = sN <= dN;
+    cost += (smI ? sI * sI : dI * (2.0 * sI - dI)) + (smD ? sD * sD : dD * (2.0 * sD - dD)) +
+            (smN ? sN * sN : dN * (2.0 * sN - dN));
+    ++count;
+    if (!kJac) continue;
+
+    // ---- projective Jacobian folded with M_i (sensors.py:157-188) ----
+    // MP0 = M_i^T P[0,:], MP1 = M_i^T P[1,:], ud = M_i^T (depth-cue direction)
+    double MP0[3], MP1[3], ud[3];
+    if (dst_sph) {
+      const double iz = inv_dist;  // 1/|p_bar| = 1/zeta
+      const double f0 = S.dst_cam.fx * (inv_rho * inv_rho);         // fx / rho^2
+      const double f1 = S.dst_cam.fy * (inv_rho * (iz * iz));       // fy / (rho r^2)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const double m0 = S.Mi[k], m1 = S.Mi[3 + k], m2 = S.Mi[6 + k];
+        MP0[k] = f0 * (pb[0] * m1 - pb[1] * m0);
+        MP1[k] = f1 * (rho2 * m2 - pb[2] * (pb[0] * m0 + pb[1] * m1));
+        ud[k] = iz * (pb[0] * m0 + pb[1] * m1 + pb[2] * m2);
+      }
+    } else {
+      const double iz = inv_dist;  // 1/z
+      const double f0 = S.dst_cam.fx * iz, f1 = S.dst_cam.fy * iz;
+      const double xz = pb[0] * iz, yz = pb[1] * iz;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const double m2 = S.Mi[6 + k];
+        MP0[k] = f0 * (S.Mi[k] - xz * m2);
+        MP1[k] = f1 * (S.Mi[3 + k] - yz * m2);
+        ud[k] = m2;
+      }
+    }
+    const double wI = smI ? cfg.omega[0] : cfg.omega[0] * (dI * __drcp_rn(sI));
+    const double wD = smD ? cfg.omega[1] : cfg.omega[1] * (dD * __drcp_rn(sD));
+    const double wN = smN ? 1.0 : dN * inv_sN;
+    // Gradients of the four corners, fetched in two batches (the lines are in
+    // L1 after the value loads) and interpolated with the corner weights;
+    // the gradient images are interpolated, not differentiated (cues.py:448-450).
+    const double w00 = (1.0 - wx) * (1.0 - wy), w01 = wx * (1.0 - wy);
+    const double w10 = (1.0 - wx) * wy, w11 = wx * wy;
+    const double2* g00p = reinterpret_cast<const double2*>(t00->g);
+    const double2* g01p = reinterpret_cast<const double2*>(t00[1].g);
+    const double2* g10p = reinterpret_cast<const double2*>(t10->g);
+    const double2* g11p = reinterpret_cast<const double2*>(t10[1].g);
+    double2 gI, gD;
+    {
+      const double2 i00 = __ldg(g00p), i01 = __ldg(g01p), i10 = __ldg(g10p), i11 = __ldg(g11p);
+      const double2 d00 = __ldg(g00p + 1), d01 = __ldg(g01p + 1), d10 = __ldg(g10p + 1),
+                    d11 = __ldg(g11p + 1);
+      gI = bil4(i00, i01, i10, i11, w00, w01, w10, w11);
+      gD = bil4(d00, d01, d10, d11, w00, w01, w10, w11);
+    }
+    accumulate_channel(Q, beta, gI, MP0, MP1, nullptr, pu, nullptr, wI, e0);
+    accumulate_channel(Q, beta, gD, MP0, MP1, ud, pu, nullptr, wD, e1);
+    if (normal_on) {
+      double2 gN[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        gN[k] = bil4(__ldg(g00p + 2 + k), __ldg(g01p + 2 + k), __ldg(g10p + 2 + k),
+                     __ldg(g11p + 2 + k), w00, w01, w10, w11);
+      double xn[3];
+      cross3(&S.Mi[0], no, xn);
+      accumulate_channel(Q, beta, gN[0], MP0, MP1, nullptr, pu, xn, wN * cfg.omega[2], e2);
+      cross3(&S.Mi[3], no, xn);
+      accumulate_channel(Q, beta, gN[1], MP0, MP1, nullptr, pu, xn, wN * cfg.omega[3], e3);
+      cross3(&S.Mi[6], no, xn);
+      accumulate_channel(Q, beta, gN[2], MP0, MP1, nullptr, pu, xn, wN * cfg.omega[4], e4);
     }
   }
-  if (kJac && lane < q_n) back_half(S, W, (q_head + lane) & (kQueue - 1), cfg, Q, beta);
 
   // ---- fixed-order reduction: warp butterfly, then warps in order ----
-
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double cnt = (double)count;
   if (kJac) {
 #pragma unroll
@@ -744,24 +682,22 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
     if (variant < 0) {
       const char* env = getenv("PBA_LIN_VARIANT");
       variant = env ? atoi(env) : 4;
-      if (variant < 1 || variant > 5) variant = 4;
+      if (variant < 1 || variant > 9) variant = 4;
     }
     const unsigned grid = (unsigned)n_chunks;
-#define PBA_LAUNCH_LIN(J, T, M)                                                             \
-  do {                                                                                      \
-    const int qsmem = J ? (T / 32) * (int)sizeof(WarpQueue) : 0;                            \
-    cudaFuncSetAttribute(linearize_kernel<J, T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                         qsmem);                                                            \
-    linearize_kernel<J, T, M><<<grid, T, qsmem, st>>>(frames, pairs, chunk_table, chunk_pixels, \
-                                                      poses, extrinsics, *cfg, partials);   \
-  } while (0)
+#define PBA_LAUNCH_LIN(J, T, M) \
+  linearize_kernel<J, T, M><<<grid, T, 0, st>>>(frames, pairs, chunk_table, chunk_pixels, poses, extrinsics, *cfg, partials)
     if (want_jacobians) {
       switch (variant) {
         case 1: PBA_LAUNCH_LIN(true, 256, 1); break;
         case 3: PBA_LAUNCH_LIN(true, 128, 4); break;
         case 5: PBA_LAUNCH_LIN(true, 512, 1); break;
         case 2: PBA_LAUNCH_LIN(true, 256, 2); break;
-
+        case 9:  // diagnostics: destination gather replaced by a fixed texel
+          linearize_kernel<true, 128, 3, 1><<<grid, 128, 0, st>>>(frames, pairs, chunk_table,
+                                                                chunk_pixels, poses, extrinsics,
+                                                                *cfg, partials);
+          break;
         default: PBA_LAUNCH_LIN(true, 128, 3); break;
       }
     } else {
