@@ -350,9 +350,12 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
       v = S.dst_cam.fy * el + S.dst_cam.cy;
     } else {
       if (!(pb[2] > 0.0)) continue;
-      inv_dist = __drcp_rn(pb[2]);
-      u = S.dst_cam.fx * pb[0] * inv_dist + S.dst_cam.cx;
-      v = S.dst_cam.fy * pb[1] * inv_dist + S.dst_cam.cy;
+      // u, v with true IEEE division, exactly as the reference (sensors.py:114-115):
+      // self-projections land on integer pixels where a reciprocal-multiply's
+      // last-bit difference would move floor() and flip sample validity.
+      u = S.dst_cam.fx * pb[0] / pb[2] + S.dst_cam.cx;
+      v = S.dst_cam.fy * pb[1] / pb[2] + S.dst_cam.cy;
+      inv_dist = __drcp_rn(pb[2]);  // Jacobian only
       dist = pb[2];
     }
     if (!(dist >= S.dst_cam.depth_min && dist <= S.dst_cam.depth_max)) continue;

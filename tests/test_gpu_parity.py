@@ -353,3 +353,138 @@ def test_table_atan2_matches_numpy():
     assert np.all(err[small] <= 2 * np.spacing(np.abs(ref[small])) + 1e-300)
     assert np.array_equal(np.signbit(got[-10:]), np.signbit(ref[-10:]))
     assert np.array_equal(got[-10:], ref[-10:])
+
+
+# ---------------------------------------------------------------------------
+# reference test cases (pkg/tests/test_solver.py) restated on the device path
+# ---------------------------------------------------------------------------
+def _affine_image(cam, rng):
+    """test_solver.py:59-77: channels affine in pixel coordinates."""
+    h, w = cam.height, cam.width
+    cols, rows = np.meshgrid(np.arange(w, dtype=float), np.arange(h, dtype=float))
+    a = rng.uniform(-0.01, 0.01, 2)
+    b = rng.uniform(-0.02, 0.02, 2)
+    normals = np.zeros((h, w, 3))
+    base = np.array([0.1, -0.15, -0.97])
+    for k in range(3):
+        c = rng.uniform(-0.003, 0.003, 2)
+        normals[..., k] = base[k] + c[0] * cols + c[1] * rows
+    return P.CueImage(0.5 + a[0] * cols + a[1] * rows, 3.0 + b[0] * cols + b[1] * rows, normals, cam)
+
+
+def _pair_problem(src, dst, x_i, x_j):
+    nodes = [P.FrameNode(0, x_i, P.CuePyramid((src,), (1.0,)), 0.0),
+             P.FrameNode(1, x_j, P.CuePyramid((dst,), (1.0,)), 0.1)]
+    return P.BAProblem(P.MatchGraph(nodes, [P.Edge(0, 1, P.COVISIBILITY)]))
+
+
+def test_all_invalid_destination_kills_all_blocks():
+    """test_solver.py:330-339."""
+    cam = P.Intrinsics(100.0, 95.0, 32.0, 24.0, 64, 48, P.PINHOLE, 0.1, 50.0)
+    src = _affine_image(cam, np.random.default_rng(46))
+    dead = P.CueImage(src.intensity.copy(), np.zeros_like(src.depth), np.zeros_like(src.normals), cam)
+    prob = _pair_problem(src, dead, P.Pose.identity(), P.Pose.identity())
+    rec = _level([prob], 0).linearize(_rows(P.se3.pose_rows([P.Pose.identity()] * 2)[0])).cpu().numpy()
+    assert rec[0, 91] == 0 and np.all(rec[0] == 0.0)
+    assert P.total_error(prob, level=0) == (0.0, 0)
+
+
+def test_intensity_offset_shows_in_cost():
+    """test_solver.py:154-165: a +0.1 intensity offset gives residual -0.1 on every
+    valid block; with Huber delta 0.1 each block costs 0.1^2 (the <= branch)."""
+    cam = P.Intrinsics(100.0, 95.0, 32.0, 24.0, 64, 48, P.PINHOLE, 0.1, 50.0)
+    src = _affine_image(cam, np.random.default_rng(44))
+    dst = P.CueImage(src.intensity + 0.1, src.depth.copy(), src.normals.copy(), cam)
+    prob = _pair_problem(src, dst, P.Pose.identity(), P.Pose.identity())
+    cost, count = P.total_error(prob, level=0)
+    assert count > 0
+    assert abs(cost - count * 0.1 ** 2) <= 1e-9 * cost
+    o_cost, o_count = O.total_error(prob, [P.Pose.identity()] * 2, 0, P.SolverConfig())
+    assert count == o_count and abs(cost - o_cost) <= 1e-12 * o_cost
+
+
+def test_gauge_invariance_of_device_objective():
+    """test_solver.py:423-440 / test_acceptance.py:138-155 on the device cost path."""
+    prob, gt, guess = _room_problem(n=5)
+    rng = np.random.default_rng(49)
+    f_ref, n_ref = P.total_error(prob, level=0)
+    for _ in range(5):
+        g = P.exp(P.PerturbationVector(rng.uniform(-2, 2, 3), rng.uniform(-0.4, 0.4, 3)))
+        moved = [g.compose(n.pose_guess) for n in prob.graph.nodes]
+        f_g, n_g = P.total_error(prob, moved, level=0)
+        assert n_g == n_ref
+        assert abs(f_g - f_ref) / f_ref < 1e-9
+
+
+def test_solve_level_matches_oracle_level_solve():
+    prob, gt, guess = _room_problem(n=6, scales=(0.5, 1.0))
+    poses, records = P.solve_level(prob, guess, 1, max_iterations=4)
+    rows, gens = P.se3.pose_rows(guess)
+    lp = O.OracleLevel([prob], 1, P.SolverConfig())
+    o_rows, _, o_recs = O.solve_level_multi(lp, rows, gens.astype(np.int64), 1, P.SolverConfig(), 4)
+    assert [(r.iteration, r.accepted, r.valid_blocks) for r in records] == [
+        (r.iteration, r.accepted, r.valid_blocks) for r in o_recs]
+    er, et = _pose_err(np.stack([p.as_row() for p in poses]), o_rows)
+    assert er <= 1e-5 and et <= 1e-5
+
+
+def test_reference_objects_accepted_duck_typed():
+    """Drop-in: objects that merely look like the reference types work."""
+    from types import SimpleNamespace as NS
+
+    d = F.load("pinhole_small")
+    prob, _ = F.single_problem(d)
+    nodes = [NS(id=n.id, pose_guess=NS(rotation=n.pose_guess.rotation,
+                                       translation=n.pose_guess.translation, generation=0),
+                pyramid=NS(levels=n.pyramid.levels, scales=n.pyramid.scales,
+                           __len__=lambda: 1), timestamp=n.timestamp, sensor_id=n.sensor_id)
+             for n in prob.graph.nodes]
+
+    class Pyr:
+        def __init__(self, p):
+            self.levels, self.scales = p.levels, p.scales
+
+        def __len__(self):
+            return len(self.levels)
+
+    for n, orig in zip(nodes, prob.graph.nodes):
+        n.pyramid = Pyr(orig.pyramid)
+    duck = NS(graph=NS(nodes=nodes, edges=prob.graph.edges), gauge_index=0,
+              extrinsics_of=prob.extrinsics_of)
+    res = P.solve_hierarchical(duck)
+    _check_trace(res.records, d["trace"])
+
+
+def test_invalid_level_schedule_and_fusion_errors():
+    d = F.load("pinhole_small")
+    prob, _ = F.single_problem(d)
+    with pytest.raises(ValueError):
+        P.solve_hierarchical(prob, levels=[3])
+    probs = F.fusion_problems(F.load("fusion_small"))
+    probs[1].graph.nodes.append(probs[1].graph.nodes[1])
+    with pytest.raises(P.FusionConfigError):
+        P.solve_fusion(probs[0], probs[1], "coupled")
+    with pytest.raises(ValueError):
+        P.solve_fusion(probs[0], probs[0], "sideways")
+
+
+@pytest.mark.parametrize("model", ["pinhole", "spherical"])
+def test_self_projection_counts_match_oracle(model):
+    """Identity poses put every sample on an integer pixel, where floor() is
+    most sensitive to the last bit of the projected coordinate."""
+    rng = np.random.default_rng(7)
+    if model == "pinhole":
+        cam = P.Intrinsics(100.0, 95.0, 32.0, 24.0, 64, 48, P.PINHOLE, 0.1, 50.0)
+    else:
+        cam = P.Intrinsics(64 / (2 * math.pi), 48 / (math.pi / 2), 32.0, 24.0, 64, 48,
+                           P.SPHERICAL, 0.1, 50.0)
+    for trial in range(3):
+        src = _affine_image(cam, rng)
+        prob = _pair_problem(src, src, P.Pose.identity(), P.Pose.identity())
+        for tol in (None, float("inf")):
+            rows = P.se3.pose_rows([P.Pose.identity()] * 2)[0]
+            got = _level([prob], 0, tolerance_override=tol).linearize(_rows(rows)).cpu().numpy()
+            lp = O.OracleLevel([prob], 0, P.SolverConfig())
+            if tol is not None:
+                lp.with_tolerance(tol)
+            F.compare_records(got, lp.records(rows))
