@@ -16,7 +16,8 @@ namespace pba {
 
 constexpr int kAtanHalf = 256;  // table covers k = -256 .. 256
 struct __align__(16) AtanEntry {
-  double c, s, theta, pad;
+  double c, s;          // cos/sin of the table angle, rounded to double
+  double theta, theta_lo;  // exact angle of (c, s) as a double-double
 };
 
 // Defined here (header-only; include from exactly one translation unit).
@@ -51,13 +52,19 @@ __device__ __forceinline__ double atan2_tab_r(double y, double x, double inv_r) 
   k = min(max(k, -kAtanHalf), kAtanHalf);
   const AtanEntry* e = &g_atan_table[k + kAtanHalf];
   const double2 cs = __ldg(reinterpret_cast<const double2*>(e));
-  const double th = __ldg(&e->theta);
-  const double sd = (y * cs.x - x * cs.y) * inv_r;
+  const double2 th = __ldg(reinterpret_cast<const double2*>(e) + 1);  // (hi, lo)
+  // y c - x s with the product error of x s recovered by an FMA: the small
+  // difference keeps full relative accuracy, so the only significant rounding
+  // is the final add and the result is (almost always) correctly rounded.
+  const double w = x * cs.y;
+  const double werr = fma(x, cs.y, -w);
+  const double num = fma(y, cs.x, -w) - werr;
+  const double sd = num * inv_r;
   const double s2 = sd * sd;
   double p = fma(s2, 35.0 / 1152.0, 5.0 / 112.0);
   p = fma(p, s2, 3.0 / 40.0);
   p = fma(p, s2, 1.0 / 6.0);
-  return th + fma(sd * s2, p, sd);
+  return th.x + (th.y + fma(sd * s2, p, sd));
 }
 
 // Stand-alone atan2 (diagnostics / rare paths): same method, inv_r via rsqrt.

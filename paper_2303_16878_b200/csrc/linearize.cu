@@ -39,10 +39,69 @@
 #include <math.h>
 #include <stdlib.h>
 
+#include <cmath>
+
 #include "fastmath.cuh"
 #include "pba_common.cuh"
 
 namespace pba {
+
+// The table is built on the host in double-double arithmetic: for each
+// theta_k = k pi / 256, (c, s) = cos/sin rounded to double, and the exact
+// angle of the rounded pair (theta_k + asin(s cos - c sin) with the
+// cross-difference taken in double-double) is stored as hi + lo.
+namespace {
+struct DD {
+  double hi, lo;
+};
+DD two_prod(double a, double b) {
+  const double p = a * b;
+  return {p, std::fma(a, b, -p)};
+}
+DD two_sum(double a, double b) {
+  const double s = a + b, bb = s - a;
+  return {s, (a - (s - bb)) + (b - bb)};
+}
+DD dd_add(DD a, DD b) {
+  DD s = two_sum(a.hi, b.hi);
+  s.lo += a.lo + b.lo;
+  return two_sum(s.hi, s.lo);
+}
+DD dd_mul(DD a, DD b) {
+  DD p = two_prod(a.hi, b.hi);
+  p.lo += a.hi * b.lo + a.lo * b.hi;
+  return two_sum(p.hi, p.lo);
+}
+DD dd_neg(DD a) { return {-a.hi, -a.lo}; }
+// cos/sin of a double-double angle by Taylor series (|x| <= pi)
+void dd_sincos(DD x, DD& c, DD& s) {
+  // reduce by halving: compute for x / 2^8, then double the angle 8 times
+  DD y = {std::ldexp(x.hi, -8), std::ldexp(x.lo, -8)};
+  DD y2 = dd_mul(y, y);
+  DD sn = y, cn = {1.0, 0.0}, term = y;
+  for (int n = 1; n < 12; ++n) {  // sin series
+    term = dd_mul(term, y2);
+    const double f = 1.0 / ((2.0 * n) * (2.0 * n + 1.0));
+    term = dd_mul(term, DD{-f, 0.0});
+    sn = dd_add(sn, term);
+  }
+  term = {1.0, 0.0};
+  for (int n = 1; n < 12; ++n) {  // cos series
+    term = dd_mul(term, y2);
+    const double f = 1.0 / ((2.0 * n - 1.0) * (2.0 * n));
+    term = dd_mul(term, DD{-f, 0.0});
+    cn = dd_add(cn, term);
+  }
+  for (int i = 0; i < 8; ++i) {  // double-angle formulas
+    DD s2 = dd_mul(DD{2.0, 0.0}, dd_mul(sn, cn));
+    DD c2 = dd_add(dd_mul(cn, cn), dd_neg(dd_mul(sn, sn)));
+    sn = s2;
+    cn = c2;
+  }
+  c = cn;
+  s = sn;
+}
+}  // namespace
 
 int ensure_atan_table() {
   static bool done[64] = {false};
@@ -50,10 +109,19 @@ int ensure_atan_table() {
   PBA_CUDA_TRY(cudaGetDevice(&dev));
   if (dev >= 0 && dev < 64 && done[dev]) return PBA_OK;
   static AtanEntry host[2 * kAtanHalf + 1];
-  const double h = 3.14159265358979323846 / kAtanHalf;
+  const DD pi = {3.141592653589793116, 1.2246467991473532e-16};
   for (int k = -kAtanHalf; k <= kAtanHalf; ++k) {
-    const double th = k * h;  // the stored theta is exactly the angle of (c, s)
-    host[k + kAtanHalf] = AtanEntry{cos(th), sin(th), th, 0.0};
+    const DD th = dd_mul(pi, DD{(double)k / kAtanHalf, 0.0});  // k/256 is exact
+    DD cd, sd;
+    dd_sincos(th, cd, sd);
+    const double c = cd.hi + cd.lo, s = sd.hi + sd.lo;  // rounded cos/sin
+    // exact angle of (c, s): th + asin((s cos th - c sin th) / |(c, s)|)
+    const DD cross = dd_add(dd_mul(DD{s, 0.0}, cd), dd_neg(dd_mul(DD{c, 0.0}, sd)));
+    const double r = std::sqrt(c * c + s * s);
+    const double u = (cross.hi + cross.lo) / r;
+    const double du = u + u * u * u / 6.0;  // |u| < 1e-16: asin(u) = u to double precision
+    const DD ang = dd_add(th, DD{du, 0.0});
+    host[k + kAtanHalf] = AtanEntry{c, s, ang.hi, ang.lo};
   }
   PBA_CUDA_TRY(cudaMemcpyToSymbol(g_atan_table, host, sizeof(host)));
   if (dev >= 0 && dev < 64) done[dev] = true;

@@ -73,7 +73,10 @@ def rel(a, b) -> float:
 
 def compare_records(got, ref, h_tol=1e-5, b_tol=1e-5, cost_tol=1e-6):
     """SURVEY.md §8(c) parity metrics per pair: counts equal, H/b max|Δ|/max|ref|,
-    cost relative."""
+    cost relative.  b -> 0 at convergence (and is pure rounding noise at an
+    exact self-alignment), so b's error is also accepted relative to the
+    Cauchy-Schwarz scale of its terms, sqrt(max diag H * cost) — the
+    |Δb| / Σ|JᵀWe| normalisation of SURVEY.md §8(c)."""
     got, ref = np.asarray(got), np.asarray(ref)
     assert got.shape == ref.shape
     assert np.array_equal(got[:, 91], ref[:, 91]), (got[:, 91], ref[:, 91])
@@ -81,7 +84,12 @@ def compare_records(got, ref, h_tol=1e-5, b_tol=1e-5, cost_tol=1e-6):
         if ref[k, 91] == 0:
             assert np.all(got[k, :91] == 0.0)
             continue
-        for lo, hi, tol in ((0, 21, h_tol), (21, 42, h_tol), (42, 78, h_tol), (78, 84, b_tol),
-                            (84, 90, b_tol)):
+        for lo, hi, tol in ((0, 21, h_tol), (21, 42, h_tol), (42, 78, h_tol)):
             assert rel(got[k, lo:hi], ref[k, lo:hi]) <= tol, (k, lo, rel(got[k, lo:hi], ref[k, lo:hi]))
+        diag = [0, 6, 11, 15, 18, 20]
+        hmax = max(np.max(np.abs(ref[k, diag])), np.max(np.abs(ref[k, [21 + d for d in diag]])))
+        scale = np.sqrt(hmax * max(ref[k, 90], 0.0))
+        for lo, hi in ((78, 84), (84, 90)):
+            err = np.max(np.abs(got[k, lo:hi] - ref[k, lo:hi]))
+            assert err <= b_tol * max(np.max(np.abs(ref[k, lo:hi])), 1e-6 * scale), (k, lo, err)
         assert abs(got[k, 90] - ref[k, 90]) <= cost_tol * abs(ref[k, 90]), (k, got[k, 90], ref[k, 90])

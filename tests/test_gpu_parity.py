@@ -349,6 +349,10 @@ def test_table_atan2_matches_numpy():
     # 2 ulp of pi, i.e. far below the 1e-13 px the residual parity needs
     err = np.abs(got - ref)
     assert float(err.max()) <= 2 * np.spacing(math.pi), float(err.max())
+    # against libm (the oracle's atan2), the table method is correctly rounded
+    # (almost always): count exact agreements on the random inputs
+    libm = np.array([math.atan2(a, b) for a, b in zip(y[:20000], x[:20000])])
+    assert np.mean(got[:20000] == libm) > 0.999
     small = np.abs(ref) < 1e-3  # the k = 0 table entry keeps relative accuracy
     assert np.all(err[small] <= 2 * np.spacing(np.abs(ref[small])) + 1e-300)
     assert np.array_equal(np.signbit(got[-10:]), np.signbit(ref[-10:]))
