@@ -397,32 +397,43 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     // reciprocal needed below (inv = 1/rho, 1/range; pinhole: 1/z).
     double u, v, dist, rho = 0.0, inv_rho = 0.0, inv_dist;
     if (dst_sph) {
-      const double rr = pb[0] * pb[0] + pb[1] * pb[1];
-      const double r2 = rr + pb[2] * pb[2];
-      inv_dist = rsqrt(r2);
-      dist = r2 * inv_dist;
-      // range gate first: it does not depend on the angles (sensors.py:126)
+      // The reference's roundings are reproduced where they decide validity:
+      // range = sqrt((x^2 + y^2) + z^2) with separately rounded terms
+      // (np.linalg.norm), hypot(x, y) correctly rounded (np.hypot), and
+      // u = fx * az + cx as a multiply then an add (no FMA contraction).
+      // Integer-pixel self-projections make floor(u) sensitive to the last bit.
+      const double xx = __dmul_rn(pb[0], pb[0]), yy = __dmul_rn(pb[1], pb[1]);
+      const double rr = __dadd_rn(xx, yy);
+      const double r2 = __dadd_rn(rr, __dmul_rn(pb[2], pb[2]));
+      dist = __dsqrt_rn(r2);
       if (!(dist >= S.dst_cam.depth_min && dist <= S.dst_cam.depth_max)) continue;
+      inv_dist = rsqrt(r2);
       double az;
       if (rr > 1e-60) {
         inv_rho = rsqrt(rr);
-        rho = rr * inv_rho;
+        // hypot: sqrt of the exact x^2 + y^2 (double-double) with one Newton
+        // correction from the rsqrt estimate -> correctly rounded (almost always)
+        const double bb = rr - xx;
+        const double sum_err = (xx - (rr - bb)) + (yy - bb);  // two_sum(xx, yy) error
+        const double tail = fma(pb[0], pb[0], -xx) + fma(pb[1], pb[1], -yy) + sum_err;
+        const double r0 = rr * inv_rho;
+        rho = fma(fma(-r0, r0, rr) + tail, 0.5 * inv_rho, r0);
         az = atan2_tab_r(pb[1], pb[0], inv_rho);
       } else {  // (practically) on the polar axis: library path, atan2's zero semantics
-        rho = sqrt(rr);
+        rho = hypot(pb[0], pb[1]);
         inv_rho = rr > 0.0 ? 1.0 / rho : 0.0;
         az = atan2(pb[1], pb[0]);
       }
       const double el = atan2_tab_r(pb[2], rho, inv_dist);
-      u = py_mod(S.dst_cam.fx * az + S.dst_cam.cx, dWd);
-      v = S.dst_cam.fy * el + S.dst_cam.cy;
+      u = py_mod(__dadd_rn(__dmul_rn(S.dst_cam.fx, az), S.dst_cam.cx), dWd);
+      v = __dadd_rn(__dmul_rn(S.dst_cam.fy, el), S.dst_cam.cy);
     } else {
       if (!(pb[2] > 0.0)) continue;
-      // u, v with true IEEE division, exactly as the reference (sensors.py:114-115):
-      // self-projections land on integer pixels where a reciprocal-multiply's
-      // last-bit difference would move floor() and flip sample validity.
-      u = S.dst_cam.fx * pb[0] / pb[2] + S.dst_cam.cx;
-      v = S.dst_cam.fy * pb[1] / pb[2] + S.dst_cam.cy;
+      // u, v with true IEEE division and separate roundings, exactly as the
+      // reference (sensors.py:114-115): self-projections land on integer
+      // pixels where a last-bit difference would move floor() and flip validity.
+      u = __dadd_rn(__ddiv_rn(__dmul_rn(S.dst_cam.fx, pb[0]), pb[2]), S.dst_cam.cx);
+      v = __dadd_rn(__ddiv_rn(__dmul_rn(S.dst_cam.fy, pb[1]), pb[2]), S.dst_cam.cy);
       inv_dist = __drcp_rn(pb[2]);  // Jacobian only
       dist = pb[2];
     }
