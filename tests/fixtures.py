@@ -95,4 +95,7 @@ def compare_records(got, ref, h_tol=1e-5, b_tol=1e-5, cost_tol=1e-6):
             # (pkg/tests/test_solver.py:414-420) — b is rounding noise there
             assert err <= max(b_tol * max(np.max(np.abs(ref[k, lo:hi])), 1e-6 * scale), 1e-10), (
                 k, lo, err)
-        assert abs(got[k, 90] - ref[k, 90]) <= cost_tol * abs(ref[k, 90]), (k, got[k, 90], ref[k, 90])
+        # cost: relative, or inside the reference's noise floor of 1e-18 per
+        # valid block (solver.py:490-492) — e.g. an exact self-alignment
+        assert abs(got[k, 90] - ref[k, 90]) <= cost_tol * abs(ref[k, 90]) + 1e-18 * ref[k, 91], (
+            k, got[k, 90], ref[k, 90])
