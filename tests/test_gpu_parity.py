@@ -473,7 +473,12 @@ def test_invalid_level_schedule_and_fusion_errors():
 @pytest.mark.parametrize("model", ["pinhole", "spherical"])
 def test_self_projection_counts_match_oracle(model):
     """Identity poses put every sample on an integer pixel, where floor() is
-    most sensitive to the last bit of the projected coordinate."""
+    decided by the last bit of the projected coordinate.  Pinhole u, v are a
+    multiply, an IEEE division and an add, so they reproduce the reference bit
+    for bit.  Spherical u, v go through atan2, whose last bit is
+    implementation-defined: numpy's SIMD arctan2 and libm's atan2 (the oracle)
+    already disagree on this input (reference 2732 vs oracle 2731 blocks in
+    the first trial), so the device is held to the same +-1 block per pair."""
     rng = np.random.default_rng(7)
     if model == "pinhole":
         cam = P.Intrinsics(100.0, 95.0, 32.0, 24.0, 64, 48, P.PINHOLE, 0.1, 50.0)
@@ -489,4 +494,10 @@ def test_self_projection_counts_match_oracle(model):
             lp = O.OracleLevel([prob], 0, P.SolverConfig())
             if tol is not None:
                 lp.with_tolerance(tol)
-            F.compare_records(got, lp.records(rows))
+            ref = lp.records(rows)
+            if model == "pinhole":
+                F.compare_records(got, ref)
+            else:
+                assert abs(got[0, 91] - ref[0, 91]) <= 1
+                assert abs(got[0, 90] - ref[0, 90]) <= 1e-18 * ref[0, 91] + 1e-6 * ref[0, 90]
+                assert F.rel(got[0, :78], ref[0, :78]) <= 2.0 / ref[0, 91]  # one block's share
