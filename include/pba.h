@@ -203,6 +203,19 @@ int pba_apply_step(const double* poses_in, const int32_t* gen_in, const double* 
                    int32_t n_poses, int32_t gauge, double* poses_out, int32_t* gen_out,
                    int32_t* status, void* stream);
 
+/* ---- match-graph construction: overlap_ratio (graph.py:70-101) ---------
+ * Valid-projection counts for directed candidate pairs (device pointers):
+ * points: sensor-frame points of every frame's valid graph-level pixels
+ * (3 doubles each, concatenated, built on the host exactly as the
+ * reference); point_offsets: n_frames+1; pair_src: source frame per pair;
+ * transforms: 12 doubles per pair, the composed sensor_j^-1 * sensor_i;
+ * dst_cams: destination camera per pair; counts: int64 per pair.  The host
+ * re-decides pairs whose ratio is within a few points of the threshold
+ * with the exact path (pairgraph.build_graph). */
+int pba_overlap_counts(const double* points, const int64_t* point_offsets, const int32_t* pair_src,
+                       const double* transforms, const pba_camera* dst_cams, int32_t n_pairs,
+                       double bound_slack, int64_t* counts, void* stream);
+
 /* ---- diagnostics ------------------------------------------------------
  * The table-corrected fp64 atan2 the spherical projection uses
  * (csrc/fastmath.cuh), exposed so tests can bound its error against the

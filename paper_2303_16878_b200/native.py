@@ -30,7 +30,7 @@ EXPORTED = (
     "pba_kernel_launches",
     "pba_build_texels_scratch_bytes", "pba_build_texels", "pba_plan_chunks", "pba_linearize",
     "pba_plan_assembly", "pba_assemble", "pba_sum_totals", "pba_solve_work_bytes",
-    "pba_solve_dense", "pba_apply_step", "pba_atan2_batch",
+    "pba_solve_dense", "pba_apply_step", "pba_overlap_counts", "pba_atan2_batch",
 )
 
 
@@ -86,6 +86,7 @@ _SIGNATURES = {
     "pba_solve_dense": (ctypes.c_int, [_vp, _vp, _i32, _dbl, _vp, _vp, _vp, _vp, _vp]),
     "pba_apply_step": (ctypes.c_int, [_vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp]),
     "pba_atan2_batch": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp]),
+    "pba_overlap_counts": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _dbl, _vp, _vp]),
 }
 
 _lib = None

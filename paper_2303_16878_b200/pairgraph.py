@@ -139,10 +139,84 @@ def _prefilter(nodes, crit: MatchCriteria) -> list:
     return out
 
 
+def _pose_rows(pose) -> np.ndarray:
+    return np.concatenate([np.asarray(pose.rotation, float).reshape(9),
+                           np.asarray(pose.translation, float).reshape(3)])
+
+
+def _gpu_overlap_verdicts(nodes, candidates, crit, extrinsics, level, stride, cache, device):
+    """Covisibility verdicts for gate-passing candidates with the overlap
+    counts computed on the GPU (csrc/overlap.cu).  Every ratio within
+    `margin` points of the threshold is recomputed with the exact host path,
+    so the verdicts equal the reference's: the device and numpy projections
+    can only disagree on knife-edge points, far fewer than the margin."""
+    import torch
+
+    from . import native as N
+    from .device import camera_struct
+
+    lib = N.load()
+    dev = torch.device(device)
+    off = (extrinsics or SensorExtrinsics.identity()).offset
+    frames = []
+    offsets = [0]
+    for nd in nodes:
+        n_valid, pts, _ = _source_points(nd.pyramid.levels[level], stride, cache)
+        frames.append(pts if n_valid else np.zeros((0, 3)))
+        offsets.append(offsets[-1] + n_valid)
+    points = torch.from_numpy(np.ascontiguousarray(np.concatenate(frames), dtype=np.float64)).to(dev)
+    offs = torch.tensor(offsets, dtype=torch.int64, device=dev)
+    sensor = [nd.pose_guess.compose(off) for nd in nodes]
+    inv = [sp.inverse() for sp in sensor]
+    gated = [ab for ab in candidates if _gates_pass(nodes[ab[0]], nodes[ab[1]], crit)]
+    if not gated:
+        return {}
+    src, trans, cams = [], [], (N.Camera * (2 * len(gated)))()
+    for k, (a, b) in enumerate(gated):
+        for d, (i, j) in enumerate(((a, b), (b, a))):
+            src.append(i)
+            trans.append(_pose_rows(inv[j].compose(sensor[i])))
+            cams[2 * k + d] = camera_struct(nodes[j].pyramid.levels[level].intrinsics)
+    src_t = torch.tensor(src, dtype=torch.int32, device=dev)
+    trans_t = torch.from_numpy(np.array(trans)).to(dev)
+    cams_t = torch.frombuffer(bytearray(bytes(memoryview(cams).cast("B"))),
+                              dtype=torch.uint8).to(dev)
+    counts = torch.zeros(len(src), dtype=torch.int64, device=dev)
+    N.check(lib.pba_overlap_counts(points.data_ptr(), offs.data_ptr(), src_t.data_ptr(),
+                                   trans_t.data_ptr(), cams_t.data_ptr(), len(src), 1e-6,
+                                   counts.data_ptr(), torch.cuda.current_stream(dev).cuda_stream),
+            "pba_overlap_counts")
+    counts = counts.cpu().numpy()
+    n_valid = np.diff(np.array(offsets))
+    verdicts = {}
+    kw = dict(level=level, stride=stride, extrinsics=extrinsics, _cache=cache)
+    margin_pts = 8
+    for k, (a, b) in enumerate(gated):
+        ok = True
+        for d, (i, j) in enumerate(((a, b), (b, a))):
+            nv = int(n_valid[i])
+            if nv == 0:
+                ratio = 0.0
+            else:
+                c = int(counts[2 * k + d])
+                if abs(c - crit.min_overlap_ratio * nv) <= margin_pts:  # near the threshold
+                    ratio = overlap_ratio(nodes[i], nodes[j], **kw)
+                else:
+                    ratio = float(c) / float(nv)
+            if ratio < crit.min_overlap_ratio:
+                ok = False
+                break
+        verdicts[(a, b)] = ok
+    return verdicts
+
+
 def build_graph(nodes, criteria: MatchCriteria | None = None, sequential: bool = True,
                 extrinsics: SensorExtrinsics | None = None, overlap_level: int = 0,
-                overlap_stride: int = 2, threads: int = 1) -> MatchGraph:
-    """Sorted edge list of covisible pairs plus odometry edges (graph.py:123-176)."""
+                overlap_stride: int = 2, threads: int = 1, device=None) -> MatchGraph:
+    """Sorted edge list of covisible pairs plus odometry edges (graph.py:123-176).
+
+    `device` (e.g. "cuda:0", an addition to the reference signature) counts the
+    overlaps on the GPU; the result is the same edge list."""
     crit = criteria or MatchCriteria()
     if len(nodes) < 2:
         raise GraphConfigError(f"need at least 2 frames to build a graph, got {len(nodes)}")
@@ -164,7 +238,11 @@ def build_graph(nodes, criteria: MatchCriteria | None = None, sequential: bool =
         return _pair_matches(nodes[a], nodes[b], crit, extrinsics, overlap_level, overlap_stride,
                              cache)
 
-    if threads > 1:
+    if device is not None:
+        got = _gpu_overlap_verdicts(nodes, candidates, crit, extrinsics, overlap_level,
+                                    overlap_stride, cache, device)
+        verdicts = [got.get(ab, False) for ab in candidates]
+    elif threads > 1:
         with ThreadPoolExecutor(max_workers=threads) as pool:
             verdicts = list(pool.map(check, candidates))
     else:
