@@ -88,7 +88,8 @@ def build_problem(name: str, device, n_override=None):
     crit = P.MatchCriteria(max_translation=c["max_translation"])
     sensor_ext = P.SensorExtrinsics(ext)
     t0 = time.perf_counter()
-    graph = P.build_graph(nodes, crit, extrinsics=sensor_ext, threads=8)
+    graph_device = device if getattr(device, "type", "cpu") == "cuda" else None
+    graph = P.build_graph(nodes, crit, extrinsics=sensor_ext, threads=8, device=graph_device)
     t_graph = time.perf_counter() - t0
     prob = P.BAProblem(graph, {"sensor0": sensor_ext})
     return prob, guess, gt, dict(name=name, desc=c["desc"], frames=n, cam=cam,
