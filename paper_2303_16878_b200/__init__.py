@@ -12,7 +12,8 @@ from .se3 import (InvalidPerturbationError, PerturbationVector, Pose, boxplus, e
                   rotation_angle, skew)
 from .camera import (PINHOLE, SPHERICAL, Intrinsics, SensorExtrinsics, project,
                      projective_jacobian, unproject)
-from .cueimage import CueImage, CuePyramid, DeviceCueImage, PyramidConfigError, footprint_index
+from .cueimage import (CueImage, CuePyramid, DeviceCueImage, NormalConfig, PyramidConfigError,
+                       build_cue_image, build_pyramid, estimate_normals, footprint_index)
 from .pairgraph import (COVISIBILITY, ODOMETRY, Edge, FrameNode, GraphConfigError, MatchCriteria,
                         MatchGraph, build_graph, dump_edges, overlap_ratio)
 from .bundle import (CONSECUTIVE, COUPLED, BAProblem, FusionConfigError, IterationRecord,
@@ -25,9 +26,9 @@ __all__ = [
     "BAProblem", "CONSECUTIVE", "COUPLED", "COVISIBILITY", "CueImage", "CuePyramid",
     "DeviceCueImage", "Edge", "FrameNode", "FusionConfigError", "GraphConfigError",
     "InvalidPerturbationError", "Intrinsics", "IterationRecord", "MatchCriteria", "MatchGraph",
-    "ODOMETRY", "PINHOLE", "PerturbationVector", "Pose", "PyramidConfigError", "SPHERICAL",
+    "NormalConfig", "ODOMETRY", "PINHOLE", "PerturbationVector", "Pose", "PyramidConfigError", "SPHERICAL",
     "SensorExtrinsics", "SolveResult", "SolverConfig", "UnderConstrainedError", "boxplus",
-    "build_graph", "check_connectivity", "dump_edges", "exp", "footprint_index",
+    "build_cue_image", "build_graph", "build_pyramid", "check_connectivity", "dump_edges", "estimate_normals", "exp", "footprint_index",
     "overlap_ratio", "project", "projective_jacobian", "relative", "rotation_angle", "skew",
     "solve_fusion", "solve_hierarchical", "solve_level", "total_error", "unproject",
 ]

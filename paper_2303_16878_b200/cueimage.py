@@ -19,7 +19,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .camera import Intrinsics
+from .camera import Intrinsics, unproject
 
 NORMAL_COHERENCE_MIN_DOT = 0.9  # cues.py:44
 
@@ -240,6 +240,105 @@ def downscale_cues(intensity, depth, normals, depth_ok, normal_ok, s):
     unit = np.zeros_like(mean_n)
     unit[good] = mean_n[good] / nrm[good, None]
     return out_i.reshape(out_h, out_w), out_d.reshape(out_h, out_w), unit.reshape(out_h, out_w, 3)
+
+
+@dataclass(frozen=True)
+class NormalConfig:
+    """Plane-fit normal estimation parameters (cues.py:26-39): Chebyshev
+    window half-width round(k_tau / depth) clamped to [radius_min,
+    radius_max], at least `min_points` valid neighbours, and a middle
+    eigenvalue above degeneracy_ratio x the largest."""
+
+    k_tau: float = 4.0
+    radius_min: float = 2.0
+    radius_max: float = 8.0
+    min_points: int = 6
+    degeneracy_ratio: float = 1e-4
+
+
+def _moment_integral(points: np.ndarray, valid: np.ndarray) -> np.ndarray:
+    """(h+1, w+1, 10) summed-area table of [x y z xx xy xz yy yz zz 1] over
+    valid pixels.  Column-wise then row-wise running sums, the summation
+    order of cues.py:174-176, so window sums round identically."""
+    h, w = valid.shape
+    m = np.zeros((h, w, 10))
+    x, y, z = (np.where(valid, points[..., k], 0.0) for k in range(3))
+    m[..., 0], m[..., 1], m[..., 2] = x, y, z
+    px, py, pz = points[..., 0], points[..., 1], points[..., 2]
+    for k, (a, b) in enumerate(((px, px), (px, py), (px, pz), (py, py), (py, pz), (pz, pz))):
+        m[..., 3 + k] = np.where(valid, a * b, 0.0)
+    m[..., 9] = valid
+    sat = np.zeros((h + 1, w + 1, 10))
+    sat[1:, 1:] = np.cumsum(np.cumsum(m, axis=0), axis=1)
+    return sat
+
+
+def estimate_normals(depth: np.ndarray, cam: Intrinsics, cfg: NormalConfig | None = None) -> np.ndarray:
+    """Observer-facing unit normals from a depth/range image (cues.py:187-246).
+
+    Each valid pixel fits a least-squares plane to the points of its
+    depth-adaptive window (smallest eigenvector of the window's scatter
+    matrix); too few neighbours, a degenerate (line-like) fit, a grazing fit
+    or a non-finite result leave the zero vector.  All pixels are handled in
+    one batch: per-pixel half-widths index the shared summed-area table.
+    """
+    cfg = cfg or NormalConfig()
+    depth = np.asarray(depth, dtype=float)
+    h, w = depth.shape
+    out = np.zeros((h, w, 3))
+    with np.errstate(invalid="ignore"):
+        valid = np.isfinite(depth) & (depth >= cam.depth_min) & (depth <= cam.depth_max)
+    if not valid.any():
+        return out
+    pts = np.zeros((h, w, 3))
+    rr, cc = np.nonzero(valid)
+    pts[rr, cc] = unproject(cam, np.stack([cc.astype(float), rr.astype(float)], axis=-1),
+                            depth[rr, cc])
+    sat = _moment_integral(pts, valid)
+    half = np.clip(np.round(cfg.k_tau / depth[rr, cc]), cfg.radius_min, cfg.radius_max).astype(np.int64)
+    top, bot = np.clip(rr - half, 0, h), np.clip(rr + half + 1, 0, h)
+    lft, rgt = np.clip(cc - half, 0, w), np.clip(cc + half + 1, 0, w)
+    win = sat[bot, rgt] - sat[top, rgt] - sat[bot, lft] + sat[top, lft]
+    cnt = win[:, 9]
+    use = cnt >= cfg.min_points
+    rr, cc, win, cnt = rr[use], cc[use], win[use], cnt[use]
+    if rr.size == 0:
+        return out
+    mu = win[:, 0:3] / cnt[:, None]
+    # scatter[i][j] = S_ij - (count * mu_i) * mu_j, entry by entry (the
+    # lower triangle is what the symmetric eigensolver reads)
+    S = win[:, (3, 4, 5, 4, 6, 7, 5, 7, 8)].reshape(-1, 3, 3)
+    S = S - (cnt[:, None] * mu)[:, :, None] * mu[:, None, :]
+    lam, vec = np.linalg.eigh(S)
+    n = vec[:, :, 0]
+    planar = lam[:, 1] > np.maximum(cfg.degeneracy_ratio * lam[:, 2], 0.0)
+    p = pts[rr, cc]
+    facing = np.einsum("ij,ij->i", n, p)
+    n = np.where(facing[:, None] > 0.0, -n, n)
+    ok = planar & (np.abs(facing) > 1e-12) & np.isfinite(n).all(axis=1)
+    out[rr[ok], cc[ok]] = n[ok]
+    return out
+
+
+def build_cue_image(intensity, depth, cam: Intrinsics, cfg: NormalConfig | None = None,
+                    normals=None) -> CueImage:
+    """Full-resolution cue image, estimating normals unless given (cues.py:329-339)."""
+    if normals is None:
+        normals = estimate_normals(depth, cam, cfg)
+    return CueImage(intensity, depth, normals, cam)
+
+
+def build_pyramid(intensity, depth, cam: Intrinsics, scales=(0.125, 0.25, 0.5),
+                  cfg: NormalConfig | None = None) -> CuePyramid:
+    """Cue pyramid of one intensity/depth pair (cues.py:342-375): normals
+    estimated once at full resolution, then each level downscaled per
+    channel; `scales` coarsest to finest in (0, 1]."""
+    scales = validate_scales(scales)
+    if np.shape(intensity) != np.shape(depth):
+        raise ValueError("intensity and depth shapes disagree")
+    depth = np.where(np.isfinite(depth), depth, 0.0)
+    return build_pyramid_from_normals(intensity, depth, estimate_normals(depth, cam, cfg), cam,
+                                      scales)
 
 
 def build_pyramid_from_normals(intensity, depth, normals, cam: Intrinsics, scales) -> CuePyramid:

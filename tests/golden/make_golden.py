@@ -32,7 +32,7 @@ from photoba.sensors import PINHOLE, Intrinsics, SensorExtrinsics  # noqa: E402
 from photoba.solver import (BAProblem, SolverConfig, _edge_term, _LevelProblem,  # noqa: E402
                             solve_fusion, solve_hierarchical, total_error)
 from photoba.synthetic import box_room_scene, render_view  # noqa: E402
-from rigs import loop_trajectory, seeded_perturbation  # noqa: E402
+from rigs import lidar_cam, loop_trajectory, rgbd_cam, seeded_perturbation  # noqa: E402
 
 OUT = Path(__file__).resolve().parent
 IU = np.triu_indices(6)
@@ -172,6 +172,35 @@ def footprint_case():
     np.savez_compressed(OUT / "footprint.npz", **d)
 
 
+def pyramid_case():
+    """Raw renders + the reference's estimate_normals / build_pyramid outputs
+    (cues.py:187-375) for a pinhole and a spherical sensor."""
+    from photoba.cues import estimate_normals
+    d = {}
+    room = box_room_scene()
+    cams = [("p", rgbd_cam(), Pose(np.eye(3), [-0.4, 0.2, -0.5]), (0.25, 0.5, 1.0)),
+            ("s", lidar_cam(128, 32), Pose(np.eye(3), [0.3, -0.2, 0.1]), (0.25, 0.5, 1.0))]
+    for tag, cam, pose, scales in cams:
+        r = render_view(room, cam, pose)
+        depth = r.depth.copy()
+        rng = np.random.default_rng(5)
+        depth[rng.random(depth.shape) < 0.02] = 0.0  # holes
+        depth[3, 5] = np.nan
+        d[f"{tag}_cam"] = cam_row(cam)
+        d[f"{tag}_I"] = r.intensity
+        d[f"{tag}_D"] = depth
+        d[f"{tag}_normals"] = estimate_normals(depth, cam)
+        pyr = build_pyramid(r.intensity, depth, cam, scales)
+        d[f"{tag}_scales"] = np.array(scales)
+        for l, img in enumerate(pyr.levels):
+            d[f"{tag}_I_{l}"] = img.intensity
+            d[f"{tag}_D_{l}"] = img.depth
+            d[f"{tag}_N_{l}"] = img.normals
+            d[f"{tag}_cam_{l}"] = cam_row(img.intrinsics)
+    np.savez_compressed(OUT / "pyramid.npz", **d)
+    print("pyramid", (OUT / "pyramid.npz").stat().st_size, "bytes")
+
+
 if __name__ == "__main__":
     pin = Intrinsics(40.0, 40.0, 32.0, 24.0, 64, 48, PINHOLE, 0.1, 50.0)
     single_sensor_case("pinhole_small", pin, 4, (1.0,), [0.0, 0.0, 0.1], 51, 0.04,
@@ -182,3 +211,4 @@ if __name__ == "__main__":
                        math.radians(1.5))
     fusion_case()
     footprint_case()
+    pyramid_case()
