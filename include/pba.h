@@ -216,6 +216,32 @@ int pba_overlap_counts(const double* points, const int64_t* point_offsets, const
                        const double* transforms, const pba_camera* dst_cams, int32_t n_pairs,
                        double bound_slack, int64_t* counts, void* stream);
 
+/* ---- cue-pyramid builder: build_pyramid (cues.py:342-375) ---------------
+ * NormalConfig (cues.py:26-39); min_points is compared as a double like the
+ * reference's float window count. */
+typedef struct pba_normal_config {
+  double k_tau, radius_min, radius_max, min_points, degeneracy_ratio;
+} pba_normal_config;
+
+/* Scratch for pba_estimate_normals: the (n, 10, H, W) fp64 moment table. */
+size_t pba_normals_scratch_bytes(const pba_camera* cam, int32_t n_frames);
+/* estimate_normals (cues.py:187-246) for n_frames depth/range images of one
+ * camera (device (n, H, W) fp64, raw: non-finite and out-of-range pixels are
+ * invalid) -> observer-facing unit normals (device (n, H, W, 3), zero where
+ * no plane fits).  ray_table: pba_ray_table_doubles(cam) doubles (device).
+ * Bit-equal to the reference up to the 3x3 eigenproblem (see pyramid.cu). */
+int pba_estimate_normals(const pba_camera* cam, const double* ray_table, const double* depth,
+                         int32_t n_frames, const pba_normal_config* cfg, double* normals,
+                         void* scratch, void* stream);
+/* _downscale_cues (cues.py:278-326) of n_frames full-resolution cue sets
+ * (cam = full-resolution camera; depth already cleaned of non-finite values
+ * as build_pyramid does) to one level of scale s: out_h/out_w must equal
+ * floor(H*s)/floor(W*s).  Bit-equal to the reference. */
+int pba_downscale_cues(const pba_camera* cam, double scale, int32_t n_frames,
+                       const double* intensity, const double* depth, const double* normals,
+                       int32_t out_h, int32_t out_w, double* out_intensity, double* out_depth,
+                       double* out_normals, void* stream);
+
 /* ---- diagnostics ------------------------------------------------------
  * The table-corrected fp64 atan2 the spherical projection uses
  * (csrc/fastmath.cuh), exposed so tests can bound its error against the

@@ -14,6 +14,7 @@ from .camera import (PINHOLE, SPHERICAL, Intrinsics, SensorExtrinsics, project,
                      projective_jacobian, unproject)
 from .cueimage import (CueImage, CuePyramid, DeviceCueImage, NormalConfig, PyramidConfigError,
                        build_cue_image, build_pyramid, estimate_normals, footprint_index)
+from .pyramid_device import build_pyramids_device, estimate_normals_device
 from .pairgraph import (COVISIBILITY, ODOMETRY, Edge, FrameNode, GraphConfigError, MatchCriteria,
                         MatchGraph, build_graph, dump_edges, overlap_ratio)
 from .bundle import (CONSECUTIVE, COUPLED, BAProblem, FusionConfigError, IterationRecord,
@@ -28,7 +29,7 @@ __all__ = [
     "InvalidPerturbationError", "Intrinsics", "IterationRecord", "MatchCriteria", "MatchGraph",
     "NormalConfig", "ODOMETRY", "PINHOLE", "PerturbationVector", "Pose", "PyramidConfigError", "SPHERICAL",
     "SensorExtrinsics", "SolveResult", "SolverConfig", "UnderConstrainedError", "boxplus",
-    "build_cue_image", "build_graph", "build_pyramid", "check_connectivity", "dump_edges", "estimate_normals", "exp", "footprint_index",
+    "build_cue_image", "build_graph", "build_pyramid", "build_pyramids_device", "check_connectivity", "dump_edges", "estimate_normals", "estimate_normals_device", "exp", "footprint_index",
     "overlap_ratio", "project", "projective_jacobian", "relative", "rotation_angle", "skew",
     "solve_fusion", "solve_hierarchical", "solve_level", "total_error", "unproject",
 ]

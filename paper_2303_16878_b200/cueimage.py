@@ -329,10 +329,15 @@ def build_cue_image(intensity, depth, cam: Intrinsics, cfg: NormalConfig | None 
 
 
 def build_pyramid(intensity, depth, cam: Intrinsics, scales=(0.125, 0.25, 0.5),
-                  cfg: NormalConfig | None = None) -> CuePyramid:
+                  cfg: NormalConfig | None = None, device=None) -> CuePyramid:
     """Cue pyramid of one intensity/depth pair (cues.py:342-375): normals
     estimated once at full resolution, then each level downscaled per
-    channel; `scales` coarsest to finest in (0, 1]."""
+    channel; `scales` coarsest to finest in (0, 1].  With `device` (e.g.
+    "cuda") the pyramid is built by the GPU kernels of pyramid_device.py and
+    its levels are DeviceCueImage."""
+    if device is not None:
+        from .pyramid_device import build_pyramids_device
+        return build_pyramids_device(intensity, depth, cam, scales, cfg, device)[0]
     scales = validate_scales(scales)
     if np.shape(intensity) != np.shape(depth):
         raise ValueError("intensity and depth shapes disagree")

@@ -30,7 +30,8 @@ EXPORTED = (
     "pba_kernel_launches",
     "pba_build_texels_scratch_bytes", "pba_build_texels", "pba_plan_chunks", "pba_linearize",
     "pba_plan_assembly", "pba_assemble", "pba_sum_totals", "pba_solve_work_bytes",
-    "pba_solve_dense", "pba_apply_step", "pba_overlap_counts", "pba_atan2_batch",
+    "pba_solve_dense", "pba_apply_step", "pba_overlap_counts", "pba_normals_scratch_bytes",
+    "pba_estimate_normals", "pba_downscale_cues", "pba_atan2_batch",
 )
 
 
@@ -55,6 +56,12 @@ class Pair(ctypes.Structure):
 class Config(ctypes.Structure):
     _fields_ = [("huber_delta", ctypes.c_double * 3), ("omega", ctypes.c_double * 5),
                 ("pixel_stride", ctypes.c_int32), ("_pad", ctypes.c_int32)]
+
+
+class NormalConfigC(ctypes.Structure):
+    _fields_ = [("k_tau", ctypes.c_double), ("radius_min", ctypes.c_double),
+                ("radius_max", ctypes.c_double), ("min_points", ctypes.c_double),
+                ("degeneracy_ratio", ctypes.c_double)]
 
 
 assert ctypes.sizeof(Camera) == 64 and ctypes.sizeof(Frame) == 88 and ctypes.sizeof(Pair) == 32
@@ -87,6 +94,11 @@ _SIGNATURES = {
     "pba_apply_step": (ctypes.c_int, [_vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp]),
     "pba_atan2_batch": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp]),
     "pba_overlap_counts": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _dbl, _vp, _vp]),
+    "pba_normals_scratch_bytes": (_sz, [ctypes.POINTER(Camera), _i32]),
+    "pba_estimate_normals": (ctypes.c_int, [ctypes.POINTER(Camera), _vp, _vp, _i32,
+                                            ctypes.POINTER(NormalConfigC), _vp, _vp, _vp]),
+    "pba_downscale_cues": (ctypes.c_int, [ctypes.POINTER(Camera), _dbl, _i32, _vp, _vp, _vp,
+                                          _i32, _i32, _vp, _vp, _vp, _vp]),
 }
 
 _lib = None

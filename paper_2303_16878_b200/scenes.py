@@ -180,24 +180,34 @@ def host_pyramids(scene, cam, platform_poses, ext: Pose, scales) -> list:
     return out
 
 
-def device_pyramids(scene, cam, platform_poses, ext: Pose, factors, device, batch: int = 64):
+def device_pyramids(scene, cam, platform_poses, ext: Pose, factors, device, batch: int = 64,
+                    normals: str = "estimate"):
     """GPU pyramids (DeviceCueImage levels) for large problems.  `factors`
-    are integer downscale factors coarsest first, e.g. (4, 2, 1)."""
+    are integer downscale factors coarsest first, e.g. (4, 2, 1).  With
+    normals="estimate" (default) the rendered intensity/depth go through the
+    device pyramid builder (pyramid_device.py: plane-fit normals + the
+    reference downscale, as build_pyramid does, cues.py:342-375); "analytic"
+    uses the renderer's exact surface normals instead."""
     rows = sensor_rows(platform_poses, ext).to(device)
     rays = unit_rays(cam, device)
     scales = tuple(1.0 / f for f in factors)
     pyrs = []
     for s0 in range(0, rows.shape[0], batch):
-        inten, depth, normals = render_batch(scene, cam, rows[s0:s0 + batch], rays)
+        inten, depth, nrm_true = render_batch(scene, cam, rows[s0:s0 + batch], rays)
+        if normals == "estimate":
+            from .pyramid_device import build_pyramids_device
+            pyrs.extend(build_pyramids_device(inten, depth, cam, scales, device=device))
+            continue
         per_level = []
         for f in factors:
             lc = cam.scaled(1.0 / f)
             if f == 1:
                 li, ld = inten, depth
-                nrm = torch.linalg.norm(normals, dim=-1, keepdim=True)
-                ln = torch.where(nrm > 0.5, normals / nrm.clamp(min=1e-300), torch.zeros_like(normals))
+                nrm = torch.linalg.norm(nrm_true, dim=-1, keepdim=True)
+                ln = torch.where(nrm > 0.5, nrm_true / nrm.clamp(min=1e-300),
+                                 torch.zeros_like(nrm_true))
             else:
-                li, ld, ln = downscale_block(inten, depth, normals, cam, f)
+                li, ld, ln = downscale_block(inten, depth, nrm_true, cam, f)
             per_level.append((lc, li, ld, ln))
         for b in range(inten.shape[0]):
             levels = tuple(DeviceCueImage(li[b].contiguous(), ld[b].contiguous(),
