@@ -83,7 +83,11 @@ typedef struct pba_camera {
 
 /* One (frame, level) image resident in HBM. */
 typedef struct pba_frame {
-  const void* texels;      /* device: width*height texels, pba_texel_bytes() each */
+  const void* texels;      /* device: texel planes, width*height*pba_texel_bytes() bytes:
+                            * 8 planes of 16-byte pairs, pair k of pixel p at
+                            * byte 16*(k*width*height + p); pairs: (I, D), (nx, ny),
+                            * (nz, mask u32 | pad), (dI/dcol, dI/drow), (dD/..),
+                            * (dnx/..), (dny/..), (dnz/..) */
   const uint8_t* mask;     /* device: width*height mask bytes (PBA_MASK_*) */
   const double* ray_table; /* device: per-column/row unprojection table, see pba_ray_table_doubles() */
   pba_camera cam;

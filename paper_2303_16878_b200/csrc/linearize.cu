@@ -147,13 +147,14 @@ struct PairSetup {
   double to[3];
   double cpb[3];   // R_o^T (R_j^T (t_i - t_j) - t_o): p_bar = M_i p_u + cpb
   double occ_tol;
-  const Texel* src_tex;
+  const double2* src_tex;  // texel planes (pba_common.cuh): pair k of pixel p at [k * src_np + p]
   const uint8_t* src_mask;
   const double* src_ray;
-  const Texel* dst_tex;
+  const double2* dst_tex;
   const uint8_t* dst_mask;
   pba_camera src_cam, dst_cam;
   int grid_w, n_px, stride;
+  int src_np, dst_np;  // pixels per texel plane
 };
 
 __device__ __forceinline__ void matmul3(const double* A, const double* B, double* C) {
@@ -200,10 +201,12 @@ __device__ void build_setup(PairSetup& S, const pba_frame* frames, const pba_pai
   S.occ_tol = P.occ_tol;
   const pba_frame& fs = frames[P.src];
   const pba_frame& fd = frames[P.dst];
-  S.src_tex = static_cast<const Texel*>(fs.texels);
+  S.src_tex = static_cast<const double2*>(fs.texels);
+  S.src_np = fs.cam.width * fs.cam.height;
+  S.dst_np = fd.cam.width * fd.cam.height;
   S.src_mask = fs.mask;
   S.src_ray = fs.ray_table;
-  S.dst_tex = static_cast<const Texel*>(fd.texels);
+  S.dst_tex = static_cast<const double2*>(fd.texels);
   S.dst_mask = fd.mask;
   S.src_cam = fs.cam;
   S.dst_cam = fd.cam;
@@ -300,6 +303,21 @@ __device__ __forceinline__ void accumulate_channel(double* Q, double* beta, doub
     for (int l = k; l < 6; ++l) Q[upper_idx(k, l)] = fma(a[k], q[l], Q[upper_idx(k, l)]);
 }
 
+// ablation (diagnostics only): fold the channel into 7 sums instead of 27
+__device__ __forceinline__ void accumulate_cheap(double* Q, double* beta, double2 g,
+                                                 const double* MP0, const double* MP1,
+                                                 double ww, double ec) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) Q[k] = fma(ww, g.x * MP0[k] + g.y * MP1[k], Q[k]);
+  beta[0] = fma(ww, ec, beta[0]);
+}
+
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
+// kProbe: 0 normal; 1 diagnostics (fixed destination texel); 5 / 6 source
+// texel prefetched into L1 one / two pixels ahead instead of into registers.
 template <bool kJac, int kT, int kMinBlocks, int kProbe = 0>
 __global__ void __launch_bounds__(kT, kMinBlocks)
     linearize_kernel(const pba_frame* __restrict__ frames, const pba_pair* __restrict__ pairs,
@@ -341,33 +359,62 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
   // ahead: (I, D) and (nz, mask) words, 2 x 16 B.  Masks come from the texel
   // lines themselves, so a pixel costs two dependent L2 round trips (source
   // texel, destination texels) instead of four.
+  // kProbe 5 / 6: the next (5) or next-but-one (6) pixel's source texel
+  // is prefetched into L1 instead of registers, and the current one is
+  // loaded at the top of the iteration.
+  constexpr bool kL1Src = kProbe == 5 || kProbe == 6;
   double2 nx0 = make_double2(0.0, 0.0), nx2 = make_double2(0.0, 0.0);
   if (first + (int)threadIdx.x < last) {
-    const double2* t = reinterpret_cast<const double2*>(S.src_tex + gr * stride * sW + gcol * stride);
-    nx0 = __ldg(t);
-    nx2 = __ldg(t + 2);
+    const double2* t = S.src_tex + gr * stride * sW + gcol * stride;
+    if (kL1Src) {
+      prefetch_l1(t), prefetch_l1(t + kPairNzM * S.src_np);
+    } else {
+      nx0 = __ldg(t);
+      nx2 = __ldg(t + kPairNzM * S.src_np);
+    }
   }
   int ngr = gr, ngcol = gcol;
+  int pgr = gr, pgcol = gcol;  // kProbe 6: pixel two iterations ahead
+  if (kProbe == 6) {
+    advance_pixel(pgr, pgcol, gw, kT);
+    if (first + (int)threadIdx.x + kT < last)
+    if (first + (int)threadIdx.x + kT < last) {
+      const double2* t = S.src_tex + pgr * stride * sW + pgcol * stride;
+      prefetch_l1(t), prefetch_l1(t + kPairNzM * S.src_np);
+    }
+  }
   for (int idx = first + (int)threadIdx.x; idx < last; idx += kT, gr = ngr, gcol = ngcol) {
     const int row = gr * stride;
     const int col = gcol * stride;
     const int sp = row * sW + col;
+    if (kL1Src) {
+      nx0 = __ldg(S.src_tex + sp);
+      nx2 = __ldg(S.src_tex + kPairNzM * S.src_np + sp);
+    }
     const double2 s_id = nx0;  // I, D
     const uint32_t sm = mask_word(nx2);
     const double mask_src_nz = nx2.x;
     ngr = gr;
     ngcol = gcol;
     advance_pixel(ngr, ngcol, gw, kT);
-    if (idx + kT < last) {
-      const double2* t =
-          reinterpret_cast<const double2*>(S.src_tex + ngr * stride * sW + ngcol * stride);
-      nx0 = __ldg(t);
-      nx2 = __ldg(t + 2);
+    if (kProbe == 6) {
+      advance_pixel(pgr, pgcol, gw, kT);
+      if (idx + 2 * kT < last) {
+        const double2* t = S.src_tex + pgr * stride * sW + pgcol * stride;
+        prefetch_l1(t), prefetch_l1(t + kPairNzM * S.src_np);
+      }
+    } else if (idx + kT < last) {
+      const double2* t = S.src_tex + ngr * stride * sW + ngcol * stride;
+      if (kL1Src) {
+        prefetch_l1(t), prefetch_l1(t + kPairNzM * S.src_np);
+      } else {
+        nx0 = __ldg(t);
+        nx2 = __ldg(t + kPairNzM * S.src_np);
+      }
     }
     if (!(sm & PBA_MASK_DEPTH_VALID)) continue;  // PairContext.build: usable = depth_valid
 
     // ---- source cue values and unprojection (sensors.py:133-154) ----
-    const double2* st = reinterpret_cast<const double2*>(S.src_tex + sp);
     const double d = s_id.y;
     double ps[3];
     if (src_sph) {
@@ -448,17 +495,23 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     const double wx = u - x0, wy = v - y0;
     // kProbe 1 (diagnostics only): every sample reads the same texel block
     const int dp = kProbe == 1 ? (dH / 2) * dW + dW / 2 : y0 * dW + x0;
-    const Texel* t00 = S.dst_tex + dp;
-    const Texel* t10 = t00 + dW;
+    const int dnp = S.dst_np;
+    const double2* t00 = S.dst_tex + dp;  // pair k of corner (r, c): t00[k * dnp + r * dW + c]
+    const double2* t10 = t00 + dW;
     // (I, D) and (nz, mask) of the four corners in one round trip
-    const double2 a00 = __ldg(reinterpret_cast<const double2*>(t00));
-    const double2 a01 = __ldg(reinterpret_cast<const double2*>(t00 + 1));
-    const double2 a10 = __ldg(reinterpret_cast<const double2*>(t10));
-    const double2 a11 = __ldg(reinterpret_cast<const double2*>(t10 + 1));
-    const double2 m00 = __ldg(reinterpret_cast<const double2*>(t00) + 2);
-    const double2 m01 = __ldg(reinterpret_cast<const double2*>(t00 + 1) + 2);
-    const double2 m10 = __ldg(reinterpret_cast<const double2*>(t10) + 2);
-    const double2 m11 = __ldg(reinterpret_cast<const double2*>(t10 + 1) + 2);
+    const double2 a00 = __ldg(t00), a01 = __ldg(t00 + 1), a10 = __ldg(t10), a11 = __ldg(t10 + 1);
+    const double2 m00 = __ldg(t00 + kPairNzM * dnp), m01 = __ldg(t00 + kPairNzM * dnp + 1);
+    const double2 m10 = __ldg(t10 + kPairNzM * dnp), m11 = __ldg(t10 + kPairNzM * dnp + 1);
+    if (kJac && kProbe == 7) {  // the remaining planes of the footprint, into L1 now
+      prefetch_l1(t00 + kPairGI * dnp), prefetch_l1(t10 + kPairGI * dnp);
+      prefetch_l1(t00 + kPairGD * dnp), prefetch_l1(t10 + kPairGD * dnp);
+      if (sm & PBA_MASK_NORMAL_VALID) {
+        prefetch_l1(t00 + kPairNxy * dnp), prefetch_l1(t10 + kPairNxy * dnp);
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+          prefetch_l1(t00 + (kPairGN + k) * dnp), prefetch_l1(t10 + (kPairGN + k) * dnp);
+      }
+    }
     const uint32_t mk = mask_word(m00) & mask_word(m01) & mask_word(m10) & mask_word(m11);
     if (!(mk & PBA_MASK_SAMP_CORE)) continue;  // core_ok
     const double Dd = bil(a00.y, a01.y, a10.y, a11.y, wx, wy);
@@ -477,12 +530,10 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     double e2 = 0.0, e3 = 0.0, e4 = 0.0;
     double no[3] = {0.0, 0.0, 0.0};  // R_o n_src
     if (normal_on) {
-      const double2 s_n01 = __ldg(st + 1);  // source nx, ny (same line: L1 hit)
+      const double2 s_n01 = __ldg(S.src_tex + kPairNxy * S.src_np + sp);  // source nx, ny
       const double ns2 = mask_src_nz;
-      const double2 b00 = __ldg(reinterpret_cast<const double2*>(t00) + 1);
-      const double2 b01 = __ldg(reinterpret_cast<const double2*>(t00 + 1) + 1);
-      const double2 b10 = __ldg(reinterpret_cast<const double2*>(t10) + 1);
-      const double2 b11 = __ldg(reinterpret_cast<const double2*>(t10 + 1) + 1);
+      const double2 b00 = __ldg(t00 + kPairNxy * dnp), b01 = __ldg(t00 + kPairNxy * dnp + 1);
+      const double2 b10 = __ldg(t10 + kPairNxy * dnp), b11 = __ldg(t10 + kPairNxy * dnp + 1);
       // rot_n n_src (solver.py:241-248)
       const double m0 = s_n01.x * S.rotn[0] + s_n01.y * S.rotn[1] + ns2 * S.rotn[2];
       const double m1 = s_n01.x * S.rotn[3] + s_n01.y * S.rotn[4] + ns2 * S.rotn[5];
@@ -544,33 +595,48 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     // the gradient images are interpolated, not differentiated (cues.py:448-450).
     const double w00 = (1.0 - wx) * (1.0 - wy), w01 = wx * (1.0 - wy);
     const double w10 = (1.0 - wx) * wy, w11 = wx * wy;
-    const double2* g00p = reinterpret_cast<const double2*>(t00->g);
-    const double2* g01p = reinterpret_cast<const double2*>(t00[1].g);
-    const double2* g10p = reinterpret_cast<const double2*>(t10->g);
-    const double2* g11p = reinterpret_cast<const double2*>(t10[1].g);
+    const double2* g00p = t00 + kPairGI * dnp;  // gradient pair k at g..p + k * dnp
+    const double2* g01p = g00p + 1;
+    const double2* g10p = g00p + dW;
+    const double2* g11p = g10p + 1;
     double2 gI, gD;
-    {
+    if (kProbe == 10) {  // ablation (diagnostics only): no gradient loads
+      gI = make_double2(a00.x * w00, a01.x * w01);
+      gD = make_double2(a10.y * w10, a11.y * w11);
+    } else {
       const double2 i00 = __ldg(g00p), i01 = __ldg(g01p), i10 = __ldg(g10p), i11 = __ldg(g11p);
-      const double2 d00 = __ldg(g00p + 1), d01 = __ldg(g01p + 1), d10 = __ldg(g10p + 1),
-                    d11 = __ldg(g11p + 1);
+      const double2 d00 = __ldg(g00p + dnp), d01 = __ldg(g01p + dnp), d10 = __ldg(g10p + dnp),
+                    d11 = __ldg(g11p + dnp);
       gI = bil4(i00, i01, i10, i11, w00, w01, w10, w11);
       gD = bil4(d00, d01, d10, d11, w00, w01, w10, w11);
     }
-    accumulate_channel(Q, beta, gI, MP0, MP1, nullptr, pu, nullptr, wI, e0);
-    accumulate_channel(Q, beta, gD, MP0, MP1, ud, pu, nullptr, wD, e1);
+    double* QA = Q;
+    double* bA = beta;
+    if (kProbe == 11) {
+      accumulate_cheap(QA, bA, gI, MP0, MP1, wI, e0);
+      accumulate_cheap(QA, bA, gD, MP0, MP1, wD, e1);
+      if (normal_on) {
+        accumulate_cheap(QA, bA, make_double2(no[0], no[1]), MP0, MP1, wN, e2 + e3 + e4);
+      }
+      continue;
+    }
+    accumulate_channel(QA, bA, gI, MP0, MP1, nullptr, pu, nullptr, wI, e0);
+    accumulate_channel(QA, bA, gD, MP0, MP1, ud, pu, nullptr, wD, e1);
     if (normal_on) {
       double2 gN[3];
 #pragma unroll
       for (int k = 0; k < 3; ++k)
-        gN[k] = bil4(__ldg(g00p + 2 + k), __ldg(g01p + 2 + k), __ldg(g10p + 2 + k),
-                     __ldg(g11p + 2 + k), w00, w01, w10, w11);
+        gN[k] = kProbe == 10 ? make_double2(gI.x * (k + 1), gD.y * k)
+                             : bil4(__ldg(g00p + (2 + k) * dnp), __ldg(g01p + (2 + k) * dnp),
+                                    __ldg(g10p + (2 + k) * dnp), __ldg(g11p + (2 + k) * dnp), w00,
+                                    w01, w10, w11);
       double xn[3];
       cross3(&S.Mi[0], no, xn);
-      accumulate_channel(Q, beta, gN[0], MP0, MP1, nullptr, pu, xn, wN * cfg.omega[2], e2);
+      accumulate_channel(QA, bA, gN[0], MP0, MP1, nullptr, pu, xn, wN * cfg.omega[2], e2);
       cross3(&S.Mi[3], no, xn);
-      accumulate_channel(Q, beta, gN[1], MP0, MP1, nullptr, pu, xn, wN * cfg.omega[3], e3);
+      accumulate_channel(QA, bA, gN[1], MP0, MP1, nullptr, pu, xn, wN * cfg.omega[3], e3);
       cross3(&S.Mi[6], no, xn);
-      accumulate_channel(Q, beta, gN[2], MP0, MP1, nullptr, pu, xn, wN * cfg.omega[4], e4);
+      accumulate_channel(QA, bA, gN[2], MP0, MP1, nullptr, pu, xn, wN * cfg.omega[4], e4);
     }
   }
 
@@ -759,12 +825,14 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
     // CTA-size / occupancy variant (PBA_LIN_VARIANT overrides):
     //   1: 256 thr, <=255 regs (8 warps/SM)    2: 256 thr, 128 regs (16 warps/SM)
     //   3: 128 thr, 128 regs (16 warps/SM)     4: 128 thr, 168 regs (12 warps/SM)
-    //   5: 512 thr, 128 regs (16 warps/SM)
+    //   5: 512 thr, 128 regs (16 warps/SM)   13 / 14: 32 / 64 thr, 12 warps/SM
+    //  15 / 16: variant 4 with the source texel prefetched into L1 1 / 2 ahead
+    //   9: diagnostics (fixed destination texel)
     static int variant = -1;
     if (variant < 0) {
       const char* env = getenv("PBA_LIN_VARIANT");
       variant = env ? atoi(env) : 4;
-      if (variant < 1 || variant > 9) variant = 4;
+      if (variant < 1 || variant > 21) variant = 4;
     }
     const unsigned grid = (unsigned)n_chunks;
 #define PBA_LAUNCH_LIN(J, T, M) \
@@ -775,6 +843,33 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
         case 3: PBA_LAUNCH_LIN(true, 128, 4); break;
         case 5: PBA_LAUNCH_LIN(true, 512, 1); break;
         case 2: PBA_LAUNCH_LIN(true, 256, 2); break;
+        case 13: PBA_LAUNCH_LIN(true, 32, 12); break;
+        case 15:
+          linearize_kernel<true, 128, 3, 5><<<grid, 128, 0, st>>>(frames, pairs, chunk_table,
+                                                                chunk_pixels, poses, extrinsics,
+                                                                *cfg, partials);
+          break;
+        case 16:
+          linearize_kernel<true, 128, 3, 6><<<grid, 128, 0, st>>>(frames, pairs, chunk_table,
+                                                                chunk_pixels, poses, extrinsics,
+                                                                *cfg, partials);
+          break;
+        case 14: PBA_LAUNCH_LIN(true, 64, 6); break;
+        case 20:
+          linearize_kernel<true, 128, 3, 10><<<grid, 128, 0, st>>>(frames, pairs, chunk_table,
+                                                                 chunk_pixels, poses, extrinsics,
+                                                                 *cfg, partials);
+          break;
+        case 21:
+          linearize_kernel<true, 128, 3, 11><<<grid, 128, 0, st>>>(frames, pairs, chunk_table,
+                                                                 chunk_pixels, poses, extrinsics,
+                                                                 *cfg, partials);
+          break;
+        case 17:
+          linearize_kernel<true, 128, 3, 7><<<grid, 128, 0, st>>>(frames, pairs, chunk_table,
+                                                                chunk_pixels, poses, extrinsics,
+                                                                *cfg, partials);
+          break;
         case 9:  // diagnostics: destination gather replaced by a fixed texel
           linearize_kernel<true, 128, 3, 1><<<grid, 128, 0, st>>>(frames, pairs, chunk_table,
                                                                 chunk_pixels, poses, extrinsics,

@@ -10,21 +10,25 @@ namespace pba {
 
 constexpr int kRec = PBA_RECORD_DOUBLES;
 
-// One (frame, level) pixel as the linearisation kernel reads it: the five
-// cue values and their ten central-difference gradients in fp64 plus the
-// validity bits, 128 B = one L2 line, so the four bilinear corners of a
-// destination sample are four aligned lines.  Field order follows the
-// reference channels [intensity, depth, nx, ny, nz] (solver.py:340) and the
-// gradient order [d/dcol, d/drow] (cues.py:63-71); every (col,row) gradient
-// pair and the (I,D), (nx,ny) value pairs sit on 16-byte boundaries so they
-// load as one 128-bit access.
-struct __align__(16) Texel {
-  double v[5];   // I, D, nx, ny, nz                                   0..39
-  uint32_t mask; // PBA_MASK_*                                         40
-  uint32_t pad;  //                                                    44
-  double g[10];  // gI(c,r), gD(c,r), gnx(c,r), gny(c,r), gnz(c,r)   48..127
+// One (frame, level) image as the linearisation kernel reads it: eight
+// planes of 16-byte pairs (128 B per pixel in total), plane-major, so the
+// 32 lanes of a warp reading the same pair of 32 neighbouring pixels touch
+// 4-5 consecutive 128-byte lines (L1 wavefronts) instead of 32 — with a
+// 128-byte per-pixel record every gather lane was its own wavefront and the
+// L1 data pipe was the bottleneck.  Pair k of pixel p is at
+// base[k * W * H + p].  Field order follows the reference channels
+// [intensity, depth, nx, ny, nz] (solver.py:340) and the gradient order
+// [d/dcol, d/drow] (cues.py:63-71).
+enum TexelPair : int {
+  kPairID = 0,    // I, D
+  kPairNxy = 1,   // nx, ny
+  kPairNzM = 2,   // nz, (mask u32, pad u32) — mask in the low word of .y
+  kPairGI = 3,    // dI/dcol, dI/drow
+  kPairGD = 4,    // dD/dcol, dD/drow
+  kPairGN = 5,    // 5, 6, 7: d(nx,ny,nz)/dcol, /drow
+  kTexelPairs = 8
 };
-static_assert(sizeof(Texel) == 128, "texel must be one 128-byte line");
+constexpr int kTexelBytes = 16 * kTexelPairs;
 
 // Thread-local error message for pba_last_error().
 void set_error(const char* fmt, ...);

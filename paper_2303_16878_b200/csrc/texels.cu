@@ -68,18 +68,13 @@ __global__ void coherence_pass(int H, int W, const double* __restrict__ n,
 
 __global__ void gradient_pass(int H, int W, const double* __restrict__ inten,
                               const double* __restrict__ d, const double* __restrict__ n,
-                              const uint8_t* __restrict__ flags, Texel* __restrict__ out,
+                              const uint8_t* __restrict__ flags, double2* __restrict__ out,
                               uint8_t* __restrict__ mask_out) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= H * W) return;
   const int r = p / W, c = p - r * W;
   const uint8_t f = flags[p];
-  Texel t;
-  t.v[0] = inten[p];
-  t.v[1] = d[p];
-  t.v[2] = n[3 * p + 0];
-  t.v[3] = n[3 * p + 1];
-  t.v[4] = n[3 * p + 2];
+  double g[10];
   bool core_ok = false, norm_ok = false;
   const bool interior = r > 0 && r < H - 1 && c > 0 && c < W - 1;
   if (interior) {
@@ -89,27 +84,30 @@ __global__ void gradient_pass(int H, int W, const double* __restrict__ inten,
   }
   // cues.py:70-71: 0.5 * (right - left), 0.5 * (down - up); zero where invalid (:80).
   if (core_ok) {
-    t.g[0] = __dmul_rn(0.5, __dsub_rn(inten[p + 1], inten[p - 1]));
-    t.g[1] = __dmul_rn(0.5, __dsub_rn(inten[p + W], inten[p - W]));
-    t.g[2] = __dmul_rn(0.5, __dsub_rn(d[p + 1], d[p - 1]));
-    t.g[3] = __dmul_rn(0.5, __dsub_rn(d[p + W], d[p - W]));
+    g[0] = __dmul_rn(0.5, __dsub_rn(inten[p + 1], inten[p - 1]));
+    g[1] = __dmul_rn(0.5, __dsub_rn(inten[p + W], inten[p - W]));
+    g[2] = __dmul_rn(0.5, __dsub_rn(d[p + 1], d[p - 1]));
+    g[3] = __dmul_rn(0.5, __dsub_rn(d[p + W], d[p - W]));
   } else {
-    t.g[0] = t.g[1] = t.g[2] = t.g[3] = 0.0;
+    g[0] = g[1] = g[2] = g[3] = 0.0;
   }
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     if (norm_ok) {
-      t.g[4 + 2 * k] = __dmul_rn(0.5, __dsub_rn(n[3 * (p + 1) + k], n[3 * (p - 1) + k]));
-      t.g[5 + 2 * k] = __dmul_rn(0.5, __dsub_rn(n[3 * (p + W) + k], n[3 * (p - W) + k]));
+      g[4 + 2 * k] = __dmul_rn(0.5, __dsub_rn(n[3 * (p + 1) + k], n[3 * (p - 1) + k]));
+      g[5 + 2 * k] = __dmul_rn(0.5, __dsub_rn(n[3 * (p + W) + k], n[3 * (p - W) + k]));
     } else {
-      t.g[4 + 2 * k] = t.g[5 + 2 * k] = 0.0;
+      g[4 + 2 * k] = g[5 + 2 * k] = 0.0;
     }
   }
   const uint32_t m = (f & (kDV | kNV)) | (core_ok ? PBA_MASK_SAMP_CORE : 0u) |
                      (norm_ok ? PBA_MASK_SAMP_NORMAL : 0u);
-  t.mask = m;
-  t.pad = 0;
-  out[p] = t;
+  const int64_t np = (int64_t)H * W;
+  out[kPairID * np + p] = make_double2(inten[p], d[p]);
+  out[kPairNxy * np + p] = make_double2(n[3 * p + 0], n[3 * p + 1]);
+  out[kPairNzM * np + p] = make_double2(n[3 * p + 2], __longlong_as_double((long long)m));
+#pragma unroll
+  for (int k = 0; k < 5; ++k) out[(kPairGI + k) * np + p] = make_double2(g[2 * k], g[2 * k + 1]);
   mask_out[p] = (uint8_t)m;
 }
 
@@ -121,7 +119,7 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 using namespace pba;
 
-extern "C" size_t pba_texel_bytes(void) { return sizeof(Texel); }
+extern "C" size_t pba_texel_bytes(void) { return kTexelBytes; }
 
 extern "C" size_t pba_ray_table_doubles(const pba_camera* cam) {
   if (!cam) return 0;
@@ -158,7 +156,7 @@ extern "C" int pba_build_texels(const pba_camera* cam, const double* intensity,
   coherence_pass<<<blocks, threads, 0, st>>>(H, W, n_clean, flags);
   PBA_LAUNCH_CHECK();
   gradient_pass<<<blocks, threads, 0, st>>>(H, W, intensity, d_clean, n_clean, flags,
-                                             static_cast<Texel*>(texels), mask);
+                                             static_cast<double2*>(texels), mask);
   PBA_LAUNCH_CHECK();
   return PBA_OK;
 }

@@ -1,7 +1,7 @@
 """GPU-resident state of the BA hot path and the calls into libpba_b200.
 
 `FrameStore` keeps every (frame, level) cue image resident in HBM as the
-128-byte texel layout plus a mask plane (built on the device from the
+texel-plane layout (8 planes of 16-byte pairs) plus a mask plane (built on the device from the
 reference CueImage channels, csrc/texels.cu).  `DeviceLevel` is the
 device replacement of the reference `_LevelProblem` (solver.py:393-460):
 pair table, chunk plan, assembly plan, and the buffers of one LM level, with
@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 
 import numpy as np
 import torch
@@ -48,7 +49,8 @@ def chunk_pixels_for(total_pixels: int) -> int:
     CTAs for ~4 waves of 148 SMs, at most 32 pixels per thread."""
     ppt = total_pixels // (THREADS_PER_CHUNK * SM_COUNT * 4)
     ppt = max(1, min(32, int(ppt)))
-    return THREADS_PER_CHUNK * ppt
+    div = int(os.environ.get("PBA_CHUNK_DIV", "1"))  # experiments only
+    return max(32, THREADS_PER_CHUNK * ppt // div)
 
 
 def tile_envelope(slot_of_pose, pose_i, pose_j, dim, tile=64) -> np.ndarray:

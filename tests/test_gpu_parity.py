@@ -54,13 +54,17 @@ def test_device_texels_bit_exact_masks_and_gradients(name):
             torch.cuda.synchronize()
             m = mask.cpu().numpy().reshape(img.shape)
             assert np.array_equal(m, d[f"M_{f}_{l}"])
-            t = tex.cpu().numpy().view(np.float64).reshape(img.shape[0], img.shape[1], 16)
-            assert np.array_equal(t[..., 0], img.intensity)
-            assert np.array_equal(t[..., 1], img.depth)
-            assert np.array_equal(t[..., 2:5], img.normals)
+            # eight planes of (h, w) 16-byte pairs, see include/pba.h
+            t = tex.cpu().numpy().view(np.float64).reshape(8, img.shape[0], img.shape[1], 2)
+            assert np.array_equal(t[0, ..., 0], img.intensity)
+            assert np.array_equal(t[0, ..., 1], img.depth)
+            assert np.array_equal(np.stack([t[1, ..., 0], t[1, ..., 1], t[2, ..., 0]], -1),
+                                  img.normals)
+            words = t[2, ..., 1].view(np.uint64) & 0xFFFFFFFF
+            assert np.array_equal(words, m.astype(np.uint64))
             if f == 0:
-                g = np.concatenate([t[..., 6:8].reshape(-1), t[..., 8:10].reshape(-1),
-                                    t[..., 10:16].reshape(-1)])
+                g = np.concatenate([t[3].reshape(-1), t[4].reshape(-1),
+                                    np.stack([t[5], t[6], t[7]], axis=2).reshape(-1)])
                 assert np.array_equal(g, d[f"G_{f}_{l}"])
 
 

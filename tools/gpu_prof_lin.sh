@@ -1,3 +1,3 @@
 CMD2="python bench.py --config c4 --frames 200 --steps 2 --warmup 3 --no-cpu-baseline"
 timeout 600 $CMD2 > gpurun_out/plain_small.log 2>&1 && \
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:linearize_kernel -s 3 -c 1 -o gpurun_out/prof_linearize -f $CMD2 > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:linearize_kernel -s 3 -c 1 -o gpurun_out/prof_linearize_v4 -f $CMD2 > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
