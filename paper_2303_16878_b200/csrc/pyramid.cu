@@ -88,29 +88,38 @@ __global__ void __launch_bounds__(128, 4) moment_colscan_kernel(pba_camera cam,
   }
 }
 
-// Row-wise running sums in place (np.cumsum(..., axis=1)); one thread per
-// (frame, moment, row), sequential along the row.
-__global__ void __launch_bounds__(128) moment_rowscan_kernel(int H, int W, int64_t n_rows,
+// Row-wise running sums in place (np.cumsum(..., axis=1)).  A CTA owns 32
+// consecutive rows of the (frame, moment, row) row list and walks them in
+// 32-column tiles staged through shared memory: coalesced tile loads and
+// stores, and one thread per row carrying the sequential sum across tiles
+// (the summation order of cumsum, so results are bit-equal).
+__global__ void __launch_bounds__(256) moment_rowscan_kernel(int W, int64_t n_rows,
                                                              double* __restrict__ sat) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n_rows) return;
-  double* p = sat + t * W;
-  double acc = p[0];
-  int c = 1;
-  for (; c + 4 <= W; c += 4) {
-    const double a0 = p[c], a1 = p[c + 1], a2 = p[c + 2], a3 = p[c + 3];
-    acc = __dadd_rn(acc, a0);
-    p[c] = acc;
-    acc = __dadd_rn(acc, a1);
-    p[c + 1] = acc;
-    acc = __dadd_rn(acc, a2);
-    p[c + 2] = acc;
-    acc = __dadd_rn(acc, a3);
-    p[c + 3] = acc;
-  }
-  for (; c < W; ++c) {
-    acc = __dadd_rn(acc, p[c]);
-    p[c] = acc;
+  __shared__ double tile[32][33];
+  const int64_t row0 = (int64_t)blockIdx.x * 32;
+  const int t = threadIdx.x;
+  double acc = 0.0;
+  for (int c0 = 0; c0 < W; c0 += 32) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int e = t + 256 * k, r = e >> 5, c = e & 31;
+      if (row0 + r < n_rows && c0 + c < W) tile[r][c] = sat[(row0 + r) * W + c0 + c];
+    }
+    __syncthreads();
+    if (t < 32) {
+      const int n = min(32, W - c0);
+      for (int c = 0; c < n; ++c) {
+        acc = (c0 == 0 && c == 0) ? tile[t][0] : __dadd_rn(acc, tile[t][c]);
+        tile[t][c] = acc;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int e = t + 256 * k, r = e >> 5, c = e & 31;
+      if (row0 + r < n_rows && c0 + c < W) sat[(row0 + r) * W + c0 + c] = tile[r][c];
+    }
+    __syncthreads();
   }
 }
 
@@ -335,7 +344,7 @@ extern "C" int pba_estimate_normals(const pba_camera* cam, const double* ray_tab
                                                                          sat);
   PBA_LAUNCH_CHECK();
   const int64_t rows = (int64_t)n_frames * kMoments * H;
-  moment_rowscan_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, st>>>(H, W, rows, sat);
+  moment_rowscan_kernel<<<(unsigned)((rows + 31) / 32), 256, 0, st>>>(W, rows, sat);
   PBA_LAUNCH_CHECK();
   const int64_t plane = (int64_t)H * W;
   normals_kernel<<<dim3((unsigned)((plane + 127) / 128), n_frames), 128, 0, st>>>(

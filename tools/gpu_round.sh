@@ -1,4 +1,4 @@
-# full round on one B200: GPU tests, smoke, default bench, ncu launch list (small) + one full capture
+# full round on one B200: GPU tests, smoke, default bench, reference arm, ncu launch lists + one full capture
 set -x
 python -c "from oracle import oracle; oracle.build(force=True)"
 timeout 900 python -m pytest tests -m gpu -q --tb=short > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
@@ -6,8 +6,11 @@ tail -3 gpurun_out/pytest_gpu.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/smoke.log
 timeout 1200 python bench.py > gpurun_out/bench_default.log 2>&1; echo "bench rc=$?"
 tail -1 gpurun_out/bench_default.log
+timeout 900 python bench.py --impl reference > gpurun_out/bench_reference.log 2>&1; echo "bench ref rc=$?"
+tail -1 gpurun_out/bench_reference.log
+CMD1="python bench.py --no-cpu-baseline"
+timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c4.csv $CMD1 > gpurun_out/ncu_launches_c4.log 2>&1; echo "ncu launches c4 rc=$?"
 CMD2="python bench.py --config c4 --frames 200 --steps 2 --warmup 3 --no-cpu-baseline"
 timeout 600 $CMD2 > gpurun_out/plain_small.log 2>&1 && \
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD2 > gpurun_out/ncu_launches.log 2>&1; echo "ncu launches rc=$?"
-timeout 600 $CMD2 > gpurun_out/plain_small2.log 2>&1 && \
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:linearize_kernel -s 3 -c 1 -o gpurun_out/prof_linearize -f $CMD2 > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
