@@ -246,6 +246,17 @@ int pba_downscale_cues(const pba_camera* cam, double scale, int32_t n_frames,
                        int32_t out_h, int32_t out_w, double* out_intensity, double* out_depth,
                        double* out_normals, void* stream);
 
+/* ---- dataset rasters: read_intensity / read_depth (dataset_io.py:74-136) --
+ * raw: device bytes of PGM P5 payloads (headers stripped by the host),
+ * frames back to back; n_samples pixels.  16-bit samples are big-endian.
+ * Intensity: raw / 65535 (8-bit: raw / 255); depth: raw * depth_scale
+ * (raw 0 = invalid -> 0.0).  out: n_samples doubles (device). */
+#define PBA_RASTER_U8_INTENSITY 0
+#define PBA_RASTER_U16_INTENSITY 1
+#define PBA_RASTER_U16_DEPTH 2
+int pba_decode_raster(const uint8_t* raw, int64_t n_samples, int32_t kind, double depth_scale,
+                      double* out, void* stream);
+
 /* ---- diagnostics ------------------------------------------------------
  * The table-corrected fp64 atan2 the spherical projection uses
  * (csrc/fastmath.cuh), exposed so tests can bound its error against the

@@ -15,6 +15,12 @@ from .camera import (PINHOLE, SPHERICAL, Intrinsics, SensorExtrinsics, project,
 from .cueimage import (CueImage, CuePyramid, DeviceCueImage, NormalConfig, PyramidConfigError,
                        build_cue_image, build_pyramid, estimate_normals, footprint_index)
 from .pyramid_device import build_pyramids_device, estimate_normals_device
+from .dataset import (DatasetError, DatasetManifest, DimensionMismatchError, ManifestError,
+                      MissingFileError, SensorConfig, Trajectory, TrajectoryFormatError,
+                      load_dataset, load_manifest, load_trajectory, read_depth, read_intensity,
+                      read_raster, save_manifest, save_trajectory, timestamp_name,
+                      trajectory_from_poses, write_dataset, write_depth, write_intensity,
+                      write_raster)
 from .pairgraph import (COVISIBILITY, ODOMETRY, Edge, FrameNode, GraphConfigError, MatchCriteria,
                         MatchGraph, build_graph, dump_edges, overlap_ratio)
 from .bundle import (CONSECUTIVE, COUPLED, BAProblem, FusionConfigError, IterationRecord,
@@ -24,6 +30,11 @@ from .bundle import (CONSECUTIVE, COUPLED, BAProblem, FusionConfigError, Iterati
 __version__ = "0.1.0"
 
 __all__ = [
+    "DatasetError", "DatasetManifest", "DimensionMismatchError", "ManifestError",
+    "MissingFileError", "SensorConfig", "Trajectory", "TrajectoryFormatError", "load_dataset",
+    "load_manifest", "load_trajectory", "read_depth", "read_intensity", "read_raster",
+    "save_manifest", "save_trajectory", "timestamp_name", "trajectory_from_poses",
+    "write_dataset", "write_depth", "write_intensity", "write_raster",
     "BAProblem", "CONSECUTIVE", "COUPLED", "COVISIBILITY", "CueImage", "CuePyramid",
     "DeviceCueImage", "Edge", "FrameNode", "FusionConfigError", "GraphConfigError",
     "InvalidPerturbationError", "Intrinsics", "IterationRecord", "MatchCriteria", "MatchGraph",

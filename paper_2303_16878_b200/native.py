@@ -19,6 +19,9 @@ PBA_ERR_ARG = 1
 PBA_ERR_CUDA = 2
 PBA_ERR_SINGULAR = 3
 PBA_ERR_PERTURBATION = 4
+PBA_RASTER_U8_INTENSITY = 0
+PBA_RASTER_U16_INTENSITY = 1
+PBA_RASTER_U16_DEPTH = 2
 PBA_PINHOLE = 0
 PBA_SPHERICAL = 1
 RECORD_DOUBLES = 92
@@ -31,7 +34,7 @@ EXPORTED = (
     "pba_build_texels_scratch_bytes", "pba_build_texels", "pba_plan_chunks", "pba_linearize",
     "pba_plan_assembly", "pba_assemble", "pba_sum_totals", "pba_solve_work_bytes",
     "pba_solve_dense", "pba_apply_step", "pba_overlap_counts", "pba_normals_scratch_bytes",
-    "pba_estimate_normals", "pba_downscale_cues", "pba_atan2_batch",
+    "pba_estimate_normals", "pba_downscale_cues", "pba_decode_raster", "pba_atan2_batch",
 )
 
 
@@ -99,6 +102,7 @@ _SIGNATURES = {
                                             ctypes.POINTER(NormalConfigC), _vp, _vp, _vp]),
     "pba_downscale_cues": (ctypes.c_int, [ctypes.POINTER(Camera), _dbl, _i32, _vp, _vp, _vp,
                                           _i32, _i32, _vp, _vp, _vp, _vp]),
+    "pba_decode_raster": (ctypes.c_int, [_vp, _i64, _i32, _dbl, _vp, _vp]),
 }
 
 _lib = None

@@ -201,6 +201,44 @@ def pyramid_case():
     print("pyramid", (OUT / "pyramid.npz").stat().st_size, "bytes")
 
 
+def dataset_case():
+    """A two-sensor dataset directory written by the reference's
+    generate_synthetic (synthetic.py:257-310), stored file by file, plus the
+    reference load_dataset output (dataset_io.py:305-342)."""
+    import tempfile
+
+    from photoba.dataset_io import load_dataset
+    from photoba.evaluation import Trajectory
+    from photoba.synthetic import SyntheticSensor, generate_synthetic
+
+    traj = Trajectory(np.arange(3, dtype=float) * 0.1 + 0.05,
+                      [Pose(np.eye(3), [0.1 * k, 0.05 * k, -0.5]) for k in range(3)])
+    sensors = [SyntheticSensor("cam0", rgbd_cam(), SensorExtrinsics.identity(), 0.001),
+               SyntheticSensor("lidar0", lidar_cam(128, 32),
+                               SensorExtrinsics(Pose(np.eye(3), [0.0, 0.0, 0.1])), 0.002)]
+    d = {}
+    with tempfile.TemporaryDirectory() as tmp:
+        ds = generate_synthetic(box_room_scene(), traj, sensors, Path(tmp) / "ds",
+                                pyramid_scales=(0.25, 0.5, 1.0))
+        files = sorted(p for p in ds.rglob("*") if p.is_file())
+        d["files"] = np.array([str(p.relative_to(ds)) for p in files])
+        for k, p in enumerate(files):
+            d[f"file_{k}"] = np.frombuffer(p.read_bytes(), dtype=np.uint8)
+        _, guess, frames = load_dataset(ds)
+        d["guess"] = pose_rows(guess.poses)
+        d["stamps"] = guess.timestamps
+        for sid, nodes in frames.items():
+            for f, node in enumerate(nodes):
+                for l, img in enumerate(node.pyramid.levels):
+                    if f > 0 and l < len(node.pyramid.levels) - 1:
+                        continue  # all levels of frame 0, the finest of the others
+                    d[f"{sid}_I_{f}_{l}"] = img.intensity
+                    d[f"{sid}_D_{f}_{l}"] = img.depth
+                    d[f"{sid}_N_{f}_{l}"] = img.normals
+    np.savez_compressed(OUT / "dataset.npz", **d)
+    print("dataset", len(d["files"]), "files", (OUT / "dataset.npz").stat().st_size, "bytes")
+
+
 if __name__ == "__main__":
     pin = Intrinsics(40.0, 40.0, 32.0, 24.0, 64, 48, PINHOLE, 0.1, 50.0)
     single_sensor_case("pinhole_small", pin, 4, (1.0,), [0.0, 0.0, 0.1], 51, 0.04,
@@ -212,3 +250,4 @@ if __name__ == "__main__":
     fusion_case()
     footprint_case()
     pyramid_case()
+    dataset_case()

@@ -139,3 +139,49 @@ def test_device_empty_depth_gives_zero_normals():
     cam = Intrinsics(20.0, 20.0, 8.0, 6.0, 16, 12, P.PINHOLE, 0.1, 10.0)
     n = P.estimate_normals_device(np.full((12, 16), math.nan), cam)
     assert n.shape == (12, 16, 3) and not bool(n.any())
+
+
+def test_device_load_dataset_matches_reference(tmp_path):
+    from paper_2303_16878_b200 import dataset as DS
+    from tests.test_dataset import unpack
+
+    root, z = unpack(tmp_path)
+    _, guess, frames = DS.load_dataset(root, device="cuda")
+    np.testing.assert_array_equal(guess.timestamps, z["stamps"])
+    checked = 0
+    for sid, nodes in frames.items():
+        for f, node in enumerate(nodes):
+            for l, img in enumerate(node.pyramid.levels):
+                key = f"{sid}_I_{f}_{l}"
+                if key not in z.files:
+                    continue
+                assert isinstance(img, P.DeviceCueImage)
+                np.testing.assert_array_equal(img.device_intensity.cpu().numpy(), z[key])
+                np.testing.assert_array_equal(img.device_depth.cpu().numpy(), z[f"{sid}_D_{f}_{l}"])
+                n = img.device_normals.cpu().numpy()
+                ref = z[f"{sid}_N_{f}_{l}"]
+                assert np.array_equal(_valid(n), _valid(ref))
+                assert np.abs(n - ref).max() <= NORMAL_TOL
+                checked += 1
+    assert checked == 2 * (3 + 2)
+
+
+def test_device_raster_decode_kinds():
+    from paper_2303_16878_b200 import native as N
+
+    lib = N.load()
+    vals = np.array([0, 1, 255, 256, 4660, 65535], dtype=">u2")
+    raw = torch.from_numpy(np.frombuffer(vals.tobytes(), dtype=np.uint8).copy()).cuda()
+    out = torch.empty(6, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+    N.check(lib.pba_decode_raster(raw.data_ptr(), 6, N.PBA_RASTER_U16_DEPTH, 0.001,
+                                  out.data_ptr(), stream), "decode")
+    np.testing.assert_array_equal(out.cpu().numpy(), vals.astype(np.uint16).astype(float) * 0.001)
+    N.check(lib.pba_decode_raster(raw.data_ptr(), 6, N.PBA_RASTER_U16_INTENSITY, 0.0,
+                                  out.data_ptr(), stream), "decode")
+    np.testing.assert_array_equal(out.cpu().numpy(), vals.astype(np.uint16).astype(float) / 65535.0)
+    N.check(lib.pba_decode_raster(raw.data_ptr(), 6, N.PBA_RASTER_U8_INTENSITY, 0.0,
+                                  out.data_ptr(), stream), "decode")
+    b = raw.cpu().numpy()[:6].astype(float) / 255.0
+    np.testing.assert_array_equal(out.cpu().numpy(), b)
+    assert lib.pba_decode_raster(raw.data_ptr(), 6, 7, 0.0, out.data_ptr(), stream) != 0
