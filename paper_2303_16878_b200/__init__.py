@@ -15,6 +15,8 @@ from .camera import (PINHOLE, SPHERICAL, Intrinsics, SensorExtrinsics, project,
 from .cueimage import (CueImage, CuePyramid, DeviceCueImage, NormalConfig, PyramidConfigError,
                        build_cue_image, build_pyramid, estimate_normals, footprint_index)
 from .pyramid_device import build_pyramids_device, estimate_normals_device
+from .evaluation import (AteReport, DegenerateAlignmentError, NoAssociationError, associate,
+                         ate_rmse, evaluate_ate, horn_align)
 from .dataset import (DatasetError, DatasetManifest, DimensionMismatchError, ManifestError,
                       MissingFileError, SensorConfig, Trajectory, TrajectoryFormatError,
                       load_dataset, load_manifest, load_trajectory, read_depth, read_intensity,
@@ -30,6 +32,8 @@ from .bundle import (CONSECUTIVE, COUPLED, BAProblem, FusionConfigError, Iterati
 __version__ = "0.1.0"
 
 __all__ = [
+    "AteReport", "DegenerateAlignmentError", "NoAssociationError", "associate", "ate_rmse",
+    "evaluate_ate", "horn_align",
     "DatasetError", "DatasetManifest", "DimensionMismatchError", "ManifestError",
     "MissingFileError", "SensorConfig", "Trajectory", "TrajectoryFormatError", "load_dataset",
     "load_manifest", "load_trajectory", "read_depth", "read_intensity", "read_raster",

@@ -28,6 +28,7 @@ import numpy as np
 
 from .camera import Intrinsics, SensorExtrinsics
 from .cueimage import NormalConfig, build_pyramid
+from .evaluation import Trajectory
 from .pairgraph import FrameNode
 from .se3 import Pose
 
@@ -50,29 +51,6 @@ class DimensionMismatchError(DatasetError):
 
 class TrajectoryFormatError(DatasetError):
     pass
-
-
-@dataclass
-class Trajectory:
-    """Timestamped poses, timestamps strictly increasing (evaluation.py:26-45)."""
-
-    timestamps: np.ndarray
-    poses: list
-
-    def __post_init__(self) -> None:
-        self.timestamps = np.asarray(self.timestamps, dtype=float)
-        if len(self.timestamps) != len(self.poses):
-            raise ValueError("timestamps and poses disagree in length")
-        if len(self.timestamps) == 0:
-            raise ValueError("trajectory must hold at least one pose")
-        if np.any(np.diff(self.timestamps) <= 0.0):
-            raise ValueError("timestamps must be strictly increasing")
-
-    def __len__(self) -> int:
-        return len(self.poses)
-
-    def translations(self) -> np.ndarray:
-        return np.stack([p.translation for p in self.poses])
 
 
 def trajectory_from_poses(timestamps, poses) -> Trajectory:

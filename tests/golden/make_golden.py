@@ -201,6 +201,39 @@ def pyramid_case():
     print("pyramid", (OUT / "pyramid.npz").stat().st_size, "bytes")
 
 
+def evaluation_case():
+    """associate / horn_align / evaluate_ate (evaluation.py:48-122) on
+    seeded trajectories: timestamp jitter, dropped poses, a rigid offset and
+    pose noise."""
+    from photoba.evaluation import Trajectory, associate, evaluate_ate
+
+    rng = np.random.default_rng(11)
+    d = {}
+    for case in range(4):
+        n = 40 + 10 * case
+        ts = np.cumsum(rng.uniform(0.05, 0.15, n))
+        ref = [boxplus(Pose(np.eye(3), rng.normal(0, 2.0, 3)), seeded_perturbation(rng, 0.0, 0.5))
+               for _ in range(n)]
+        g = boxplus(Pose(np.eye(3), [1.0, -2.0, 0.5]), seeded_perturbation(rng, 0.0, 0.7))
+        keep = np.sort(rng.choice(n, n - 5, replace=False))
+        est_ts = ts[keep] + rng.uniform(-0.01, 0.01, keep.size)
+        order = np.argsort(est_ts)
+        est = [g.compose(boxplus(ref[k], seeded_perturbation(rng, 0.02, 0.01))) for k in keep[order]]
+        tr_ref = Trajectory(ts, ref)
+        tr_est = Trajectory(est_ts[order], est)
+        pairs = associate(tr_est, tr_ref, 0.02)
+        rep = evaluate_ate(tr_est, tr_ref, 0.02)
+        d[f"ref_ts_{case}"] = ts
+        d[f"ref_{case}"] = pose_rows(ref)
+        d[f"est_ts_{case}"] = tr_est.timestamps
+        d[f"est_{case}"] = pose_rows(est)
+        d[f"pairs_{case}"] = np.array(pairs, dtype=np.int64)
+        d[f"report_{case}"] = np.array([rep.rmse, rep.rotation_rmse, rep.matches])
+        d[f"align_{case}"] = pose_rows([rep.alignment])[0]
+    np.savez_compressed(OUT / "evaluation.npz", **d)
+    print("evaluation", (OUT / "evaluation.npz").stat().st_size, "bytes")
+
+
 def dataset_case():
     """A two-sensor dataset directory written by the reference's
     generate_synthetic (synthetic.py:257-310), stored file by file, plus the
@@ -251,3 +284,4 @@ if __name__ == "__main__":
     footprint_case()
     pyramid_case()
     dataset_case()
+    evaluation_case()
