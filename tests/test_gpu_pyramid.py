@@ -185,3 +185,29 @@ def test_device_raster_decode_kinds():
     b = raw.cpu().numpy()[:6].astype(float) / 255.0
     np.testing.assert_array_equal(out.cpu().numpy(), b)
     assert lib.pba_decode_raster(raw.data_ptr(), 6, 7, 0.0, out.data_ptr(), stream) != 0
+
+
+def test_pipeline_from_disk_on_device_matches_host_pipeline(tmp_path):
+    """load_dataset -> build_graph -> solve_hierarchical -> evaluate_ate, all
+    GPU options on, against the same pipeline on host-built pyramids."""
+    from paper_2303_16878_b200 import dataset as DS
+    from tests.test_dataset import unpack
+
+    root, _ = unpack(tmp_path)
+    gt = DS.load_trajectory(root / "trajectory_gt.txt")
+    results = []
+    for device in (None, "cuda"):
+        manifest, guess, frames = DS.load_dataset(root, device=device)
+        ext = manifest.sensors[0].extrinsics
+        graph = P.build_graph(frames["cam0"], extrinsics=ext, device=device)
+        prob = P.BAProblem(graph, {"cam0": ext})
+        res = P.solve_hierarchical(prob, P.SolverConfig())
+        rep = P.evaluate_ate(P.trajectory_from_poses(guess.timestamps, res.poses), gt)
+        results.append((graph.edge_pairs(), res, rep))
+    (e_h, r_h, a_h), (e_d, r_d, a_d) = results
+    assert e_h == e_d
+    assert [(r.level, r.iteration, r.accepted, r.valid_blocks) for r in r_h.records] == \
+        [(r.level, r.iteration, r.accepted, r.valid_blocks) for r in r_d.records]
+    for p, q in zip(r_h.poses, r_d.poses):
+        assert np.abs(p.translation - q.translation).max() < 1e-9
+    assert abs(a_h.rmse - a_d.rmse) < 1e-9
