@@ -272,7 +272,7 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
-    if world > 1:
+    if world > 1 or os.environ.get("PBA_FORCE_SHARDED") == "1":
         dist.init_process_group("nccl", device_id=device)
     lib = native.load()
 
@@ -371,7 +371,7 @@ def run_ours(args):
            "path": "DeviceLevel.try_step via the C ABI; poses in/out through pinned host buffers"}
 
     if rank != 0:
-        if world > 1:
+        if dist.is_initialized():
             dist.destroy_process_group()
         return None
 
@@ -434,7 +434,7 @@ def run_ours(args):
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(prob, guess, level, total_pp)
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
     return line
 

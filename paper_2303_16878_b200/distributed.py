@@ -32,9 +32,12 @@ except Exception:  # pragma: no cover
 
 
 def current_group():
+    """The default process group when more than one rank shares the level
+    (PBA_FORCE_SHARDED=1 keeps the sharded path at world size 1, to exercise
+    the NCCL collectives on a single-GPU box)."""
     if dist is None or not dist.is_available() or not dist.is_initialized():
         return None
-    if dist.get_world_size() == 1:
+    if dist.get_world_size() == 1 and os.environ.get("PBA_FORCE_SHARDED") != "1":
         return None
     return dist.group.WORLD
 

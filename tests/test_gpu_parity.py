@@ -532,3 +532,42 @@ def test_build_graph_gpu_equals_host_on_corridor():
     g_gpu = P.build_graph(nodes, crit, extrinsics=ext, device="cuda:0")
     assert g_gpu.edges == prob.graph.edges  # bench built it on the host
     assert len(g_gpu.edges) == 968  # SURVEY.md App. C validated prototype
+
+
+_NCCL_SCRIPT = r"""
+import json, os, sys
+sys.path.insert(0, os.getcwd())
+import numpy as np, torch, torch.distributed as dist
+import paper_2303_16878_b200 as P
+from tests import fixtures as F
+d = F.load("pinhole_small")
+prob, _ = F.single_problem(d)
+out = {}
+res = P.solve_hierarchical(prob, P.SolverConfig())
+out["plain"] = [list(p.as_row()) for p in res.poses]
+os.environ["PBA_FORCE_SHARDED"] = "1"
+dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+res = P.solve_hierarchical(prob, P.SolverConfig())
+out["nccl"] = [list(p.as_row()) for p in res.poses]
+out["trace"] = [(r.level, r.iteration, r.accepted, r.valid_blocks) for r in res.records]
+dist.destroy_process_group()
+print(json.dumps(out))
+"""
+
+
+def test_sharded_path_over_nccl_matches_single_gpu():
+    """The multi-GPU code path (ShardedLevel: record all_gather, pose and
+    scalar broadcasts over NCCL) on one rank gives bit-identical poses."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT="29517")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _NCCL_SCRIPT], cwd=root, env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    assert np.array_equal(np.array(out["plain"]), np.array(out["nccl"]))
+    assert len(out["trace"]) > 0
