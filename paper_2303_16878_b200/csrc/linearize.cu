@@ -312,12 +312,10 @@ __device__ __forceinline__ void accumulate_cheap(double* Q, double* beta, double
   beta[0] = fma(ww, ec, beta[0]);
 }
 
-__device__ __forceinline__ void prefetch_l1(const void* p) {
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-}
 
-// kProbe: 0 normal; 1 diagnostics (fixed destination texel); 5 / 6 source
-// texel prefetched into L1 one / two pixels ahead instead of into registers.
+// kProbe (diagnostics only, K1 ablations): 0 normal; 1 every
+// sample reads one fixed destination texel; 10 no gradient gathers; 11 a
+// 7-sum stand-in for the 27-sum accumulation.
 template <bool kJac, int kT, int kMinBlocks, int kProbe = 0>
 __global__ void __launch_bounds__(kT, kMinBlocks)
     linearize_kernel(const pba_frame* __restrict__ frames, const pba_pair* __restrict__ pairs,
@@ -359,58 +357,27 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
   // ahead: (I, D) and (nz, mask) words, 2 x 16 B.  Masks come from the texel
   // lines themselves, so a pixel costs two dependent L2 round trips (source
   // texel, destination texels) instead of four.
-  // kProbe 5 / 6: the next (5) or next-but-one (6) pixel's source texel
-  // is prefetched into L1 instead of registers, and the current one is
-  // loaded at the top of the iteration.
-  constexpr bool kL1Src = kProbe == 5 || kProbe == 6;
   double2 nx0 = make_double2(0.0, 0.0), nx2 = make_double2(0.0, 0.0);
   if (first + (int)threadIdx.x < last) {
     const double2* t = S.src_tex + gr * stride * sW + gcol * stride;
-    if (kL1Src) {
-      prefetch_l1(t), prefetch_l1(t + kPairNzM * S.src_np);
-    } else {
-      nx0 = __ldg(t);
-      nx2 = __ldg(t + kPairNzM * S.src_np);
-    }
+    nx0 = __ldg(t);
+    nx2 = __ldg(t + kPairNzM * S.src_np);
   }
   int ngr = gr, ngcol = gcol;
-  int pgr = gr, pgcol = gcol;  // kProbe 6: pixel two iterations ahead
-  if (kProbe == 6) {
-    advance_pixel(pgr, pgcol, gw, kT);
-    if (first + (int)threadIdx.x + kT < last)
-    if (first + (int)threadIdx.x + kT < last) {
-      const double2* t = S.src_tex + pgr * stride * sW + pgcol * stride;
-      prefetch_l1(t), prefetch_l1(t + kPairNzM * S.src_np);
-    }
-  }
   for (int idx = first + (int)threadIdx.x; idx < last; idx += kT, gr = ngr, gcol = ngcol) {
     const int row = gr * stride;
     const int col = gcol * stride;
     const int sp = row * sW + col;
-    if (kL1Src) {
-      nx0 = __ldg(S.src_tex + sp);
-      nx2 = __ldg(S.src_tex + kPairNzM * S.src_np + sp);
-    }
     const double2 s_id = nx0;  // I, D
     const uint32_t sm = mask_word(nx2);
     const double mask_src_nz = nx2.x;
     ngr = gr;
     ngcol = gcol;
     advance_pixel(ngr, ngcol, gw, kT);
-    if (kProbe == 6) {
-      advance_pixel(pgr, pgcol, gw, kT);
-      if (idx + 2 * kT < last) {
-        const double2* t = S.src_tex + pgr * stride * sW + pgcol * stride;
-        prefetch_l1(t), prefetch_l1(t + kPairNzM * S.src_np);
-      }
-    } else if (idx + kT < last) {
+    if (idx + kT < last) {
       const double2* t = S.src_tex + ngr * stride * sW + ngcol * stride;
-      if (kL1Src) {
-        prefetch_l1(t), prefetch_l1(t + kPairNzM * S.src_np);
-      } else {
-        nx0 = __ldg(t);
-        nx2 = __ldg(t + kPairNzM * S.src_np);
-      }
+      nx0 = __ldg(t);
+      nx2 = __ldg(t + kPairNzM * S.src_np);
     }
     if (!(sm & PBA_MASK_DEPTH_VALID)) continue;  // PairContext.build: usable = depth_valid
 
@@ -502,16 +469,6 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     const double2 a00 = __ldg(t00), a01 = __ldg(t00 + 1), a10 = __ldg(t10), a11 = __ldg(t10 + 1);
     const double2 m00 = __ldg(t00 + kPairNzM * dnp), m01 = __ldg(t00 + kPairNzM * dnp + 1);
     const double2 m10 = __ldg(t10 + kPairNzM * dnp), m11 = __ldg(t10 + kPairNzM * dnp + 1);
-    if (kJac && kProbe == 7) {  // the remaining planes of the footprint, into L1 now
-      prefetch_l1(t00 + kPairGI * dnp), prefetch_l1(t10 + kPairGI * dnp);
-      prefetch_l1(t00 + kPairGD * dnp), prefetch_l1(t10 + kPairGD * dnp);
-      if (sm & PBA_MASK_NORMAL_VALID) {
-        prefetch_l1(t00 + kPairNxy * dnp), prefetch_l1(t10 + kPairNxy * dnp);
-#pragma unroll
-        for (int k = 0; k < 3; ++k)
-          prefetch_l1(t00 + (kPairGN + k) * dnp), prefetch_l1(t10 + (kPairGN + k) * dnp);
-      }
-    }
     const uint32_t mk = mask_word(m00) & mask_word(m01) & mask_word(m10) & mask_word(m11);
     if (!(mk & PBA_MASK_SAMP_CORE)) continue;  // core_ok
     const double Dd = bil(a00.y, a01.y, a10.y, a11.y, wx, wy);
@@ -825,9 +782,9 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
     // CTA-size / occupancy variant (PBA_LIN_VARIANT overrides):
     //   1: 256 thr, <=255 regs (8 warps/SM)    2: 256 thr, 128 regs (16 warps/SM)
     //   3: 128 thr, 128 regs (16 warps/SM)     4: 128 thr, 168 regs (12 warps/SM)
-    //   5: 512 thr, 128 regs (16 warps/SM)   13 / 14: 32 / 64 thr, 12 warps/SM
-    //  15 / 16: variant 4 with the source texel prefetched into L1 1 / 2 ahead
-    //   9: diagnostics (fixed destination texel)
+    //   5: 512 thr, 128 regs (16 warps/SM)
+    //   9 / 20 / 21: diagnostics (fixed destination texel / no gradient
+    //   gathers / reduced accumulation), see kProbe
     static int variant = -1;
     if (variant < 0) {
       const char* env = getenv("PBA_LIN_VARIANT");
@@ -843,18 +800,6 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
         case 3: PBA_LAUNCH_LIN(true, 128, 4); break;
         case 5: PBA_LAUNCH_LIN(true, 512, 1); break;
         case 2: PBA_LAUNCH_LIN(true, 256, 2); break;
-        case 13: PBA_LAUNCH_LIN(true, 32, 12); break;
-        case 15:
-          linearize_kernel<true, 128, 3, 5><<<grid, 128, 0, st>>>(frames, pairs, chunk_table,
-                                                                chunk_pixels, poses, extrinsics,
-                                                                *cfg, partials);
-          break;
-        case 16:
-          linearize_kernel<true, 128, 3, 6><<<grid, 128, 0, st>>>(frames, pairs, chunk_table,
-                                                                chunk_pixels, poses, extrinsics,
-                                                                *cfg, partials);
-          break;
-        case 14: PBA_LAUNCH_LIN(true, 64, 6); break;
         case 20:
           linearize_kernel<true, 128, 3, 10><<<grid, 128, 0, st>>>(frames, pairs, chunk_table,
                                                                  chunk_pixels, poses, extrinsics,
@@ -864,11 +809,6 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
           linearize_kernel<true, 128, 3, 11><<<grid, 128, 0, st>>>(frames, pairs, chunk_table,
                                                                  chunk_pixels, poses, extrinsics,
                                                                  *cfg, partials);
-          break;
-        case 17:
-          linearize_kernel<true, 128, 3, 7><<<grid, 128, 0, st>>>(frames, pairs, chunk_table,
-                                                                chunk_pixels, poses, extrinsics,
-                                                                *cfg, partials);
           break;
         case 9:  // diagnostics: destination gather replaced by a fixed texel
           linearize_kernel<true, 128, 3, 1><<<grid, 128, 0, st>>>(frames, pairs, chunk_table,
