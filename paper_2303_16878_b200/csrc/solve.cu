@@ -19,6 +19,7 @@
 // path (solver.py:513-522).
 
 #include <math.h>
+#include <stdlib.h>
 
 #include <vector>
 
@@ -182,6 +183,137 @@ __global__ void __launch_bounds__(1024) potrf_inv_kernel(double* __restrict__ A,
         if (j < c1) s0 = fma(a[i][j], x[j][col], s0);
         x[i][col] -= s0 + s1;
       }
+    }
+    __syncthreads();
+  }
+  double* Li = Linv + (long)k * NB * NB;
+  for (int e = tid; e < NB * NB; e += blockDim.x) {
+    const int r = e / NB, c = e % NB;
+    Li[e] = (c <= r) ? x[r][c] : 0.0;
+    if (r < n && c <= r) A[(long)(k0 + r) * dim + k0 + c] = a[r][c];
+  }
+}
+
+// Register-panel variant of potrf_inv (256 threads).  The tile is factored
+// in four 16-column panels; warp 0 factors a panel with the panel rows in
+// registers (lane l owns rows l and l + 32, 2 x 16 doubles), pivots and
+// column entries exchanged by shuffles, so a column step is a shuffle, an
+// rsqrt and one FMA wave with no shared-memory round trip.  All eight warps
+// then apply the rank-16 trailing update.  The inverse is blocked 16x16:
+// the four diagonal-block inverses in parallel (one warp each), then the
+// three block rows below with two barriers each.  Rows past the matrix end
+// are identity, so every tile runs the same schedule.
+constexpr int PW = 8;  // panel width
+
+__global__ void __launch_bounds__(256) potrf_reg_kernel(double* __restrict__ A, int dim, int k,
+                                                        double* __restrict__ Linv,
+                                                        int32_t* __restrict__ status) {
+  extern __shared__ double psm[];
+  double(*a)[LD] = reinterpret_cast<double(*)[LD]>(psm);
+  double(*x)[LD] = reinterpret_cast<double(*)[LD]>(psm + NB * LD);
+  double(*tt)[PW + 1] = reinterpret_cast<double(*)[PW + 1]>(psm + 2 * NB * LD);
+  __shared__ double rdiag[NB];
+  __shared__ int bad;
+  if (*status) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int k0 = k * NB;
+  const int n = min(NB, dim - k0);
+  for (int e = tid; e < NB * NB; e += blockDim.x) {
+    const int r = e / NB, c = e % NB;
+    a[r][c] = (r < n && c <= r) ? A[(long)(k0 + r) * dim + k0 + c] : (r == c ? 1.0 : 0.0);
+    x[r][c] = 0.0;
+  }
+  if (tid == 0) bad = 0;
+  __syncthreads();
+#pragma unroll 1
+  for (int c0 = 0; c0 < NB; c0 += PW) {
+    if (warp == 0) {
+      const int hp = c0 >> 5;  // half (row block) the panel's diagonal rows live in
+      double v0[PW], v1[PW];
+#pragma unroll
+      for (int c = 0; c < PW; ++c) {
+        v0[c] = a[lane][c0 + c];
+        v1[c] = a[lane + 32][c0 + c];
+      }
+#pragma unroll
+      for (int jj = 0; jj < PW; ++jj) {
+        const int j = c0 + jj;
+        const double dj = __shfl_sync(0xffffffffu, hp ? v1[jj] : v0[jj], j & 31);
+        if (lane == 0 && (!(dj > 0.0) || !isfinite(dj))) bad = 1;
+        const double inv = rsqrt(dj);
+        const double piv = dj * inv;
+        if (lane == 0) rdiag[j] = inv;
+        if (lane > j) v0[jj] *= inv;
+        else if (lane == j) v0[jj] = piv;
+        if (lane + 32 > j) v1[jj] *= inv;
+        else if (lane + 32 == j) v1[jj] = piv;
+#pragma unroll
+        for (int cc = jj + 1; cc < PW; ++cc) {
+          const int c = c0 + cc;
+          const double lcj = __shfl_sync(0xffffffffu, hp ? v1[jj] : v0[jj], c & 31);
+          if (lane >= c) v0[cc] = fma(-v0[jj], lcj, v0[cc]);
+          if (lane + 32 >= c) v1[cc] = fma(-v1[jj], lcj, v1[cc]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < PW; ++c) {
+        a[lane][c0 + c] = v0[c];
+        a[lane + 32][c0 + c] = v1[c];
+      }
+    }
+    __syncthreads();
+    if (bad) break;
+    // rank-16 trailing update: a[r][c] -= sum_j a[r][j] a[c][j], c1 <= c <= r
+    const int c1 = c0 + PW, m = NB - c1;
+    for (int e = tid; e < m * m; e += blockDim.x) {
+      const int r = c1 + e / m, c = c1 + e % m;
+      if (c <= r) {
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+        for (int j = 0; j < PW; j += 4) {
+          s0 = fma(a[r][c0 + j], a[c][c0 + j], s0);
+          s1 = fma(a[r][c0 + j + 1], a[c][c0 + j + 1], s1);
+          s2 = fma(a[r][c0 + j + 2], a[c][c0 + j + 2], s2);
+          s3 = fma(a[r][c0 + j + 3], a[c][c0 + j + 3], s3);
+        }
+        a[r][c] -= (s0 + s1) + (s2 + s3);
+      }
+    }
+    __syncthreads();
+  }
+  if (bad) {
+    if (tid == 0) *status = 1;
+    return;
+  }
+  // inverse, diagonal blocks: warp b < 4 inverts L_bb, lane c < 16 owns column c
+  if (warp < NB / PW && lane < PW) {
+    const int o = warp * PW, c = lane;
+    for (int i = 0; i < PW; ++i) {
+      double s = (i == c) ? 1.0 : 0.0;
+      for (int j = c; j < i; ++j) s = fma(-a[o + i][o + j], x[o + j][o + c], s);
+      x[o + i][o + c] = (i >= c) ? s * rdiag[o + i] : 0.0;
+    }
+  }
+  __syncthreads();
+  // block rows i = 1..3: T_ij = sum_{k=j}^{i-1} L_ik X_kj, then X_ij = -X_ii T_ij
+  for (int bi = 1; bi < NB / PW; ++bi) {
+    const int oi = bi * PW;
+    for (int e = tid; e < bi * PW * PW; e += blockDim.x) {
+      const int bj = e / (PW * PW), r = (e / PW) % PW, c = e % PW;
+      const int oj = bj * PW;
+      double s0 = 0.0, s1 = 0.0;
+      for (int q = oj; q < oi; q += 2) {
+        s0 = fma(a[oi + r][q], x[q][oj + c], s0);
+        s1 = fma(a[oi + r][q + 1], x[q + 1][oj + c], s1);
+      }
+      tt[bj * PW + r][c] = s0 + s1;
+    }
+    __syncthreads();
+    for (int e = tid; e < bi * PW * PW; e += blockDim.x) {
+      const int bj = e / (PW * PW), r = (e / PW) % PW, c = e % PW;
+      double s = 0.0;
+      for (int q = 0; q <= r; ++q) s = fma(x[oi + r][oi + q], tt[bj * PW + q][c], s);
+      x[oi + r][bj * PW + c] = -s;
     }
     __syncthreads();
   }
@@ -409,8 +541,19 @@ extern "C" int pba_solve_dense(const double* H, const double* b, int32_t dim, do
                                     tile_smem));
   PBA_CUDA_TRY(cudaFuncSetAttribute(potrf_inv_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));
+  const int reg_smem = tile_smem + (NB / PW - 1) * PW * (PW + 1) * (int)sizeof(double);
+  PBA_CUDA_TRY(cudaFuncSetAttribute(potrf_reg_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, reg_smem));
+  static int potrf_variant = -1;
+  if (potrf_variant < 0) {
+    const char* env = getenv("PBA_POTRF_VARIANT");
+    potrf_variant = env ? atoi(env) : 1;
+  }
   for (int k = 0; k < T; ++k) {
-    potrf_inv_kernel<<<1, 1024, tile_smem, st>>>(w.A, dim, k, w.Linv, status);
+    if (potrf_variant == 1)
+      potrf_reg_kernel<<<1, 256, reg_smem, st>>>(w.A, dim, k, w.Linv, status);
+    else
+      potrf_inv_kernel<<<1, 1024, tile_smem, st>>>(w.A, dim, k, w.Linv, status);
     PBA_LAUNCH_CHECK();
     const int m = last[k] - k;  // tile rows below k inside the envelope
     if (m > 0) {
