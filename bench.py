@@ -306,6 +306,11 @@ def run_ours(args):
 
     for _ in range(args.warmup):
         step()
+    # LM state at the start of the timed region, restored before the e2e loop
+    # so both loops run the identical sequence of steps
+    snap_rows = local_level.poses[local_level.cur].cpu().numpy().copy()
+    snap_gens = local_level.gens[local_level.cur].cpu().numpy().copy()
+    snap_state = dict(state)
     stream = torch.cuda.current_stream(device)
     local_level.kernel_events = []
     if getattr(local_level, "has_solver", False):
@@ -337,13 +342,17 @@ def run_ours(args):
     ms_per_step = elapsed_ms / args.steps
 
     # ---- e2e: host pose buffers in, poses + cost out, every step --------
+    # Same start state and hence the same step sequence as the timed loop.
     # The step's input (current poses + generations) is copied in from pinned
     # host memory and its result (the accepted poses) copied back out, so the
     # next step starts from host data; cost/count/status come back inside
     # try_step's scalar readback.
     L = local_level
-    host_in = torch.from_numpy(L.poses[L.cur].cpu().numpy()).pin_memory()
-    gens_in = torch.from_numpy(L.gens[L.cur].cpu().numpy()).pin_memory()
+    backend.set_poses(snap_rows, snap_gens)
+    backend.evaluate_current()
+    state.update(snap_state)
+    host_in = torch.from_numpy(snap_rows.copy()).pin_memory()
+    gens_in = torch.from_numpy(snap_gens.copy()).pin_memory()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
