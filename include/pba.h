@@ -262,6 +262,10 @@ int pba_decode_raster(const uint8_t* raw, int64_t n_samples, int32_t kind, doubl
  * (csrc/fastmath.cuh), exposed so tests can bound its error against the
  * library atan2 / numpy.arctan2 (sensors.py:120-121).  Device pointers. */
 int pba_atan2_batch(const double* y, const double* x, int64_t n, double* out, void* stream);
+/* Section timing of the linearisation kernel (PBA_LIN_VARIANT=24 only):
+ * summed clock64 cycles and visit counts of 8 per-pixel sections, host
+ * arrays of 8; reset != 0 zeroes the counters after reading. */
+int pba_diag_section_cycles(uint64_t* cycles, uint64_t* counts, int32_t reset);
 
 #ifdef __cplusplus
 }

@@ -313,6 +313,11 @@ __device__ __forceinline__ void accumulate_cheap(double* Q, double* beta, double
 }
 
 
+// kProbe 13 (diagnostics only): per-thread clock64 section timing, summed
+// into g_sect_cycles / g_sect_count (read by pba_diag_section_cycles).
+__device__ unsigned long long g_sect_cycles[8];
+__device__ unsigned long long g_sect_count[8];
+
 // kProbe (diagnostics only, K1 ablations): 0 normal; 1 every
 // sample reads one fixed destination texel; 10 no gradient gathers; 11 a
 // 7-sum stand-in for the 27-sum accumulation.
@@ -364,7 +369,19 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     nx2 = __ldg(t + kPairNzM * S.src_np);
   }
   int ngr = gr, ngcol = gcol;
+  constexpr bool kTime = kProbe == 13;
+  long long sect[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int sect_n[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long t_prev = kTime ? clock64() : 0;
+#define PBA_SECT(k)                          \
+  if (kTime) {                               \
+    const long long t_now = clock64();       \
+    sect[k] += t_now - t_prev;               \
+    ++sect_n[k];                             \
+    t_prev = t_now;                          \
+  }
   for (int idx = first + (int)threadIdx.x; idx < last; idx += kT, gr = ngr, gcol = ngcol) {
+    PBA_SECT(7)  // tail of the previous iteration (rejected pixels: their last section)
     const int row = gr * stride;
     const int col = gcol * stride;
     const int sp = row * sW + col;
@@ -380,6 +397,7 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
       nx2 = __ldg(t + kPairNzM * S.src_np);
     }
     if (!(sm & PBA_MASK_DEPTH_VALID)) continue;  // PairContext.build: usable = depth_valid
+    PBA_SECT(0)  // source texel + next-texel prefetch
 
     // ---- source cue values and unprojection (sensors.py:133-154) ----
     const double d = s_id.y;
@@ -454,6 +472,7 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     if (!(dist >= S.dst_cam.depth_min && dist <= S.dst_cam.depth_max)) continue;
     if (!(u >= 0.0 && u < dWd && v >= 0.0 && v < dHd)) continue;
 
+    PBA_SECT(1)  // unprojection + warp + projection
     // ---- bilinear footprint and validity (cues.py:397-409, 451-456) ----
     if (!(u <= dWd - 1.0 && v <= dHd - 1.0)) continue;  // inside (u, v >= 0 already)
     int x0 = (int)floor(u), y0 = (int)floor(v);
@@ -483,6 +502,7 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     }
     const double e0 = s_id.x - bil(a00.x, a01.x, a10.x, a11.x, wx, wy);
 
+    PBA_SECT(2)  // footprint, first destination gather, masks, occlusion
     const bool normal_on = (mk & PBA_MASK_SAMP_NORMAL) && (sm & PBA_MASK_NORMAL_VALID);
     double e2 = 0.0, e3 = 0.0, e4 = 0.0;
     double no[3] = {0.0, 0.0, 0.0};  // R_o n_src
@@ -516,6 +536,7 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     cost += (smI ? sI * sI : dI * (2.0 * sI - dI)) + (smD ? sD * sD : dD * (2.0 * sD - dD)) +
             (smN ? sN * sN : dN * (2.0 * sN - dN));
     ++count;
+    PBA_SECT(3)  // normal gather, residuals, Huber, cost
     if (!kJac) continue;
 
     // ---- projective Jacobian folded with M_i (sensors.py:157-188) ----
@@ -567,6 +588,7 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
       gI = bil4(i00, i01, i10, i11, w00, w01, w10, w11);
       gD = bil4(d00, d01, d10, d11, w00, w01, w10, w11);
     }
+    PBA_SECT(4)  // projective Jacobian, weights, I/D gradient gathers
     double* QA = Q;
     double* bA = beta;
     if (kProbe == 11) {
@@ -594,6 +616,15 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
       accumulate_channel(QA, bA, gN[1], MP0, MP1, nullptr, pu, xn, wN * cfg.omega[3], e3);
       cross3(&S.Mi[6], no, xn);
       accumulate_channel(QA, bA, gN[2], MP0, MP1, nullptr, pu, xn, wN * cfg.omega[4], e4);
+    }
+    PBA_SECT(5)  // q rows + accumulation (incl. normal-gradient gathers)
+  }
+  PBA_SECT(7)
+#undef PBA_SECT
+  if (kTime) {
+    for (int k = 0; k < 8; ++k) {
+      atomicAdd(&g_sect_cycles[k], (unsigned long long)sect[k]);
+      atomicAdd(&g_sect_count[k], (unsigned long long)sect_n[k]);
     }
   }
 
@@ -789,7 +820,7 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
     if (variant < 0) {
       const char* env = getenv("PBA_LIN_VARIANT");
       variant = env ? atoi(env) : 4;
-      if (variant < 1 || variant > 21) variant = 4;
+      if (variant < 1 || variant > 24) variant = 4;
     }
     const unsigned grid = (unsigned)n_chunks;
 #define PBA_LAUNCH_LIN(J, T, M) \
@@ -807,6 +838,11 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
           break;
         case 21:
           linearize_kernel<true, 128, 3, 11><<<grid, 128, 0, st>>>(frames, pairs, chunk_table,
+                                                                 chunk_pixels, poses, extrinsics,
+                                                                 *cfg, partials);
+          break;
+        case 24:
+          linearize_kernel<true, 128, 3, 13><<<grid, 128, 0, st>>>(frames, pairs, chunk_table,
                                                                  chunk_pixels, poses, extrinsics,
                                                                  *cfg, partials);
           break;
@@ -840,6 +876,18 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
   finalize_pairs_kernel<<<(unsigned)((n_pairs + 3) / 4), 128, 0, st>>>(
       partials, pair_chunk_offsets, pairs, poses, n_pairs, records);
   PBA_LAUNCH_CHECK();
+  return PBA_OK;
+}
+
+extern "C" int pba_diag_section_cycles(uint64_t* cycles, uint64_t* counts, int32_t reset) {
+  PBA_ARG_CHECK(cycles && counts, "NULL buffer");
+  PBA_CUDA_TRY(cudaMemcpyFromSymbol(cycles, g_sect_cycles, sizeof(g_sect_cycles)));
+  PBA_CUDA_TRY(cudaMemcpyFromSymbol(counts, g_sect_count, sizeof(g_sect_count)));
+  if (reset) {
+    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    PBA_CUDA_TRY(cudaMemcpyToSymbol(g_sect_cycles, z, sizeof(z)));
+    PBA_CUDA_TRY(cudaMemcpyToSymbol(g_sect_count, z, sizeof(z)));
+  }
   return PBA_OK;
 }
 

@@ -35,6 +35,7 @@ EXPORTED = (
     "pba_plan_assembly", "pba_assemble", "pba_sum_totals", "pba_solve_work_bytes",
     "pba_solve_dense", "pba_apply_step", "pba_overlap_counts", "pba_normals_scratch_bytes",
     "pba_estimate_normals", "pba_downscale_cues", "pba_decode_raster", "pba_atan2_batch",
+    "pba_diag_section_cycles",
 )
 
 
@@ -96,6 +97,7 @@ _SIGNATURES = {
     "pba_solve_dense": (ctypes.c_int, [_vp, _vp, _i32, _dbl, _vp, _vp, _vp, _vp, _vp]),
     "pba_apply_step": (ctypes.c_int, [_vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp]),
     "pba_atan2_batch": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp]),
+    "pba_diag_section_cycles": (ctypes.c_int, [_vp, _vp, _i32]),
     "pba_overlap_counts": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _dbl, _vp, _vp]),
     "pba_normals_scratch_bytes": (_sz, [ctypes.POINTER(Camera), _i32]),
     "pba_estimate_normals": (ctypes.c_int, [ctypes.POINTER(Camera), _vp, _vp, _i32,
