@@ -16,7 +16,6 @@ from __future__ import annotations
 
 import ctypes
 import math
-import os
 
 import numpy as np
 import torch
@@ -49,8 +48,7 @@ def chunk_pixels_for(total_pixels: int) -> int:
     CTAs for ~4 waves of 148 SMs, at most 32 pixels per thread."""
     ppt = total_pixels // (THREADS_PER_CHUNK * SM_COUNT * 4)
     ppt = max(1, min(32, int(ppt)))
-    div = int(os.environ.get("PBA_CHUNK_DIV", "1"))  # experiments only
-    return max(32, THREADS_PER_CHUNK * ppt // div)
+    return THREADS_PER_CHUNK * ppt
 
 
 def tile_envelope(slot_of_pose, pose_i, pose_j, dim, tile=64) -> np.ndarray:
