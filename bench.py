@@ -183,6 +183,25 @@ def measured_peak_hbm():
     return FALLBACK_HBM_GBS, "fallback"
 
 
+FLOPS_PER_VALID_PAIR = 1600  # SURVEY.md §8(d) F_alg, the reference formulation
+FP64_PEAK_TFLOPS = 35.7       # DFMA, measured on this B200 by tools/micro/dmma.cu
+
+
+def compute_roofline(counts, lin_ms):
+    """Informational fp64 view of K1: algorithmic flops of the reference's
+    formulation (F_alg per valid pixel-pair) over the measured DFMA peak.
+    The q-basis executes fewer flops than F_alg, so this is an algorithmic
+    rate, like roofline.achieved is for bytes."""
+    if not counts or not lin_ms:
+        return None
+    valid = statistics.mean(counts)
+    achieved = valid * FLOPS_PER_VALID_PAIR / (lin_ms * 1e-3) / 1e12
+    return {"bound": "fp64", "unit": "TFLOP/s", "achieved": achieved,
+            "peak": FP64_PEAK_TFLOPS, "peak_kind": "measured DFMA (tools/micro/dmma.cu)",
+            "frac": achieved / FP64_PEAK_TFLOPS, "valid_pairs_per_launch": valid,
+            "flops_per_valid_pair": FLOPS_PER_VALID_PAIR}
+
+
 def ncu_traffic(name):
     """dram bytes per pixel-pair of the linearisation kernel from the committed
     ncu --set full summary (profiles/), scaled to this launch; None if absent."""
@@ -295,8 +314,11 @@ def run_ours(args):
     lam = cfg.lm_initial_lambda
     state = {"cost": cost0, "lam": lam}
 
+    counts = []  # valid pixel-pairs (the reference's `count`) of every linearisation
+
     def step():
         ok_s, ok_u, c, n = backend.try_step(state["lam"])
+        counts.append(n)
         if ok_s and ok_u and c < state["cost"] and n > 0:
             backend.accept()
             state["cost"] = c
@@ -436,6 +458,8 @@ def run_ours(args):
             "solve_ms": statistics.mean(solve_ms) if solve_ms else None,
             "algorithmic_bytes_per_launch": shard_pp * BYTES_PER_PIXEL_PAIR,
         },
+        "compute": compute_roofline(counts[args.warmup:args.warmup + args.steps], lin_avg_ms)
+        if world == 1 else None,
         "e2e": e2e,
         "gpu_launches": int(round(launches)),
         "clocks": clocks.summary(),
