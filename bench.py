@@ -4,7 +4,7 @@ finest pyramid level (solve + pose update + linearise + assemble), the
 metric of BASELINE.json ("GN iteration time (ms) and pixel-pair
 residuals/sec at 1/2/4/8 B200; % HBM roofline").
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4|c2|c1]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4|c1|c2|c3|c5]
                   [--impl ours|reference]
 
 value    = pixel-pair residuals per second of GN iteration, whole job
@@ -55,9 +55,18 @@ CONFIGS = {
                factors=(1,), max_translation=1.0),
     "c2": dict(desc="synthetic LiDAR spherical 64x1024 (HDL-64), 100 scans, 3 levels",
                kind="hdl64", n=100, spacing=0.1, factors=(4, 2, 1), max_translation=1.0),
+    "c3": dict(desc="synthetic RGB-D pinhole 640x480 (TUM-shaped), 500 frames, 3 levels",
+               kind="tum", n=500, spacing=0.05, factors=(4, 2, 1), max_translation=1.0),
     "c4": dict(desc="synthetic OS0-128 128x1024, 1000 scans, 2 km corridor, 3 levels, ~20k pairs",
                kind="os0", n=1000, spacing=2.0, factors=(4, 2, 1), max_translation=40.0),
+    "c5": dict(desc="joint LiDAR+RGB-D coupled BA: 500 platform poses x (OS0-128 128x1024 + "
+                    "RGB-D 640x480), 3 levels", kind="fused", n=500, spacing=0.5,
+               factors=(4, 2, 1), max_translation=10.0, max_translation_rgbd=1.0),
 }
+
+# pinhole camera looking along the corridor (+x of the platform): camera z ->
+# platform x, camera x -> platform -y, camera y -> platform -z
+FORWARD_CAMERA = np.array([[0.0, 0.0, 1.0], [-1.0, 0.0, 0.0], [0.0, -1.0, 0.0]])
 
 
 def build_problem(name: str, device, n_override=None):
@@ -68,32 +77,54 @@ def build_problem(name: str, device, n_override=None):
 
     c = CONFIGS[name]
     n = n_override or c["n"]
-    if c["kind"] == "room":
-        cam, scene = S.rgbd_160(), S.BoxScene()
-        gt = S.room_loop(n)
-        ext = P.Pose.identity()
-    elif c["kind"] == "hdl64":
-        cam = S.hdl64()
-        gt = S.corridor_trajectory(n, c["spacing"])
-        scene = S.corridor_scene(c["spacing"] * n + 20.0)
-        ext = P.Pose.identity()
-    else:
+    graph_device = device if getattr(device, "type", "cpu") == "cuda" else None
+
+    t_graph = 0.0
+
+    def sensor_problem(cam, scene, gt, guess, ext, max_translation, sensor_id):
+        nonlocal t_graph
+        pyrs = S.device_pyramids(scene, cam, gt, ext, c["factors"], device)
+        nodes = [P.FrameNode(k, guess[k], pyrs[k], 0.1 * k, sensor_id) for k in range(n)]
+        crit = P.MatchCriteria(max_translation=max_translation)
+        sensor_ext = P.SensorExtrinsics(ext)
+        t0 = time.perf_counter()
+        graph = P.build_graph(nodes, crit, extrinsics=sensor_ext, threads=8, device=graph_device)
+        t_graph += time.perf_counter() - t0
+        return P.BAProblem(graph, {sensor_id: sensor_ext})
+
+    if c["kind"] in ("room", "hdl64", "os0", "tum"):
+        if c["kind"] == "room":
+            cam, scene, gt = S.rgbd_160(), S.BoxScene(), S.room_loop(n)
+            ext = P.Pose.identity()
+        elif c["kind"] == "tum":
+            cam = S.tum_640()
+            gt = S.corridor_trajectory(n, c["spacing"])
+            scene = S.corridor_scene(c["spacing"] * n + 20.0)
+            ext = P.Pose(FORWARD_CAMERA, [0.0, 0.0, 0.1])
+        else:
+            cam = S.hdl64() if c["kind"] == "hdl64" else S.lidar_os0_128()
+            gt = S.corridor_trajectory(n, c["spacing"])
+            scene = S.corridor_scene(c["spacing"] * n + 20.0)
+            ext = P.Pose.identity() if c["kind"] == "hdl64" else P.Pose(np.eye(3), [0.0, 0.0, -0.05])
+        guess = S.perturb(gt, 0.05, math.radians(2.0), 11)
+        problems = [sensor_problem(cam, scene, gt, guess, ext, c["max_translation"], "sensor0")]
+    else:  # fused: one platform trajectory, a LiDAR and a forward RGB-D camera
         cam = S.lidar_os0_128()
         gt = S.corridor_trajectory(n, c["spacing"])
         scene = S.corridor_scene(c["spacing"] * n + 20.0)
-        ext = P.Pose(np.eye(3), [0.0, 0.0, -0.05])
-    guess = S.perturb(gt, 0.05, math.radians(2.0), 11)
-    pyrs = S.device_pyramids(scene, cam, gt, ext, c["factors"], device)
-    nodes = [P.FrameNode(k, guess[k], pyrs[k], 0.1 * k) for k in range(n)]
-    crit = P.MatchCriteria(max_translation=c["max_translation"])
-    sensor_ext = P.SensorExtrinsics(ext)
-    t0 = time.perf_counter()
-    graph_device = device if getattr(device, "type", "cpu") == "cuda" else None
-    graph = P.build_graph(nodes, crit, extrinsics=sensor_ext, threads=8, device=graph_device)
-    t_graph = time.perf_counter() - t0
-    prob = P.BAProblem(graph, {"sensor0": sensor_ext})
-    return prob, guess, gt, dict(name=name, desc=c["desc"], frames=n, cam=cam,
-                                 level=len(c["factors"]) - 1, graph_seconds=t_graph)
+        guess = S.perturb(gt, 0.05, math.radians(2.0), 11)
+        problems = [
+            sensor_problem(cam, scene, gt, guess, P.Pose(np.eye(3), [0.0, 0.0, -0.05]),
+                           c["max_translation"], "lidar0"),
+            sensor_problem(S.tum_640(), scene, gt, guess, P.Pose(FORWARD_CAMERA, [0.1, 0.0, 0.1]),
+                           c["max_translation_rgbd"], "rgbd0"),
+        ]
+    return problems, guess, gt, dict(name=name, desc=c["desc"], frames=n, cam=cam,
+                                     level=len(c["factors"]) - 1, graph_seconds=t_graph)
+
+
+def problems_pixel_pairs(problems, level) -> int:
+    return sum(valid_pixel_pairs(p, level) for p in problems)
 
 
 def valid_pixel_pairs(prob, level) -> int:
@@ -218,9 +249,9 @@ def ncu_traffic(name):
 # ---------------------------------------------------------------------------
 # CPU baseline: the oracle port on a bounded sample
 # ---------------------------------------------------------------------------
-def cpu_baseline(prob, guess, level, total_pp, target_seconds=12.0, threads=None):
-    import copy
-
+def cpu_baseline(problems, guess, level, total_pp, target_seconds=12.0, threads=None):
+    """The oracle C port on all host cores over a bounded prefix of every
+    problem's pairs, extrapolated by pixel count, + the full dense LU solve."""
     import paper_2303_16878_b200 as P
     from oracle import oracle as O
 
@@ -228,26 +259,33 @@ def cpu_baseline(prob, guess, level, total_pp, target_seconds=12.0, threads=None
     cfg = P.SolverConfig()
     rows, _ = P.se3.pose_rows(guess)
 
-    def sub_problem(k):
+    def sub_problem(prob, k):
         g = P.MatchGraph(prob.graph.nodes, prob.graph.edges[:k])
         return P.BAProblem(g, prob.extrinsics, prob.gauge_index)
 
-    # calibrate on a few pairs, then size the sample to ~target_seconds
-    k = min(4, len(prob.graph.edges))
-    lp = O.OracleLevel([sub_problem(k)], level, cfg)
-    t0 = time.perf_counter()
-    lp.records(rows, True, threads)
-    dt = max(time.perf_counter() - t0, 1e-6)
-    per_pair = dt / k * min(k, threads) / threads if k < threads else dt / k
-    k2 = int(max(k, min(len(prob.graph.edges), target_seconds / max(per_pair, 1e-6))))
-    k2 = max(threads, min(k2, len(prob.graph.edges)))
-    lp = O.OracleLevel([sub_problem(k2)], level, cfg)
-    sample_pp = valid_pixel_pairs(sub_problem(k2), level)
-    t0 = time.perf_counter()
-    lp.records(rows, True, threads)
-    t_lin = time.perf_counter() - t0
+    t_lin_total, parts = 0.0, []
+    for prob in problems:
+        budget = target_seconds / len(problems)
+        # calibrate on a few pairs, then size the sample to the budget
+        k = min(4, len(prob.graph.edges))
+        lp = O.OracleLevel([sub_problem(prob, k)], level, cfg)
+        t0 = time.perf_counter()
+        lp.records(rows, True, threads)
+        dt = max(time.perf_counter() - t0, 1e-6)
+        per_pair = dt / k * min(k, threads) / threads if k < threads else dt / k
+        k2 = int(max(k, min(len(prob.graph.edges), budget / max(per_pair, 1e-6))))
+        k2 = max(min(threads, len(prob.graph.edges)), min(k2, len(prob.graph.edges)))
+        lp = O.OracleLevel([sub_problem(prob, k2)], level, cfg)
+        sample_pp = valid_pixel_pairs(sub_problem(prob, k2), level)
+        t0 = time.perf_counter()
+        lp.records(rows, True, threads)
+        t_lin = time.perf_counter() - t0
+        full_pp = valid_pixel_pairs(prob, level)
+        t_lin_total += t_lin * (full_pp / max(sample_pp, 1))
+        parts.append(f"the first {k2} of {len(prob.graph.edges)} pairs ({sample_pp} pixel-pairs, "
+                     f"{t_lin:.2f} s)")
     # dense LU of the reference (np.linalg.solve on dim 6(N-1)), timed in full
-    n = len(prob.graph.nodes)
+    n = len(problems[0].graph.nodes)
     dim = 6 * (n - 1)
     rng = np.random.default_rng(0)
     A = rng.normal(size=(dim, 64))
@@ -260,16 +298,15 @@ def cpu_baseline(prob, guess, level, total_pp, target_seconds=12.0, threads=None
     t0 = time.perf_counter()
     lp.apply_step(rows, gens, np.zeros(dim))
     t_upd = time.perf_counter() - t0
-    t_iter = t_lin * (total_pp / max(sample_pp, 1)) + t_solve + t_upd
+    t_iter = t_lin_total + t_solve + t_upd
     return {
         "value": total_pp / t_iter,
         "unit": "pixel-pairs/s",
         "cores": threads,
         "kind": "port",
-        "sample": (f"oracle C port (OpenMP {threads} threads) linearising the first {k2} of "
-                   f"{len(prob.graph.edges)} pairs ({sample_pp} pixel-pairs, {t_lin:.2f} s), "
-                   f"extrapolated by pixel count to {total_pp}; + full np.linalg.solve dim {dim} "
-                   f"({t_solve:.2f} s) + apply_step ({t_upd * 1e3:.1f} ms)"),
+        "sample": (f"oracle C port (OpenMP {threads} threads) linearising " + "; ".join(parts) +
+                   f", extrapolated by pixel count to {total_pp}; + full np.linalg.solve dim "
+                   f"{dim} ({t_solve:.2f} s) + apply_step ({t_upd * 1e3:.1f} ms)"),
         "gn_iteration_ms_extrapolated": t_iter * 1e3,
     }
 
@@ -296,20 +333,22 @@ def run_ours(args):
     lib = native.load()
 
     t_setup = time.perf_counter()
-    prob, guess, gt, meta = build_problem(args.config, device, args.frames)
+    problems, guess, gt, meta = build_problem(args.config, device, args.frames)
+    if len(problems) > 1 and (world > 1 or os.environ.get("PBA_FORCE_SHARDED") == "1"):
+        raise SystemExit("fused (multi-sensor) configs are benchmarked on one GPU")
     level = meta["level"]
     cfg = P.SolverConfig()
     store = FrameStore(device)
     group = D.current_group()
-    backend = D.make_level([prob], level, cfg, store, group)
+    backend = D.make_level(problems, level, cfg, store, group)
     local_level = backend.local if hasattr(backend, "local") else backend
     rows, gens = P.se3.pose_rows(guess)
     backend.set_poses(rows, gens)
     cost0, count0 = backend.evaluate_current()
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t_setup
-    total_pp = valid_pixel_pairs(prob, level)
-    n_pairs = len(prob.graph.edges)
+    total_pp = problems_pixel_pairs(problems, level)
+    n_pairs = sum(len(p.graph.edges) for p in problems)
 
     lam = cfg.lm_initial_lambda
     state = {"cost": cost0, "lam": lam}
@@ -409,7 +448,7 @@ def run_ours(args):
     peak, peak_kind = measured_peak_hbm()
     lin_avg_ms = statistics.mean(lin_ms) if lin_ms else float("nan")
     my_pp = getattr(local_level, "pixels_shard", None)
-    shard_pp = total_pp if world == 1 else valid_pixel_pairs_shard(prob, level, local_level)
+    shard_pp = total_pp if world == 1 else valid_pixel_pairs_shard(problems[0], level, local_level)
     achieved = shard_pp * BYTES_PER_PIXEL_PAIR / (lin_avg_ms / 1e3) / 1e9
     trafficd = ncu_traffic(args.config)
     traffic = None
@@ -465,7 +504,7 @@ def run_ours(args):
         "clocks": clocks.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(prob, guess, level, total_pp)
+        line["cpu_baseline"] = cpu_baseline(problems, guess, level, total_pp)
     print(json.dumps(line), flush=True)
     if dist.is_initialized():
         dist.destroy_process_group()
@@ -490,12 +529,12 @@ def run_reference(args):
     import torch
 
     device = torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
-    prob, guess, gt, meta = build_problem(args.config, device, args.frames)
+    problems, guess, gt, meta = build_problem(args.config, device, args.frames)
     level = meta["level"]
-    total_pp = valid_pixel_pairs(prob, level)
+    total_pp = problems_pixel_pairs(problems, level)
     vals = []
     for k in range(args.warmup + args.steps):
-        cb = cpu_baseline(prob, guess, level, total_pp, target_seconds=args.ref_seconds)
+        cb = cpu_baseline(problems, guess, level, total_pp, target_seconds=args.ref_seconds)
         if k >= args.warmup:
             vals.append(cb)
     v = statistics.median(c["value"] for c in vals)
@@ -516,7 +555,8 @@ def run_reference(args):
         "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": f"{args.config}: {meta['desc']}", "frames": meta["frames"],
-                   "pairs": len(prob.graph.edges), "pixel_pairs_per_iteration": total_pp},
+                   "pairs": sum(len(p.graph.edges) for p in problems),
+                   "pixel_pairs_per_iteration": total_pp},
         "cpu_baseline": {"value": v, "unit": "pixel-pairs/s", "cores": vals[-1]["cores"],
                          "kind": "port", "sample": vals[-1]["sample"]},
         "e2e": {"value": v, "unit": "pixel-pairs/s", "h2d_bytes_per_step": 0,

@@ -229,6 +229,11 @@ def hdl64(width: int = 1024, height: int = 64) -> Intrinsics:
                       height, SPHERICAL, 0.5, 80.0)
 
 
+def tum_640() -> Intrinsics:
+    """TUM-shaped 640x480 RGB-D camera of App. C configs 3 and 5."""
+    return Intrinsics(525.0, 525.0, 319.5, 239.5, 640, 480, PINHOLE, 0.1, 20.0)
+
+
 def rgbd_160() -> Intrinsics:
     """App. C config 1 pinhole camera."""
     return Intrinsics(70.0, 70.0, 80.0, 60.0, 160, 120, PINHOLE, 0.1, 50.0)

@@ -8,8 +8,8 @@ import paper_2303_16878_b200 as P
 from paper_2303_16878_b200.device import DeviceLevel, FrameStore
 
 dev = torch.device("cuda", 0)
-prob, guess, gt, meta = bench.build_problem("c4", dev, int(sys.argv[1]) if len(sys.argv) > 1 else 200)
-lv = DeviceLevel([prob], meta["level"], P.SolverConfig(), FrameStore(dev))
+problems, guess, gt, meta = bench.build_problem("c4", dev, int(sys.argv[1]) if len(sys.argv) > 1 else 200)
+lv = DeviceLevel(problems, meta["level"], P.SolverConfig(), FrameStore(dev))
 rows, _ = P.se3.pose_rows(guess)
 pt = torch.from_numpy(rows).to(dev)
 for want in (True, False, True, False):

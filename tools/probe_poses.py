@@ -8,8 +8,8 @@ import paper_2303_16878_b200 as P
 from paper_2303_16878_b200.device import DeviceLevel, FrameStore
 
 dev = torch.device("cuda", 0)
-prob, guess, gt, meta = bench.build_problem("c4", dev, 200)
-lv = DeviceLevel([prob], meta["level"], P.SolverConfig(), FrameStore(dev))
+problems, guess, gt, meta = bench.build_problem("c4", dev, 200)
+lv = DeviceLevel(problems, meta["level"], P.SolverConfig(), FrameStore(dev))
 for name, poses in (("guess", guess), ("gt", gt), ("guess", guess)):
     rows, _ = P.se3.pose_rows(poses)
     pt = torch.from_numpy(rows).to(dev)

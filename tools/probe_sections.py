@@ -19,8 +19,8 @@ NAMES = ["src texel", "unproject+warp+project", "gather1+masks+occlusion",
          "normals+residuals+Huber", "Jacobian+I/D gradients", "accumulate (+N gradients)",
          "-", "rejected tail"]
 dev = torch.device("cuda", 0)
-prob, guess, gt, meta = bench.build_problem("c4", dev, 200)
-lv = DeviceLevel([prob], meta["level"], P.SolverConfig(), FrameStore(dev))
+problems, guess, gt, meta = bench.build_problem("c4", dev, 200)
+lv = DeviceLevel(problems, meta["level"], P.SolverConfig(), FrameStore(dev))
 lib = N.load()
 cyc = (ctypes.c_uint64 * 8)()
 cnt = (ctypes.c_uint64 * 8)()
