@@ -525,13 +525,14 @@ def test_build_graph_gpu_equals_reference_edges(name):
 def test_build_graph_gpu_equals_host_on_corridor():
     import bench
 
-    prob, guess, gt, meta = bench.build_problem("c4", torch.device("cuda", 0), 60)
+    problems, guess, gt, meta = bench.build_problem("c4", torch.device("cuda", 0), 60)
+    prob = problems[0]
     nodes = prob.graph.nodes
     ext = prob.extrinsics_of("sensor0")
     crit = P.MatchCriteria(max_translation=40.0)
-    g_gpu = P.build_graph(nodes, crit, extrinsics=ext, device="cuda:0")
-    assert g_gpu.edges == prob.graph.edges  # bench built it on the host
-    assert len(g_gpu.edges) == 968  # SURVEY.md App. C validated prototype
+    g_host = P.build_graph(nodes, crit, extrinsics=ext, threads=8)
+    assert prob.graph.edges == g_host.edges  # bench built it on the device
+    assert len(g_host.edges) == 968  # SURVEY.md App. C validated prototype
 
 
 _NCCL_SCRIPT = r"""
