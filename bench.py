@@ -69,7 +69,7 @@ CONFIGS = {
 FORWARD_CAMERA = np.array([[0.0, 0.0, 1.0], [-1.0, 0.0, 0.0], [0.0, -1.0, 0.0]])
 
 
-def build_problem(name: str, device, n_override=None):
+def build_problem(name: str, device, n_override=None, normals: str = "estimate"):
     import torch
 
     import paper_2303_16878_b200 as P
@@ -83,7 +83,7 @@ def build_problem(name: str, device, n_override=None):
 
     def sensor_problem(cam, scene, gt, guess, ext, max_translation, sensor_id):
         nonlocal t_graph
-        pyrs = S.device_pyramids(scene, cam, gt, ext, c["factors"], device)
+        pyrs = S.device_pyramids(scene, cam, gt, ext, c["factors"], device, normals=normals)
         nodes = [P.FrameNode(k, guess[k], pyrs[k], 0.1 * k, sensor_id) for k in range(n)]
         crit = P.MatchCriteria(max_translation=max_translation)
         sensor_ext = P.SensorExtrinsics(ext)
