@@ -572,3 +572,30 @@ def test_sharded_path_over_nccl_matches_single_gpu():
     out = json.loads(r.stdout.strip().splitlines()[-1])
     assert np.array_equal(np.array(out["plain"]), np.array(out["nccl"]))
     assert len(out["trace"]) > 0
+
+
+def test_os0_128_full_resolution_records_and_trace_match_oracle():
+    """The bench's sensor shape (OS0-128, 128x1024, K6-estimated normals,
+    8192-pixel chunks): per-pair records at full resolution and a short LM
+    trace against the oracle."""
+    import bench
+
+    problems, guess, gt, meta = bench.build_problem("c4", torch.device("cuda", 0), 5)
+    prob = problems[0]
+    level = meta["level"]
+    rows, _ = P.se3.pose_rows(guess)
+    got = _level([prob], level).linearize(_rows(rows)).cpu().numpy()
+    ref = O.OracleLevel([prob], level, P.SolverConfig()).records(rows)
+    F.compare_records(got, ref)
+    assert ref[:, 91].sum() > 1e5
+    poses, records = P.solve_level(prob, guess, level, max_iterations=3)
+    lp = O.OracleLevel([prob], level, P.SolverConfig())
+    gens = np.zeros(len(guess), np.int64)
+    o_rows, _, o_recs = O.solve_level_multi(lp, rows, gens, level, P.SolverConfig(), 3)
+    assert [(r.iteration, r.accepted, r.valid_blocks) for r in records] == [
+        (r.iteration, r.accepted, r.valid_blocks) for r in o_recs]
+    for a, b in zip(records, o_recs):
+        assert a.lam == b.lam
+        assert abs(a.error - b.error) <= 1e-6 * b.error
+    er, et = _pose_err(np.stack([p.as_row() for p in poses]), o_rows)
+    assert er <= 1e-5 and et <= 1e-5
