@@ -599,3 +599,34 @@ def test_os0_128_full_resolution_records_and_trace_match_oracle():
         assert abs(a.error - b.error) <= 1e-6 * b.error
     er, et = _pose_err(np.stack([p.as_row() for p in poses]), o_rows)
     assert er <= 1e-5 and et <= 1e-5
+
+
+def test_c4_full_size_properties():
+    """BASELINE's c4 at full size (1000 OS0-128 scans, ~19k pairs), where the
+    oracle is too slow: records bit-identical across launches and across a
+    3-way pair sharding (so 1/2/4/8 GPUs give identical results), assembled
+    totals equal to the record sums, and a sampled pair equal to the oracle."""
+    import bench
+
+    dev = torch.device("cuda", 0)
+    problems, guess, gt, meta = bench.build_problem("c4", dev)
+    prob = problems[0]
+    level = meta["level"]
+    n = len(prob.graph.edges)
+    assert n > 18000
+    rows, gens = P.se3.pose_rows(guess)
+    lv = _level([prob], level)
+    full = lv.linearize(_rows(rows)).cpu().numpy()
+    assert np.array_equal(full, lv.linearize(_rows(rows)).cpu().numpy())
+    cuts = [0, n // 3, (2 * n) // 3, n]
+    parts = [_level([prob], level, pair_range=(a, b), assemble=False).linearize(_rows(rows))
+             .cpu().numpy() for a, b in zip(cuts, cuts[1:])]
+    assert np.array_equal(np.concatenate(parts), full)
+    lv.set_poses(rows, gens)
+    cost, count = lv.evaluate_current()
+    assert count == int(full[:, 91].sum())
+    assert abs(cost - full[:, 90].sum()) <= 1e-12 * cost
+    k = n // 2
+    sub = P.BAProblem(P.MatchGraph(prob.graph.nodes, prob.graph.edges[k:k + 1]), prob.extrinsics)
+    ref = O.OracleLevel([sub], level, P.SolverConfig()).records(rows)
+    F.compare_records(full[k:k + 1], ref)
