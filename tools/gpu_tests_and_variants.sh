@@ -1,2 +1,2 @@
 timeout 900 python -m pytest tests -m gpu -q --tb=short -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
-bash tools/gpu_quick3.sh
+bash tools/gpu_variants.sh
