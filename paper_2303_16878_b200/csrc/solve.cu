@@ -225,45 +225,15 @@ __global__ void __launch_bounds__(256) potrf_reg_kernel(double* __restrict__ A, 
   }
   if (tid == 0) bad = 0;
   __syncthreads();
-  // Look-ahead factorisation.  Warp 0 walks the panels: it loads panel p,
-  // applies panel p-1's rank-8 update to it in registers, factors it and
-  // publishes it (named barrier 1).  Warps 1-7 apply each published panel's
-  // update to the columns from panel p+2 on (so they never touch the panel
-  // warp 0 works on) and report (barrier 2); warp 0 waits for that report
-  // only two panels later.  The trailing updates leave the critical path.
-  constexpr int NP = NB / PW;
-  if (warp == 0) {
 #pragma unroll 1
-    for (int p = 0; p < NP; ++p) {
-      const int c0 = p * PW;
-      if (p >= 2) asm volatile("bar.sync 2, 256;" ::: "memory");  // rest-updates of p-2 done
+  for (int c0 = 0; c0 < NB; c0 += PW) {
+    if (warp == 0) {
       const int hp = c0 >> 5;  // half (row block) the panel's diagonal rows live in
       double v0[PW], v1[PW];
 #pragma unroll
       for (int c = 0; c < PW; ++c) {
         v0[c] = a[lane][c0 + c];
         v1[c] = a[lane + 32][c0 + c];
-      }
-      if (p >= 1) {  // rank-8 update from panel p-1, in registers
-        const int cp = c0 - PW;
-        double l0[PW], l1[PW];
-#pragma unroll
-        for (int j = 0; j < PW; ++j) {
-          l0[j] = a[lane][cp + j];
-          l1[j] = a[lane + 32][cp + j];
-        }
-#pragma unroll
-        for (int cc = 0; cc < PW; ++cc) {
-          double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-          for (int j = 0; j < PW; ++j) {
-            const double lc = a[c0 + cc][cp + j];
-            s0 = fma(l0[j], lc, s0);
-            s1 = fma(l1[j], lc, s1);
-          }
-          if (lane >= c0 + cc) v0[cc] -= s0;
-          if (lane + 32 >= c0 + cc) v1[cc] -= s1;
-        }
       }
 #pragma unroll
       for (int jj = 0; jj < PW; ++jj) {
@@ -290,33 +260,27 @@ __global__ void __launch_bounds__(256) potrf_reg_kernel(double* __restrict__ A, 
         a[lane][c0 + c] = v0[c];
         a[lane + 32][c0 + c] = v1[c];
       }
-      __syncwarp();
-      asm volatile("bar.arrive 1, 256;" ::: "memory");  // panel p published
     }
-  } else {
-    const int t = tid - 32;
-#pragma unroll 1
-    for (int p = 0; p < NP; ++p) {
-      asm volatile("bar.sync 1, 256;" ::: "memory");  // panel p published
-      const int c0 = p * PW, c2 = c0 + 2 * PW, m = NB - c2;
-      for (int e = t; e < m * m; e += blockDim.x - 32) {
-        const int r = c2 + e / m, c = c2 + e % m;
-        if (c <= r) {
-          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    __syncthreads();
+    if (bad) break;
+    // rank-16 trailing update: a[r][c] -= sum_j a[r][j] a[c][j], c1 <= c <= r
+    const int c1 = c0 + PW, m = NB - c1;
+    for (int e = tid; e < m * m; e += blockDim.x) {
+      const int r = c1 + e / m, c = c1 + e % m;
+      if (c <= r) {
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
-          for (int j = 0; j < PW; j += 4) {
-            s0 = fma(a[r][c0 + j], a[c][c0 + j], s0);
-            s1 = fma(a[r][c0 + j + 1], a[c][c0 + j + 1], s1);
-            s2 = fma(a[r][c0 + j + 2], a[c][c0 + j + 2], s2);
-            s3 = fma(a[r][c0 + j + 3], a[c][c0 + j + 3], s3);
-          }
-          a[r][c] -= (s0 + s1) + (s2 + s3);
+        for (int j = 0; j < PW; j += 4) {
+          s0 = fma(a[r][c0 + j], a[c][c0 + j], s0);
+          s1 = fma(a[r][c0 + j + 1], a[c][c0 + j + 1], s1);
+          s2 = fma(a[r][c0 + j + 2], a[c][c0 + j + 2], s2);
+          s3 = fma(a[r][c0 + j + 3], a[c][c0 + j + 3], s3);
         }
+        a[r][c] -= (s0 + s1) + (s2 + s3);
       }
-      if (p <= NP - 3) asm volatile("bar.arrive 2, 256;" ::: "memory");  // rest of p done
     }
+    __syncthreads();
   }
-  __syncthreads();
   if (bad) {
     if (tid == 0) *status = 1;
     return;
