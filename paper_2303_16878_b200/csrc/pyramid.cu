@@ -162,7 +162,7 @@ __device__ __forceinline__ double sat_at(const double* __restrict__ s, int W, in
   return (R == 0 || C == 0) ? 0.0 : s[(int64_t)(R - 1) * W + (C - 1)];
 }
 
-__global__ void __launch_bounds__(128, 4) normals_kernel(pba_camera cam,
+__global__ void __launch_bounds__(128, 6) normals_kernel(pba_camera cam,
                                                       const double* __restrict__ tab,
                                                       const double* __restrict__ depth,
                                                       const double* __restrict__ sat,
