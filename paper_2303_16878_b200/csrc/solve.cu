@@ -34,22 +34,39 @@ constexpr int LD = NB + 1;
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct SolveWork {
-  double* A;     // dim x dim (lower triangle used)
+  double* A;     // D x D, D = NB * T (lower triangle used; the dense path uses dim x dim)
   double* Linv;  // T x NB x NB inverses of the diagonal tiles
-  double* y;     // dim
-  int32_t* nz;   // T x T tile non-zero flags
+  double* y;     // D
+  double* bp;    // D: permuted right-hand side (dissection path)
+  double* xp;    // D: permuted solution (dissection path)
+  int32_t* lists;  // schedule of the dissection path (kListInts ints)
+  int32_t* nz;   // T x T tile non-zero flags, then env / last (2T)
 };
 
+constexpr int kMaxBand = 3;  // dissection: widest tile band handled
+
+// schedule buffer: new->old tile map, structural tiles, tile lists, pairs, triples
+size_t list_ints(size_t T) {
+  const size_t B = kMaxBand;
+  return T * (2 + 2 * (2 * B + 1) + 4 * B + 3 * B * (2 * B + 1));
+}
+
 SolveWork carve(void* work, int dim) {
-  const size_t T = (dim + NB - 1) / NB;
+  const size_t T = (dim + NB - 1) / NB, D = T * NB;
   char* p = static_cast<char*>(work);
   SolveWork w;
   w.A = reinterpret_cast<double*>(p);
-  p += align_up((size_t)dim * dim * sizeof(double), 256);
+  p += align_up(D * D * sizeof(double), 256);
   w.Linv = reinterpret_cast<double*>(p);
   p += align_up(T * NB * NB * sizeof(double), 256);
   w.y = reinterpret_cast<double*>(p);
-  p += align_up((size_t)dim * sizeof(double), 256);
+  p += align_up(D * sizeof(double), 256);
+  w.bp = reinterpret_cast<double*>(p);
+  p += align_up(D * sizeof(double), 256);
+  w.xp = reinterpret_cast<double*>(p);
+  p += align_up(D * sizeof(double), 256);
+  w.lists = reinterpret_cast<int32_t*>(p);
+  p += align_up(list_ints(T) * sizeof(int32_t), 256);
   w.nz = reinterpret_cast<int32_t*>(p);
   return w;
 }
@@ -205,7 +222,9 @@ __global__ void __launch_bounds__(1024) potrf_inv_kernel(double* __restrict__ A,
 // are identity, so every tile runs the same schedule.
 constexpr int PW = 8;  // panel width
 
-__global__ void __launch_bounds__(256) potrf_reg_kernel(double* __restrict__ A, int dim, int k,
+__global__ void __launch_bounds__(256) potrf_reg_kernel(double* __restrict__ A, int dim,
+                                                        int k_arg,
+                                                        const int32_t* __restrict__ klist,
                                                         double* __restrict__ Linv,
                                                         int32_t* __restrict__ status) {
   extern __shared__ double psm[];
@@ -216,6 +235,7 @@ __global__ void __launch_bounds__(256) potrf_reg_kernel(double* __restrict__ A, 
   __shared__ int bad;
   if (*status) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int k = klist ? klist[blockIdx.x] : k_arg;  // dissection path: one tile per CTA
   const int k0 = k * NB;
   const int n = min(NB, dim - k0);
   for (int e = tid; e < NB * NB; e += blockDim.x) {
@@ -421,6 +441,104 @@ __global__ void __launch_bounds__(256) syrk_kernel(double* __restrict__ A, int d
 // Forward (L y = -b) and backward (L^T x = y) substitution in one CTA of 1024
 // threads with the tile inverses: per tile row a gather over the non-zero
 // tiles (16 threads per row, shuffle-reduced), then a 64x64 mat-vec.
+// ---- nested-dissection path (long chain-like pose graphs) ---------------
+// Tiles are reordered so that P independent chain segments come first and
+// the (band-wide) separators between them last; the segments' steps run as
+// batched launches (one CTA per segment), then the separators' small Schur
+// complement is factored as usual.  See pba_solve_dense.
+
+// Ap (D x D, lower) = P (H + lam diag H) P^T on the structural tiles listed in
+// tiles (pairs of new tile indices, row >= col); padding rows are identity.
+__global__ void damp_copy_perm_kernel(const double* __restrict__ H, int dim, double lam, int D,
+                                      const int32_t* __restrict__ tiles,
+                                      const int32_t* __restrict__ new_to_old,
+                                      double* __restrict__ Ap) {
+  const int ti = tiles[2 * blockIdx.x], tj = tiles[2 * blockIdx.x + 1];
+  const int oi = new_to_old[ti], oj = new_to_old[tj];
+  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
+    const int r = e / NB, c = e % NB;
+    const int gr = oi * NB + r, gc = oj * NB + c;  // original scalar indices
+    double v;
+    if (gr >= dim || gc >= dim) {
+      v = (ti == tj && r == c) ? 1.0 : 0.0;
+    } else {
+      const int hi = max(gr, gc), lo = min(gr, gc);
+      const double h = H[(long)hi * dim + lo];
+      v = (gr == gc) ? h + lam * h : h;
+    }
+    Ap[(long)(ti * NB + r) * D + tj * NB + c] = v;
+  }
+}
+
+__global__ void permute_vec_kernel(const double* __restrict__ src, int dim, int T,
+                                   const int32_t* __restrict__ new_to_old,
+                                   double* __restrict__ dst, int to_new) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= T * NB) return;
+  const int g = new_to_old[i / NB] * NB + i % NB;  // original index of new index i
+  if (to_new) {
+    dst[i] = g < dim ? src[g] : 0.0;
+  } else if (g < dim) {
+    dst[g] = src[i];
+  }
+}
+
+// L_ik = A_ik L_kk^{-T} for listed (k, i) pairs
+__global__ void __launch_bounds__(256) panel_list_kernel(double* __restrict__ A, int D,
+                                                         const int32_t* __restrict__ pairs,
+                                                         const double* __restrict__ Linv,
+                                                         const int32_t* __restrict__ status) {
+  if (*status) return;
+  const int k = pairs[2 * blockIdx.x], bi = pairs[2 * blockIdx.x + 1];
+  extern __shared__ double smem[];
+  double* P = smem;
+  double* Q = smem + NB * LD;
+  const int k0 = k * NB, r0 = bi * NB;
+  const double* Li = Linv + (long)k * NB * NB;
+  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
+    const int r = e / NB, c = e % NB;
+    P[r * LD + c] = A[(long)(r0 + r) * D + k0 + c];
+    Q[r * LD + c] = Li[e];
+  }
+  __syncthreads();
+  double acc[4][4];
+  tile_abt(P, Q, acc);
+  const int tr = threadIdx.x / 16, tc = threadIdx.x % 16;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) A[(long)(r0 + tr + 16 * a) * D + k0 + tc + 16 * c] = acc[a][c];
+}
+
+// A_ij -= L_ik L_jk^T for listed (k, i, j) triples, i >= j
+__global__ void __launch_bounds__(256) syrk_list_kernel(double* __restrict__ A, int D,
+                                                        const int32_t* __restrict__ triples,
+                                                        const int32_t* __restrict__ status) {
+  if (*status) return;
+  const int k = triples[3 * blockIdx.x], ti = triples[3 * blockIdx.x + 1],
+            tj = triples[3 * blockIdx.x + 2];
+  extern __shared__ double smem[];
+  double* Pi = smem;
+  double* Pj = smem + NB * LD;
+  const int k0 = k * NB, ri = ti * NB, rj = tj * NB;
+  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
+    const int r = e / NB, c = e % NB;
+    Pi[r * LD + c] = A[(long)(ri + r) * D + k0 + c];
+    Pj[r * LD + c] = A[(long)(rj + r) * D + k0 + c];
+  }
+  __syncthreads();
+  double acc[4][4];
+  tile_abt(Pi, Pj, acc);
+  const int tr = threadIdx.x / 16, tc = threadIdx.x % 16;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int r = ri + tr + 16 * a, col = rj + tc + 16 * c;
+      if (col <= r) A[(long)r * D + col] -= acc[a][c];
+    }
+}
+
 __global__ void __launch_bounds__(1024) trisolve_kernel(const double* __restrict__ A, int dim, int T,
                                                          const int32_t* __restrict__ env,
                                                          const int32_t* __restrict__ last,
@@ -488,13 +606,177 @@ __global__ void __launch_bounds__(1024) trisolve_kernel(const double* __restrict
 
 using namespace pba;
 
+// Nested dissection of a chain-like (narrow tile band) system.  Returns
+// PBA_OK when solved, 1 when the structure does not qualify (caller falls
+// back to the sequential tiled factorisation), or an error code.
+//
+// The original tile order is cut into P segments separated by w-tile
+// separators (w = tile half-bandwidth), so no segment couples to another.
+// New order: all segments, then all separators.  The right-looking tiled
+// Cholesky of P A P^T then has independent segment steps: step s of every
+// segment of one parity runs in one batched launch (segments of equal
+// parity share no separator, so their trailing updates touch disjoint
+// tiles), after which the separators' Schur complement is factored tile by
+// tile.  Sequential steps: 2 * max segment length + (P - 1) * w instead of T.
+// Each tile update is the same arithmetic as the sequential path, in the
+// order of the new elimination sequence.
+int solve_dissected(const double* H, const double* b, int dim, double lam,
+                    const std::vector<int32_t>& env, const std::vector<int32_t>& last,
+                    const SolveWork& w, double* delta, int32_t* status, cudaStream_t st) {
+  const int T = (int)env.size(), D = T * NB;
+  int band = 0;
+  for (int k = 0; k < T; ++k) band = max(band, last[k] - k);
+  if (band < 1 || band > kMaxBand) return 1;
+  const int P = min(8, T / (4 * band));
+  if (P < 2) return 1;
+  // segments and separators in the original tile order
+  const int seg_total = T - (P - 1) * band;
+  std::vector<int> seg_start(P), seg_len(P);
+  for (int g = 0, pos = 0; g < P; ++g) {
+    seg_len[g] = seg_total / P + (g < seg_total % P ? 1 : 0);
+    seg_start[g] = pos;
+    pos += seg_len[g] + (g < P - 1 ? band : 0);
+  }
+  std::vector<int32_t> n2o, o2n(T);
+  std::vector<int> new_seg(P);
+  for (int g = 0; g < P; ++g) {
+    new_seg[g] = (int)n2o.size();
+    for (int t = 0; t < seg_len[g]; ++t) n2o.push_back(seg_start[g] + t);
+  }
+  const int sep_base = (int)n2o.size();
+  for (int g = 0; g + 1 < P; ++g)
+    for (int t = 0; t < band; ++t) n2o.push_back(seg_start[g] + seg_len[g] + t);
+  if ((int)n2o.size() != T) return 1;
+  for (int i = 0; i < T; ++i) o2n[n2o[i]] = i;
+  // symbolic structure of the permuted matrix (lower tiles) and its fill
+  std::vector<char> S((size_t)T * T, 0);
+  for (int oi = 0; oi < T; ++oi)
+    for (int oj = env[oi]; oj <= oi; ++oj) {
+      const int a = o2n[oi], c = o2n[oj];
+      S[(size_t)max(a, c) * T + min(a, c)] = 1;
+    }
+  std::vector<std::vector<int>> rows(T);
+  for (int k = 0; k < T; ++k) {
+    for (int i = k + 1; i < T; ++i)
+      if (S[(size_t)i * T + k]) rows[k].push_back(i);
+    if ((int)rows[k].size() > 2 * kMaxBand) return 1;
+    for (int x : rows[k])
+      for (int y : rows[k])
+        if (y <= x) S[(size_t)x * T + y] = 1;
+  }
+  // staging: [n2o | tiles | klist | pairs | triples]
+  std::vector<int32_t> tiles, klist, pairs, triples;
+  for (int i = 0; i < T; ++i)
+    for (int j = 0; j <= i; ++j)
+      if (S[(size_t)i * T + j] || i == j) tiles.push_back(i), tiles.push_back(j);
+  struct Launch { int k0, nk, p0, np, t0, nt; };
+  std::vector<Launch> launches;
+  auto add_batch = [&](const std::vector<int>& ks) {
+    Launch L{(int)klist.size(), (int)ks.size(), (int)pairs.size() / 2, 0, (int)triples.size() / 3, 0};
+    for (int k : ks) {
+      klist.push_back(k);
+      for (int i : rows[k]) pairs.push_back(k), pairs.push_back(i);
+      for (size_t a = 0; a < rows[k].size(); ++a)
+        for (size_t c = 0; c <= a; ++c)
+          triples.push_back(k), triples.push_back(rows[k][a]), triples.push_back(rows[k][c]);
+    }
+    L.np = (int)pairs.size() / 2 - L.p0;
+    L.nt = (int)triples.size() / 3 - L.t0;
+    launches.push_back(L);
+  };
+  int lmax = 0;
+  for (int g = 0; g < P; ++g) lmax = max(lmax, seg_len[g]);
+  for (int st_ = 0; st_ < lmax; ++st_)
+    for (int parity = 0; parity < 2; ++parity) {
+      std::vector<int> ks;
+      for (int g = parity; g < P; g += 2)
+        if (st_ < seg_len[g]) ks.push_back(new_seg[g] + st_);
+      if (!ks.empty()) add_batch(ks);
+    }
+  for (int k = sep_base; k < T; ++k) add_batch(std::vector<int>{k});
+  static thread_local std::vector<int32_t> staging;
+  staging.clear();
+  staging.insert(staging.end(), n2o.begin(), n2o.end());
+  const size_t off_tiles = staging.size();
+  staging.insert(staging.end(), tiles.begin(), tiles.end());
+  const size_t off_k = staging.size();
+  staging.insert(staging.end(), klist.begin(), klist.end());
+  const size_t off_p = staging.size();
+  staging.insert(staging.end(), pairs.begin(), pairs.end());
+  const size_t off_t = staging.size();
+  staging.insert(staging.end(), triples.begin(), triples.end());
+  if (staging.size() > list_ints(T)) return 1;
+  const size_t off_nz = staging.size();
+  // tile flags (with fill) and envelope of the permuted matrix for trisolve
+  std::vector<int32_t> envp(T), lastp(T);
+  for (int i = 0; i < T; ++i) {
+    int e = i;
+    for (int j = 0; j <= i; ++j)
+      if (S[(size_t)i * T + j]) { e = j; break; }
+    envp[i] = e;
+  }
+  for (int k = 0; k < T; ++k) {
+    int l = k;
+    for (int i = k + 1; i < T; ++i)
+      if (S[(size_t)i * T + k]) l = i;
+    lastp[k] = l;
+  }
+  for (size_t e = 0; e < (size_t)T * T; ++e) staging.push_back(S[e] ? 1 : 0);
+  for (int i = 0; i < T; ++i) staging[off_nz + (size_t)i * T + i] = 1;
+  staging.insert(staging.end(), envp.begin(), envp.end());
+  staging.insert(staging.end(), lastp.begin(), lastp.end());
+  int32_t* d_lists = w.lists;
+  int32_t* d_env = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(w.nz) +
+                                              align_up((size_t)T * T * sizeof(int32_t), 256));
+  PBA_CUDA_TRY(cudaMemcpyAsync(d_lists, staging.data(), off_nz * sizeof(int32_t),
+                               cudaMemcpyHostToDevice, st));
+  PBA_CUDA_TRY(cudaMemcpyAsync(w.nz, staging.data() + off_nz, (size_t)T * T * sizeof(int32_t),
+                               cudaMemcpyHostToDevice, st));
+  PBA_CUDA_TRY(cudaMemcpyAsync(d_env, staging.data() + off_nz + (size_t)T * T,
+                               2 * T * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  const int32_t* d_n2o = d_lists;
+  damp_copy_perm_kernel<<<(unsigned)(tiles.size() / 2), 256, 0, st>>>(H, dim, lam, D,
+                                                                    d_lists + off_tiles, d_n2o,
+                                                                    w.A);
+  PBA_LAUNCH_CHECK();
+  permute_vec_kernel<<<(D + 255) / 256, 256, 0, st>>>(b, dim, T, d_n2o, w.bp, 1);
+  PBA_LAUNCH_CHECK();
+  const int tile_smem = 2 * NB * LD * sizeof(double);
+  const int reg_smem = tile_smem + (NB / PW - 1) * PW * (PW + 1) * (int)sizeof(double);
+  PBA_CUDA_TRY(cudaFuncSetAttribute(potrf_reg_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, reg_smem));
+  PBA_CUDA_TRY(cudaFuncSetAttribute(panel_list_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));
+  PBA_CUDA_TRY(cudaFuncSetAttribute(syrk_list_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));
+  for (const Launch& L : launches) {
+    potrf_reg_kernel<<<L.nk, 256, reg_smem, st>>>(w.A, D, 0, d_lists + off_k + L.k0, w.Linv,
+                                                  status);
+    PBA_LAUNCH_CHECK();
+    if (L.np) {
+      panel_list_kernel<<<L.np, 256, tile_smem, st>>>(w.A, D, d_lists + off_p + 2 * L.p0,
+                                                      w.Linv, status);
+      PBA_LAUNCH_CHECK();
+    }
+    if (L.nt) {
+      syrk_list_kernel<<<L.nt, 256, tile_smem, st>>>(w.A, D, d_lists + off_t + 3 * L.t0, status);
+      PBA_LAUNCH_CHECK();
+    }
+  }
+  trisolve_kernel<<<1, 1024, 0, st>>>(w.A, D, T, d_env, d_env + T, w.nz, w.Linv, w.bp, w.y, w.xp,
+                                      status);
+  PBA_LAUNCH_CHECK();
+  permute_vec_kernel<<<(D + 255) / 256, 256, 0, st>>>(w.xp, dim, T, d_n2o, delta, 0);
+  PBA_LAUNCH_CHECK();
+  return PBA_OK;
+}
+
 extern "C" size_t pba_solve_work_bytes(int32_t dim) {
   if (dim <= 0) return 0;
-  const size_t T = (dim + NB - 1) / NB;
-  return align_up((size_t)dim * dim * sizeof(double), 256) +
-         align_up(T * NB * NB * sizeof(double), 256) +
-         align_up((size_t)dim * sizeof(double), 256) + align_up(T * T * sizeof(int32_t), 256) +
-         align_up(2 * T * sizeof(int32_t), 256);
+  const size_t T = (dim + NB - 1) / NB, D = T * NB;
+  return align_up(D * D * sizeof(double), 256) + align_up(T * NB * NB * sizeof(double), 256) +
+         3 * align_up(D * sizeof(double), 256) + align_up(list_ints(T) * sizeof(int32_t), 256) +
+         align_up(T * T * sizeof(int32_t), 256) + align_up(2 * T * sizeof(int32_t), 256);
 }
 
 extern "C" int pba_solve_dense(const double* H, const double* b, int32_t dim, double lam,
@@ -518,6 +800,21 @@ extern "C" int pba_solve_dense(const double* H, const double* b, int32_t dim, do
     for (int i = k + 1; i < T; ++i)
       if (env[i] <= k) l = i;
     last[k] = l;
+  }
+  static int potrf_variant = -1;
+  if (potrf_variant < 0) {
+    const char* env = getenv("PBA_POTRF_VARIANT");
+    potrf_variant = env ? atoi(env) : 1;
+  }
+  static int dissect = -1;
+  if (dissect < 0) {
+    const char* env = getenv("PBA_SOLVE_DISSECT");
+    dissect = !(env && env[0] == '0');
+  }
+  if (dissect && potrf_variant == 1) {
+    PBA_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int32_t), st));
+    const int rc = solve_dissected(H, b, dim, lam, env, last, w, delta, status, st);
+    if (rc != 1) return rc;  // 1: structure not suited, the sequential path follows
   }
   int32_t* d_env = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(w.nz) +
                                               align_up((size_t)T * T * sizeof(int32_t), 256));
@@ -544,14 +841,9 @@ extern "C" int pba_solve_dense(const double* H, const double* b, int32_t dim, do
   const int reg_smem = tile_smem + (NB / PW - 1) * PW * (PW + 1) * (int)sizeof(double);
   PBA_CUDA_TRY(cudaFuncSetAttribute(potrf_reg_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, reg_smem));
-  static int potrf_variant = -1;
-  if (potrf_variant < 0) {
-    const char* env = getenv("PBA_POTRF_VARIANT");
-    potrf_variant = env ? atoi(env) : 1;
-  }
   for (int k = 0; k < T; ++k) {
     if (potrf_variant == 1)
-      potrf_reg_kernel<<<1, 256, reg_smem, st>>>(w.A, dim, k, w.Linv, status);
+      potrf_reg_kernel<<<1, 256, reg_smem, st>>>(w.A, dim, k, nullptr, w.Linv, status);
     else
       potrf_inv_kernel<<<1, 1024, tile_smem, st>>>(w.A, dim, k, w.Linv, status);
     PBA_LAUNCH_CHECK();

@@ -276,6 +276,40 @@ def test_dense_cholesky_matches_numpy_solve(dim, band):
         assert np.max(np.abs(x2 - ref)) <= 1e-8 * np.max(np.abs(ref))
 
 
+def _band_env(H):
+    dim = H.shape[0]
+    T = (dim + 63) // 64
+    first = np.array([(np.nonzero(H[r, : r + 1])[0][:1].tolist() or [r])[0] for r in range(dim)])
+    return np.array([first[t * 64: (t + 1) * 64].min() // 64 for t in range(T)], np.int32)
+
+
+@pytest.mark.parametrize("dim,band", [(3000, 40), (2049, 20), (6016, 60), (4000, 90)])
+def test_dissected_cholesky_matches_numpy_solve(dim, band):
+    """Narrow tile bands over many tiles take the nested-dissection path
+    (segments batched, separators last, padded to whole tiles)."""
+    rng = np.random.default_rng(dim + band)
+    A = np.triu(np.tril(rng.normal(size=(dim, dim)), band), -band)
+    H = A @ A.T + 1e-3 * np.eye(dim)
+    b = rng.normal(size=dim)
+    lam = 1e-3
+    ref = np.linalg.solve(H + lam * np.diag(np.diag(H)), -b)
+    env = _band_env(H)
+    T = len(env)
+    assert max(k - e for k, e in enumerate(env)) <= 3 and T >= 24  # qualifies
+    x, st = _dense_solve(H, b, lam, env)
+    assert st == 0
+    assert np.max(np.abs(x - ref)) <= 1e-8 * np.max(np.abs(ref))
+
+
+def test_dissected_cholesky_reports_singular():
+    dim = 3000
+    H = np.eye(dim) + np.diag(np.full(dim - 1, 0.1), -1) + np.diag(np.full(dim - 1, 0.1), 1)
+    H[1700, :] = 0.0
+    H[:, 1700] = 0.0
+    _, st = _dense_solve(H, np.ones(dim), 1e-3, _band_env(H))
+    assert st == 1
+
+
 def test_dense_cholesky_reports_singular():
     H = np.eye(12)
     H[5, 5] = 0.0
