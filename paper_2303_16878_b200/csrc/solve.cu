@@ -48,7 +48,7 @@ constexpr int kMaxBand = 3;  // dissection: widest tile band handled
 // schedule buffer: new->old tile map, structural tiles, tile lists, pairs, triples
 size_t list_ints(size_t T) {
   const size_t B = kMaxBand;
-  return T * (2 + 2 * (2 * B + 1) + 4 * B + 3 * B * (2 * B + 1));
+  return T * (4 + 2 * (2 * B + 1) + 4 * B + 3 * B * (2 * B + 1));
 }
 
 SolveWork carve(void* work, int dim) {
@@ -539,6 +539,69 @@ __global__ void __launch_bounds__(256) syrk_list_kernel(double* __restrict__ A, 
     }
 }
 
+// One forward step of L y = -b on tile row k: y_k = Linv_kk (-b_k - sum_{j<k} L_kj y_j)
+__device__ __forceinline__ void fwd_step(const double* __restrict__ A, int dim, int T, int k,
+                                         const int32_t* __restrict__ env,
+                                         const int32_t* __restrict__ nz,
+                                         const double* __restrict__ Linv,
+                                         const double* __restrict__ b, double* __restrict__ y,
+                                         double* r) {
+  const int tid = threadIdx.x;
+  const int row = tid >> 4, sub = tid & 15;  // 64 rows x 16 lanes
+  const int k0 = k * NB, nk = min(NB, dim - k0);
+  double s = 0.0;
+  if (row < nk) {
+    for (int j = env[k]; j < k; ++j) {
+      if (!nz[k * T + j]) continue;
+      const double* Lr = A + (long)(k0 + row) * dim + j * NB;
+      const double* yj = y + j * NB;
+      for (int c = sub; c < NB; c += 16) s += Lr[c] * yj[c];
+    }
+  }
+#pragma unroll
+  for (int off = 8; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (sub == 0) r[row] = (row < nk) ? -b[k0 + row] - s : 0.0;
+  __syncthreads();
+  const double* Li = Linv + (long)k * NB * NB;
+  double t = 0.0;
+  for (int c = sub; c <= row; c += 16) t += Li[row * NB + c] * r[c];
+#pragma unroll
+  for (int off = 8; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+  if (sub == 0 && row < nk) y[k0 + row] = t;
+  __syncthreads();
+}
+
+// One backward step of L^T x = y on tile row k: x_k = Linv_kk^T (y_k - sum_{i>k} L_ik^T x_i)
+__device__ __forceinline__ void bwd_step(const double* __restrict__ A, int dim, int T, int k,
+                                         const int32_t* __restrict__ last,
+                                         const int32_t* __restrict__ nz,
+                                         const double* __restrict__ Linv,
+                                         const double* __restrict__ y, double* __restrict__ x,
+                                         double* r) {
+  const int tid = threadIdx.x;
+  const int row = tid >> 4, sub = tid & 15;
+  const int k0 = k * NB, nk = min(NB, dim - k0);
+  double s = 0.0;
+  if (row < nk) {
+    for (int i = k + 1; i <= last[k]; ++i) {
+      if (!nz[i * T + k]) continue;
+      const int i0 = i * NB, ni = min(NB, dim - i0);
+      for (int rr = sub; rr < ni; rr += 16) s += A[(long)(i0 + rr) * dim + k0 + row] * x[i0 + rr];
+    }
+  }
+#pragma unroll
+  for (int off = 8; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (sub == 0) r[row] = (row < nk) ? y[k0 + row] - s : 0.0;
+  __syncthreads();
+  const double* Li = Linv + (long)k * NB * NB;
+  double t = 0.0;
+  for (int c = row + sub; c < NB; c += 16) t += Li[c * NB + row] * r[c];
+#pragma unroll
+  for (int off = 8; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+  if (sub == 0 && row < nk) x[k0 + row] = t;
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(1024) trisolve_kernel(const double* __restrict__ A, int dim, int T,
                                                          const int32_t* __restrict__ env,
                                                          const int32_t* __restrict__ last,
@@ -550,54 +613,25 @@ __global__ void __launch_bounds__(1024) trisolve_kernel(const double* __restrict
                                                          const int32_t* __restrict__ status) {
   if (*status) return;
   __shared__ double r[NB];
-  const int tid = threadIdx.x;
-  const int row = tid >> 4, sub = tid & 15;  // 64 rows x 16 lanes
-  // forward: y_k = Linv_kk (-b_k - sum_{j<k} L_kj y_j)
-  for (int k = 0; k < T; ++k) {
-    const int k0 = k * NB, nk = min(NB, dim - k0);
-    double s = 0.0;
-    if (row < nk) {
-      for (int j = env[k]; j < k; ++j) {
-        if (!nz[k * T + j]) continue;
-        const double* Lr = A + (long)(k0 + row) * dim + j * NB;
-        const double* yj = y + j * NB;
-        for (int c = sub; c < NB; c += 16) s += Lr[c] * yj[c];
-      }
-    }
-#pragma unroll
-    for (int off = 8; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if (sub == 0) r[row] = (row < nk) ? -b[k0 + row] - s : 0.0;
-    __syncthreads();
-    const double* Li = Linv + (long)k * NB * NB;
-    double t = 0.0;
-    for (int c = sub; c <= row; c += 16) t += Li[row * NB + c] * r[c];
-#pragma unroll
-    for (int off = 8; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
-    if (sub == 0 && row < nk) y[k0 + row] = t;
-    __syncthreads();
-  }
-  // backward: x_k = Linv_kk^T (y_k - sum_{i>k} L_ik^T x_i)
-  for (int k = T - 1; k >= 0; --k) {
-    const int k0 = k * NB, nk = min(NB, dim - k0);
-    double s = 0.0;
-    if (row < nk) {
-      for (int i = k + 1; i <= last[k]; ++i) {
-        if (!nz[i * T + k]) continue;
-        const int i0 = i * NB, ni = min(NB, dim - i0);
-        for (int rr = sub; rr < ni; rr += 16) s += A[(long)(i0 + rr) * dim + k0 + row] * x[i0 + rr];
-      }
-    }
-#pragma unroll
-    for (int off = 8; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if (sub == 0) r[row] = (row < nk) ? y[k0 + row] - s : 0.0;
-    __syncthreads();
-    const double* Li = Linv + (long)k * NB * NB;
-    double t = 0.0;
-    for (int c = row + sub; c < NB; c += 16) t += Li[c * NB + row] * r[c];
-#pragma unroll
-    for (int off = 8; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
-    if (sub == 0 && row < nk) x[k0 + row] = t;
-    __syncthreads();
+  for (int k = 0; k < T; ++k) fwd_step(A, dim, T, k, env, nz, Linv, b, y, r);
+  for (int k = T - 1; k >= 0; --k) bwd_step(A, dim, T, k, last, nz, Linv, y, x, r);
+}
+
+// Substitution over independent tile ranges (dissection path): CTA c walks
+// tiles [ranges[2c], ranges[2c+1]) forwards (forward != 0) or backwards.
+__global__ void __launch_bounds__(1024) trisolve_range_kernel(
+    const double* __restrict__ A, int dim, int T, const int32_t* __restrict__ env,
+    const int32_t* __restrict__ last, const int32_t* __restrict__ nz,
+    const double* __restrict__ Linv, const double* __restrict__ b, double* __restrict__ y,
+    double* __restrict__ x, const int32_t* __restrict__ ranges, int forward,
+    const int32_t* __restrict__ status) {
+  if (*status) return;
+  __shared__ double r[NB];
+  const int lo = ranges[2 * blockIdx.x], hi = ranges[2 * blockIdx.x + 1];
+  if (forward) {
+    for (int k = lo; k < hi; ++k) fwd_step(A, dim, T, k, env, nz, Linv, b, y, r);
+  } else {
+    for (int k = hi - 1; k >= lo; --k) bwd_step(A, dim, T, k, last, nz, Linv, y, x, r);
   }
 }
 
@@ -705,6 +739,9 @@ int solve_dissected(const double* H, const double* b, int dim, double lam,
   staging.insert(staging.end(), pairs.begin(), pairs.end());
   const size_t off_t = staging.size();
   staging.insert(staging.end(), triples.begin(), triples.end());
+  const size_t off_ranges = staging.size();  // P segment ranges, then the separator range
+  for (int g = 0; g < P; ++g) staging.push_back(new_seg[g]), staging.push_back(new_seg[g] + seg_len[g]);
+  staging.push_back(sep_base), staging.push_back(T);
   if (staging.size() > list_ints(T)) return 1;
   const size_t off_nz = staging.size();
   // tile flags (with fill) and envelope of the permuted matrix for trisolve
@@ -763,8 +800,20 @@ int solve_dissected(const double* H, const double* b, int dim, double lam,
       PBA_LAUNCH_CHECK();
     }
   }
-  trisolve_kernel<<<1, 1024, 0, st>>>(w.A, D, T, d_env, d_env + T, w.nz, w.Linv, w.bp, w.y, w.xp,
-                                      status);
+  // substitutions: segments in parallel, separators after (forward) / before
+  // (backward) them
+  const int32_t* d_ranges = d_lists + off_ranges;
+  trisolve_range_kernel<<<P, 1024, 0, st>>>(w.A, D, T, d_env, d_env + T, w.nz, w.Linv, w.bp, w.y,
+                                            w.xp, d_ranges, 1, status);
+  PBA_LAUNCH_CHECK();
+  trisolve_range_kernel<<<1, 1024, 0, st>>>(w.A, D, T, d_env, d_env + T, w.nz, w.Linv, w.bp, w.y,
+                                            w.xp, d_ranges + 2 * P, 1, status);
+  PBA_LAUNCH_CHECK();
+  trisolve_range_kernel<<<1, 1024, 0, st>>>(w.A, D, T, d_env, d_env + T, w.nz, w.Linv, w.bp, w.y,
+                                            w.xp, d_ranges + 2 * P, 0, status);
+  PBA_LAUNCH_CHECK();
+  trisolve_range_kernel<<<P, 1024, 0, st>>>(w.A, D, T, d_env, d_env + T, w.nz, w.Linv, w.bp, w.y,
+                                            w.xp, d_ranges, 0, status);
   PBA_LAUNCH_CHECK();
   permute_vec_kernel<<<(D + 255) / 256, 256, 0, st>>>(w.xp, dim, T, d_n2o, delta, 0);
   PBA_LAUNCH_CHECK();
