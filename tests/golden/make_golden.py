@@ -201,6 +201,44 @@ def pyramid_case():
     print("pyramid", (OUT / "pyramid.npz").stat().st_size, "bytes")
 
 
+def behaviour_case():
+    """Raw renders (intensity, depth) and seeded perturbations for the
+    reference's behavioural solver tests (test_solver.py:374-563), so the
+    same scenarios run on the GPU path (pyramids are rebuilt with the
+    package's bit-exact build_pyramid)."""
+    from rigs import LIDAR_EXTRINSICS, RGBD_EXTRINSICS
+
+    d = {}
+    cam_r, cam_l = rgbd_cam(), lidar_cam()
+    d["cam_rgbd"], d["cam_lidar"] = cam_row(cam_r), cam_row(cam_l)
+    room = box_room_scene()
+
+    def view(tag, cam, pose, ext=None):
+        off = ext.offset if ext is not None else Pose.identity()
+        r = render_view(room, cam, pose.compose(off))
+        d[f"{tag}_I"], d[f"{tag}_D"] = r.intensity, r.depth
+
+    view("zero", cam_r, Pose.identity())
+    view("selfalign", cam_r, Pose(np.eye(3), [-0.5, -0.3, -0.8]))
+    view("optimal", cam_r, Pose(np.eye(3), [-0.4, 0.2, -0.5]))
+    gt_f = Pose(np.eye(3), [-0.4, -0.2, -0.6])
+    view("fusion_rgbd", cam_r, gt_f, RGBD_EXTRINSICS)
+    view("fusion_lidar", cam_l, gt_f, LIDAR_EXTRINSICS)
+    loop = loop_trajectory(5)
+    for k, p in enumerate(loop.poses):
+        view(f"loop{k}", cam_r, p)
+    d["loop_gt"] = pose_rows(loop.poses)
+    gt_s = Pose(np.eye(3), [-0.5, -0.3, -0.8])
+    d["selfalign_bad"] = pose_rows([boxplus(gt_s, seeded_perturbation(np.random.default_rng(47), 0.1, 0.0))])
+    d["monotone_bad"] = pose_rows([boxplus(gt_s, seeded_perturbation(np.random.default_rng(48), 0.12, 0.08))])
+    d["coupled_bad"] = pose_rows([boxplus(gt_f, seeded_perturbation(np.random.default_rng(4242), 0.25, 0.3))])
+    rng = np.random.default_rng(51)
+    d["loop_guess"] = pose_rows([loop.poses[0]] + [
+        boxplus(p, seeded_perturbation(rng, 0.04, math.radians(1.5))) for p in loop.poses[1:]])
+    np.savez_compressed(OUT / "behaviour.npz", **d)
+    print("behaviour", (OUT / "behaviour.npz").stat().st_size, "bytes")
+
+
 def evaluation_case():
     """associate / horn_align / evaluate_ate (evaluation.py:48-122) on
     seeded trajectories: timestamp jitter, dropped poses, a rigid offset and
@@ -285,3 +323,4 @@ if __name__ == "__main__":
     pyramid_case()
     dataset_case()
     evaluation_case()
+    behaviour_case()

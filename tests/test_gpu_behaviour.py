@@ -1,0 +1,125 @@
+"""The reference's behavioural solver tests (pkg/tests/test_solver.py:374-563)
+run on the GPU path: same scenes (raw renders from the reference renderer in
+tests/golden/behaviour.npz, pyramids rebuilt with the bit-exact host
+build_pyramid), same seeded perturbations, same assertions."""
+import math
+
+import numpy as np
+import pytest
+
+import paper_2303_16878_b200 as P
+from paper_2303_16878_b200.camera import Intrinsics
+from paper_2303_16878_b200.evaluation import Trajectory
+from tests.fixtures import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+RGBD_EXT = P.SensorExtrinsics(P.Pose(np.eye(3), [0.0, 0.0, 0.1]))
+LIDAR_EXT = P.SensorExtrinsics(P.Pose(np.eye(3), [0.0, 0.0, -0.05]))
+
+
+@pytest.fixture(scope="module")
+def z():
+    return np.load(GOLDEN / "behaviour.npz")
+
+
+def _cam(row):
+    model = P.PINHOLE if row[6] == 0 else P.SPHERICAL
+    return Intrinsics(row[0], row[1], row[2], row[3], int(row[4]), int(row[5]), model, row[7],
+                      row[8])
+
+
+def _pyr(z, tag, cam_key="cam_rgbd"):
+    return P.build_pyramid(z[f"{tag}_I"], z[f"{tag}_D"], _cam(z[cam_key]), (0.125, 0.25, 0.5))
+
+
+def _selfalign(pyr, gt, bad, sensor="sensor0", ext=None):
+    nodes = [P.FrameNode(0, gt, pyr, 0.0, sensor), P.FrameNode(1, bad, pyr, 0.1, sensor)]
+    exts = {sensor: ext} if ext is not None else {}
+    return P.BAProblem(P.MatchGraph(nodes, [P.Edge(0, 1, P.COVISIBILITY)]), exts)
+
+
+def _err(a, b):
+    rel = P.relative(a, b)
+    return float(np.linalg.norm(rel.translation)), P.rotation_angle(rel.rotation)
+
+
+def test_zero_perturbation_terminates_immediately(z):
+    I = P.Pose.identity()
+    prob = _selfalign(_pyr(z, "zero"), I, I)
+    poses, records = P.solve_level(prob, [I, I], 0)
+    assert len(records) <= 2
+    assert np.allclose(poses[1].matrix(), np.eye(4), atol=1e-9)
+
+
+def test_two_frame_selfalign_recovers_pose(z):
+    gt = P.Pose(np.eye(3), [-0.5, -0.3, -0.8])
+    bad = P.Pose.from_row(z["selfalign_bad"][0])
+    res = P.solve_hierarchical(_selfalign(_pyr(z, "selfalign"), gt, bad))
+    et, er = _err(res.poses[1], gt)
+    assert et < 1e-4 and er < 1e-4
+
+
+def test_accepted_error_trace_is_monotone(z):
+    gt = P.Pose(np.eye(3), [-0.5, -0.3, -0.8])
+    bad = P.Pose.from_row(z["monotone_bad"][0])
+    res = P.solve_hierarchical(_selfalign(_pyr(z, "selfalign"), gt, bad))
+    for level in set(r.level for r in res.records):
+        errors = [r.error for r in res.records if r.level == level]
+        assert all(b <= a + 1e-15 for a, b in zip(errors, errors[1:]))
+
+
+def test_already_optimal_hierarchical_is_identity_operation(z):
+    gt = P.Pose(np.eye(3), [-0.4, 0.2, -0.5])
+    res = P.solve_hierarchical(_selfalign(_pyr(z, "optimal"), gt, gt))
+    assert np.allclose(res.poses[1].matrix(), gt.matrix(), atol=1e-9)
+
+
+def test_small_recovery_improves_ate(z):
+    gt_poses = [P.Pose.from_row(r) for r in z["loop_gt"]]
+    guess = [P.Pose.from_row(r) for r in z["loop_guess"]]
+    stamps = np.arange(5) * 0.1
+    nodes = [P.FrameNode(k, guess[k], _pyr(z, f"loop{k}"), float(stamps[k])) for k in range(5)]
+    res = P.solve_hierarchical(P.BAProblem(P.build_graph(nodes)))
+    gt_t = Trajectory(stamps, gt_poses)
+    assert P.ate_rmse(Trajectory(stamps, res.poses), gt_t) < 0.5 * P.ate_rmse(
+        Trajectory(stamps, guess), gt_t)
+
+
+def _fusion(z, gt, bad):
+    prob_r = _selfalign(_pyr(z, "fusion_rgbd"), gt, bad, "rgbd", RGBD_EXT)
+    prob_l = _selfalign(_pyr(z, "fusion_lidar", "cam_lidar"), gt, bad, "lidar", LIDAR_EXT)
+    return prob_r, prob_l
+
+
+def test_fusion_zero_perturbation_is_identity_both_modes(z):
+    gt = P.Pose(np.eye(3), [-0.4, -0.2, -0.6])
+    prob_r, prob_l = _fusion(z, gt, gt)
+    for mode in (P.COUPLED, P.CONSECUTIVE):
+        res = (P.solve_fusion(prob_r, prob_l, mode) if mode == P.COUPLED
+               else P.solve_fusion(prob_l, prob_r, mode))
+        et, er = _err(res.poses[1], gt)
+        assert et < 1e-6 and er < 1e-6
+
+
+def test_fusion_rejects_mismatched_lengths(z):
+    gt = P.Pose(np.eye(3), [-0.4, -0.2, -0.6])
+    prob_r, prob_l = _fusion(z, gt, gt)
+    prob_l.graph.nodes.append(prob_l.graph.nodes[1])
+    with pytest.raises(P.FusionConfigError):
+        P.solve_fusion(prob_r, prob_l, P.COUPLED)
+
+
+def test_coupled_converges_where_pinhole_fails(z):
+    gt = P.Pose(np.eye(3), [-0.4, -0.2, -0.6])
+    bad = P.Pose.from_row(z["coupled_bad"][0])
+    prob_r, prob_l = _fusion(z, gt, bad)
+    res_pin = P.solve_hierarchical(prob_r)
+    res_cpl = P.solve_fusion(prob_r, prob_l, P.COUPLED)
+    et, er = _err(res_pin.poses[1], gt)
+    assert not (et < 1e-3 and er < 1e-3)
+    et, er = _err(res_cpl.poses[1], gt)
+    assert et < 1e-3 and er < 1e-3
+    assert math.isfinite(res_cpl.records[-1].error)
