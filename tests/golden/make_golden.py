@@ -239,6 +239,36 @@ def behaviour_case():
     print("behaviour", (OUT / "behaviour.npz").stat().st_size, "bytes")
 
 
+def acceptance_case():
+    """Inputs of the reference's acceptance criteria (test_acceptance.py:60-255):
+    the 10-pose recovery case (loop_trajectory(10), perturb_trajectory seed 11),
+    the hierarchical-benefit case (seed 3) and the 5x5 fusion-ordering grid
+    (seed 42); renders are raw intensity/depth."""
+    from photoba.synthetic import perturb_trajectory
+
+    d = {}
+    cam = rgbd_cam()
+    room = box_room_scene()
+    gt = loop_trajectory(10)
+    for k, p in enumerate(gt.poses):
+        r = render_view(room, cam, p)
+        d[f"loop10_{k}_I"], d[f"loop10_{k}_D"] = r.intensity, r.depth
+    d["loop10_gt"] = pose_rows(gt.poses)
+    d["loop10_stamps"] = gt.timestamps
+    d["loop10_guess"] = pose_rows(perturb_trajectory(gt, 0.05, math.radians(2.0), seed=11).poses)
+    rng = np.random.default_rng(3)
+    d["benefit_bad2"] = pose_rows([boxplus(gt.poses[2], seeded_perturbation(rng, 0.22, 0.22))])
+    gt_f = Pose(np.eye(3), [-0.4, -0.2, -0.6])
+    rng = np.random.default_rng(42)
+    bad = []
+    for r_mag in np.linspace(0.0, 0.3, 5):
+        for t_mag in np.linspace(0.0, 0.3, 5):
+            bad.append(boxplus(gt_f, seeded_perturbation(rng, t_mag, r_mag)))
+    d["fusion_grid_bad"] = pose_rows(bad)
+    np.savez_compressed(OUT / "acceptance.npz", **d)
+    print("acceptance", (OUT / "acceptance.npz").stat().st_size, "bytes")
+
+
 def evaluation_case():
     """associate / horn_align / evaluate_ate (evaluation.py:48-122) on
     seeded trajectories: timestamp jitter, dropped poses, a rigid offset and
@@ -324,3 +354,4 @@ if __name__ == "__main__":
     dataset_case()
     evaluation_case()
     behaviour_case()
+    acceptance_case()
