@@ -189,6 +189,9 @@ int pba_sum_totals(const double* records, int32_t n_pairs, double* totals, void*
  * inputs (not modified).  tile_env: optional host array of ceil(dim/64)
  * ints, tile_env[i] = first tile column that may be non-zero in tile row i
  * (the matrix envelope; Cholesky fill-in never leaves it) — NULL means dense.
+ * Narrow envelopes over many tiles (chain-like pose graphs) are solved by
+ * nested dissection (independent segments batched, separators last); other
+ * matrices by the sequential tiled factorisation.
  * work: device, pba_solve_work_bytes(dim) bytes.  delta: device output.
  * status: device int32 written 0 on success, 1 when the damped matrix is
  * not positive definite (the reference's LinAlgError). */
