@@ -299,6 +299,15 @@ def cpu_baseline(problems, guess, level, total_pp, target_seconds=12.0, threads=
     lp.apply_step(rows, gens, np.zeros(dim))
     t_upd = time.perf_counter() - t0
     t_iter = t_lin_total + t_solve + t_upd
+    # one-thread rate on a small sample (BASELINE.md asks for T = 1 and T = all)
+    prob0 = problems[0]
+    k1 = min(2, len(prob0.graph.edges))
+    lp1 = O.OracleLevel([sub_problem(prob0, k1)], level, cfg)
+    pp1 = valid_pixel_pairs(sub_problem(prob0, k1), level)
+    t0 = time.perf_counter()
+    lp1.records(rows, True, 1)
+    per_px_1 = (time.perf_counter() - t0) / max(pp1, 1)
+    t_iter_1 = per_px_1 * total_pp + t_solve + t_upd
     return {
         "value": total_pp / t_iter,
         "unit": "pixel-pairs/s",
@@ -308,6 +317,8 @@ def cpu_baseline(problems, guess, level, total_pp, target_seconds=12.0, threads=
                    f", extrapolated by pixel count to {total_pp}; + full np.linalg.solve dim "
                    f"{dim} ({t_solve:.2f} s) + apply_step ({t_upd * 1e3:.1f} ms)"),
         "gn_iteration_ms_extrapolated": t_iter * 1e3,
+        "value_1_thread": total_pp / t_iter_1,
+        "sample_1_thread": f"first {k1} pairs ({pp1} pixel-pairs) on one thread, extrapolated",
     }
 
 
