@@ -28,8 +28,10 @@
 //
 // Work decomposition: one CTA per chunk of `chunk_pixels` consecutive source
 // pixels of one pair (row-major over the strided source grid).  A thread
-// walks pixels tid, tid+256, ... so a warp reads 32 consecutive source
-// texels and samples a compact destination footprint.  Per-thread sums are
+// walks pixels tid, tid+128, ... (128-thread CTAs, 3 per SM at 168
+// registers) so a warp reads 32 consecutive source texels and samples a
+// compact destination footprint.  Texels are the plane layout of
+// pba_common.cuh (16-byte pairs, plane-major).  Per-thread sums are
 // reduced by a fixed warp-shuffle tree and a fixed cross-warp order into one
 // 32-double partial per chunk; a finalisation kernel sums the chunk partials
 // of each pair in chunk order and expands them into the 92-double record.
@@ -359,9 +361,9 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
   int gr = (first + (int)threadIdx.x) / gw;       // strided-grid row / column of
   int gcol = first + (int)threadIdx.x - gr * gw;  // this thread's current pixel
   // The source texel of the next pixel is always in flight one iteration
-  // ahead: (I, D) and (nz, mask) words, 2 x 16 B.  Masks come from the texel
-  // lines themselves, so a pixel costs two dependent L2 round trips (source
-  // texel, destination texels) instead of four.
+  // ahead: its (I, D) and (nz, mask) pairs, 2 x 16 B.  Masks come from the
+  // texel planes themselves (not the separate mask plane), so a pixel costs
+  // two dependent round trips (source texel, destination texels), not four.
   double2 nx0 = make_double2(0.0, 0.0), nx2 = make_double2(0.0, 0.0);
   if (first + (int)threadIdx.x < last) {
     const double2* t = S.src_tex + gr * stride * sW + gcol * stride;
