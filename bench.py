@@ -55,8 +55,9 @@ CONFIGS = {
                factors=(1,), max_translation=1.0),
     "c2": dict(desc="synthetic LiDAR spherical 64x1024 (HDL-64), 100 scans, 3 levels",
                kind="hdl64", n=100, spacing=0.1, factors=(4, 2, 1), max_translation=1.0),
-    "c3": dict(desc="synthetic RGB-D pinhole 640x480 (TUM-shaped), 500 frames, 3 levels",
-               kind="tum", n=500, spacing=0.05, factors=(4, 2, 1), max_translation=1.0),
+    "c3": dict(desc="synthetic RGB-D pinhole 640x480 (TUM-shaped), 500 frames, 3 levels, "
+                    "LM with block-Jacobi PCG", kind="tum", n=500, spacing=0.05,
+               factors=(4, 2, 1), max_translation=1.0, solver="pcg"),
     "c4": dict(desc="synthetic OS0-128 128x1024, 1000 scans, 2 km corridor, 3 levels, ~20k pairs",
                kind="os0", n=1000, spacing=2.0, factors=(4, 2, 1), max_translation=40.0),
     "c5": dict(desc="joint LiDAR+RGB-D coupled BA: 500 platform poses x (OS0-128 128x1024 + "
@@ -348,7 +349,8 @@ def run_ours(args):
     if len(problems) > 1 and (world > 1 or os.environ.get("PBA_FORCE_SHARDED") == "1"):
         raise SystemExit("fused (multi-sensor) configs are benchmarked on one GPU")
     level = meta["level"]
-    cfg = P.SolverConfig()
+    solver = args.solver or CONFIGS[args.config].get("solver", "cholesky")
+    cfg = P.SolverConfig(linear_solver=solver)
     store = FrameStore(device)
     group = D.current_group()
     backend = D.make_level(problems, level, cfg, store, group)
@@ -407,6 +409,10 @@ def run_ours(args):
     solve_ms = [a.elapsed_time(b) for a, b in (local_level.solve_events or [])]
     local_level.kernel_events = None
     local_level.solve_events = None
+    pcg_info = None
+    if getattr(local_level, "pcg", False):
+        it, relres, conv = local_level.pcg_info.cpu().tolist()
+        pcg_info = {"iterations": int(it), "rel_residual": relres, "converged": bool(conv)}
     t = torch.tensor([elapsed_ms], dtype=torch.float64, device=device)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -489,6 +495,7 @@ def run_ours(args):
             "l2": "inputs larger than L2: %.1f GB of resident texels" % (store.texel_bytes() / 1e9),
             "precision": "fp64 throughout (geometry, residuals, Jacobians, H/b/cost sums)",
             "gn_iteration_ms": ms_per_step,
+            "linear_solver": solver,
             "setup_seconds": round(t_setup, 2),
             "graph_seconds": round(meta["graph_seconds"], 2),
             "initial_cost": cost0,
@@ -506,6 +513,7 @@ def run_ours(args):
             "linearize_ms": lin_avg_ms,
             "linearize_share_of_step": lin_avg_ms / ms_per_step,
             "solve_ms": statistics.mean(solve_ms) if solve_ms else None,
+            "pcg_last_solve": pcg_info,
             "algorithmic_bytes_per_launch": shard_pp * BYTES_PER_PIXEL_PAIR,
         },
         "compute": compute_roofline(counts[args.warmup:args.warmup + args.steps], lin_avg_ms)
@@ -585,6 +593,8 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--frames", type=int, default=None, help="override the frame count")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--solver", default=None, choices=["cholesky", "pcg"],
+                    help="damped-system solver (default: pcg for c3, cholesky otherwise)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=4.0)
     args = ap.parse_args()

@@ -200,6 +200,22 @@ int pba_solve_dense(const double* H, const double* b, int32_t dim, double lam,
                     const int32_t* tile_env, void* work, double* delta, int32_t* status,
                     void* stream);
 
+/* ---- the same system by block-Jacobi PCG (App. C c3: "LM with block-Jacobi
+ * PCG"); replaces np.linalg.solve at solver.py:510-512 by an iterative solve.
+ * One cooperative kernel.  H: the assembled dense matrix (n_free 6x6 block
+ * rows, dim = 6 n_free, full symmetric storage as pba_assemble writes it).
+ * row_ptr (n_free+1) / cols: device block-row CSR of the structurally
+ * non-zero blocks (diagonal included), cols ascending per row.  Stops when
+ * ||r|| <= tol ||b|| or after max_iter iterations (the iterate is then
+ * returned as an inexact LM step).  work: pba_pcg_work_bytes(n_free) bytes.
+ * status: 0 ok, 1 when a damped diagonal block or the system is not
+ * positive definite.  info (device, 3 doubles): iterations, final relative
+ * residual, converged flag. */
+size_t pba_pcg_work_bytes(int32_t n_free);
+int pba_solve_pcg(const double* H, const double* b, int32_t n_free, double lam,
+                  const int32_t* row_ptr, const int32_t* cols, int32_t max_iter, double tol,
+                  void* work, double* delta, int32_t* status, double* info, void* stream);
+
 /* ---- pose update: _LevelProblem.apply_step (solver.py:451-460) --------
  * poses_out[k] = poses_in[k] * exp(delta[slot_k]) for every non-gauge pose
  * (geometry.py:202-219), in fp64.  generation (device int32, n_poses) is

@@ -19,7 +19,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OUT_DIR = PKG / "_lib"
 LIB = OUT_DIR / "libpba_b200.so"
-SOURCES = ["capi.cu", "texels.cu", "linearize.cu", "assemble.cu", "solve.cu", "update.cu",
+SOURCES = ["capi.cu", "texels.cu", "linearize.cu", "assemble.cu", "solve.cu", "pcg.cu", "update.cu",
            "overlap.cu", "pyramid.cu", "rasters.cu"]
 GENCODE = "-gencode=arch=compute_100a,code=sm_100a"
 

@@ -59,6 +59,12 @@ class SolverConfig:
     occlusion_depth_tolerance: float = 0.05
     pixel_stride: int = 1
     threads: int = 1  # accepted for API compatibility; the GPU path ignores it
+    # B200 extension (App. C c3): "cholesky" solves the damped system exactly
+    # like the reference's np.linalg.solve; "pcg" uses block-Jacobi PCG to
+    # ||r|| <= pcg_tolerance * ||b|| (or pcg_max_iterations, an inexact step).
+    linear_solver: str = "cholesky"
+    pcg_max_iterations: int = 2000
+    pcg_tolerance: float = 1e-12
 
     def __post_init__(self) -> None:
         positive = (self.huber_delta_intensity, self.huber_delta_depth, self.huber_delta_normal,
@@ -69,6 +75,10 @@ class SolverConfig:
             raise ValueError("termination_rel_decrease must lie in (0, 1)")
         if self.pixel_stride < 1 or min(self.max_iterations_per_level) < 1:
             raise ValueError("strides and iteration caps must be >= 1")
+        if self.linear_solver not in ("cholesky", "pcg"):
+            raise ValueError("linear_solver must be 'cholesky' or 'pcg'")
+        if self.pcg_max_iterations < 1 or not self.pcg_tolerance >= 0.0:
+            raise ValueError("pcg_max_iterations must be >= 1 and pcg_tolerance >= 0")
 
     def omega_diagonal(self) -> np.ndarray:
         return np.array([self.omega_intensity, self.omega_depth, *self.omega_normal], dtype=float)

@@ -51,6 +51,23 @@ def chunk_pixels_for(total_pixels: int) -> int:
     return THREADS_PER_CHUNK * ppt
 
 
+def block_rows(slot_of_pose, pose_i, pose_j):
+    """Block-row CSR (row_ptr, cols) of the damped normal matrix's non-zero
+    6x6 blocks: the diagonal plus one block per pair of free poses that share
+    an edge, columns ascending (the PCG mat-vec order)."""
+    n_free = int((slot_of_pose >= 0).sum())
+    si = slot_of_pose[pose_i]
+    sj = slot_of_pose[pose_j]
+    both = (si >= 0) & (sj >= 0)
+    r = np.concatenate([np.arange(n_free), si[both], sj[both]]).astype(np.int64)
+    c = np.concatenate([np.arange(n_free), sj[both], si[both]]).astype(np.int64)
+    key = np.unique(r * max(1, n_free) + c)
+    rows, cols = key // max(1, n_free), key % max(1, n_free)
+    row_ptr = np.zeros(n_free + 1, dtype=np.int32)
+    np.add.at(row_ptr, rows + 1, 1)
+    return np.cumsum(row_ptr).astype(np.int32), cols.astype(np.int32)
+
+
 def tile_envelope(slot_of_pose, pose_i, pose_j, dim, tile=64) -> np.ndarray:
     """First possibly non-zero 64-wide tile column of every tile row of the
     damped normal matrix: the envelope of its block sparsity (diagonal
@@ -284,10 +301,18 @@ class DeviceLevel:
         self.H = [torch.zeros((d, d), dtype=torch.float64, device=dev) for _ in range(2)]
         self.b = [torch.zeros(d, dtype=torch.float64, device=dev) for _ in range(2)]
         self.totals = [torch.zeros(2, dtype=torch.float64, device=dev) for _ in range(2)]
-        self.work = torch.empty(max(8, int(lib.pba_solve_work_bytes(d))), dtype=torch.uint8,
-                                device=dev)
+        self.pcg = self.cfg.linear_solver == "pcg" and self.n_free > 0
+        if not self.pcg:  # the Cholesky workspace (D x D) is not needed by PCG
+            self.work = torch.empty(max(8, int(lib.pba_solve_work_bytes(d))), dtype=torch.uint8,
+                                    device=dev)
         self.delta = torch.zeros(d, dtype=torch.float64, device=dev)
         self.tile_env = tile_envelope(slot, self.pose_i, self.pose_j, self.dim)
+        if self.pcg:
+            row_ptr, cols = block_rows(slot, self.pose_i, self.pose_j)
+            self.pcg_rows = [t(row_ptr), t(cols)]
+            self.pcg_work = torch.empty(max(8, int(lib.pba_pcg_work_bytes(self.n_free))),
+                                        dtype=torch.uint8, device=dev)
+            self.pcg_info = torch.zeros(3, dtype=torch.float64, device=dev)
         self.has_solver = True
 
     # ---- primitive steps -----------------------------------------------------
@@ -328,11 +353,21 @@ class DeviceLevel:
         if ev is not None:
             e0 = torch.cuda.Event(enable_timing=True)
             e0.record(torch.cuda.current_stream(self.device))
-        N.check(self.lib.pba_solve_dense(self.H[which].data_ptr(), self.b[which].data_ptr(),
-                                         self.dim, float(lam), self.tile_env.ctypes.data,
-                                         self.work.data_ptr(),
-                                         self.delta.data_ptr(), status_ptr,
-                                         _stream_ptr(self.device)), "pba_solve_dense")
+        if self.pcg:
+            rp, cols = self.pcg_rows
+            N.check(self.lib.pba_solve_pcg(self.H[which].data_ptr(), self.b[which].data_ptr(),
+                                           self.n_free, float(lam), rp.data_ptr(), cols.data_ptr(),
+                                           int(self.cfg.pcg_max_iterations),
+                                           float(self.cfg.pcg_tolerance),
+                                           self.pcg_work.data_ptr(), self.delta.data_ptr(),
+                                           status_ptr, self.pcg_info.data_ptr(),
+                                           _stream_ptr(self.device)), "pba_solve_pcg")
+        else:
+            N.check(self.lib.pba_solve_dense(self.H[which].data_ptr(), self.b[which].data_ptr(),
+                                             self.dim, float(lam), self.tile_env.ctypes.data,
+                                             self.work.data_ptr(),
+                                             self.delta.data_ptr(), status_ptr,
+                                             _stream_ptr(self.device)), "pba_solve_dense")
         if ev is not None:
             e1 = torch.cuda.Event(enable_timing=True)
             e1.record(torch.cuda.current_stream(self.device))

@@ -33,7 +33,8 @@ EXPORTED = (
     "pba_kernel_launches",
     "pba_build_texels_scratch_bytes", "pba_build_texels", "pba_plan_chunks", "pba_linearize",
     "pba_plan_assembly", "pba_assemble", "pba_sum_totals", "pba_solve_work_bytes",
-    "pba_solve_dense", "pba_apply_step", "pba_overlap_counts", "pba_normals_scratch_bytes",
+    "pba_solve_dense", "pba_pcg_work_bytes", "pba_solve_pcg", "pba_apply_step",
+    "pba_overlap_counts", "pba_normals_scratch_bytes",
     "pba_estimate_normals", "pba_downscale_cues", "pba_decode_raster", "pba_atan2_batch",
     "pba_diag_section_cycles",
 )
@@ -95,6 +96,9 @@ _SIGNATURES = {
     "pba_sum_totals": (ctypes.c_int, [_vp, _i32, _vp, _vp]),
     "pba_solve_work_bytes": (_sz, [_i32]),
     "pba_solve_dense": (ctypes.c_int, [_vp, _vp, _i32, _dbl, _vp, _vp, _vp, _vp, _vp]),
+    "pba_pcg_work_bytes": (_sz, [_i32]),
+    "pba_solve_pcg": (ctypes.c_int, [_vp, _vp, _i32, _dbl, _vp, _vp, _i32, _dbl, _vp, _vp, _vp,
+                                     _vp, _vp]),
     "pba_apply_step": (ctypes.c_int, [_vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp]),
     "pba_atan2_batch": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp]),
     "pba_diag_section_cycles": (ctypes.c_int, [_vp, _vp, _i32]),

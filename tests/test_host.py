@@ -121,6 +121,30 @@ def test_solver_config_validation_and_defaults():
         P.SolverConfig(termination_rel_decrease=1.0)
     with pytest.raises(ValueError):
         P.SolverConfig(pixel_stride=0)
+    assert cfg.linear_solver == "cholesky"
+    with pytest.raises(ValueError):
+        P.SolverConfig(linear_solver="lu")
+    with pytest.raises(ValueError):
+        P.SolverConfig(linear_solver="pcg", pcg_max_iterations=0)
+
+
+def test_pcg_block_rows_pattern():
+    from paper_2303_16878_b200.device import block_rows
+
+    rng = np.random.default_rng(2)
+    n = 30
+    slot = np.array([-1 if k == 4 else k - (k > 4) for k in range(n)], np.int32)
+    pi = rng.integers(0, n, 200).astype(np.int32)
+    pj = (pi + rng.integers(1, n, 200)) % n
+    pj = pj.astype(np.int32)
+    row_ptr, cols = block_rows(slot, pi, pj)
+    dense = np.eye(n - 1, dtype=bool)
+    for a, b in zip(slot[pi], slot[pj]):
+        if a >= 0 and b >= 0:
+            dense[a, b] = dense[b, a] = True
+    for r in range(n - 1):
+        got = cols[row_ptr[r]: row_ptr[r + 1]]
+        assert list(got) == list(np.nonzero(dense[r])[0])  # ascending, diagonal included
 
 
 def test_check_connectivity_names_stranded_pose():
