@@ -301,7 +301,8 @@ class DeviceLevel:
         self.H = [torch.zeros((d, d), dtype=torch.float64, device=dev) for _ in range(2)]
         self.b = [torch.zeros(d, dtype=torch.float64, device=dev) for _ in range(2)]
         self.totals = [torch.zeros(2, dtype=torch.float64, device=dev) for _ in range(2)]
-        self.pcg = self.cfg.linear_solver == "pcg" and self.n_free > 0
+        # getattr: a reference photoba SolverConfig (no B200 fields) is accepted as-is
+        self.pcg = getattr(self.cfg, "linear_solver", "cholesky") == "pcg" and self.n_free > 0
         if not self.pcg:  # the Cholesky workspace (D x D) is not needed by PCG
             self.work = torch.empty(max(8, int(lib.pba_solve_work_bytes(d))), dtype=torch.uint8,
                                     device=dev)
@@ -357,8 +358,8 @@ class DeviceLevel:
             rp, cols = self.pcg_rows
             N.check(self.lib.pba_solve_pcg(self.H[which].data_ptr(), self.b[which].data_ptr(),
                                            self.n_free, float(lam), rp.data_ptr(), cols.data_ptr(),
-                                           int(self.cfg.pcg_max_iterations),
-                                           float(self.cfg.pcg_tolerance),
+                                           int(getattr(self.cfg, "pcg_max_iterations", 2000)),
+                                           float(getattr(self.cfg, "pcg_tolerance", 1e-12)),
                                            self.pcg_work.data_ptr(), self.delta.data_ptr(),
                                            status_ptr, self.pcg_info.data_ptr(),
                                            _stream_ptr(self.device)), "pba_solve_pcg")

@@ -122,3 +122,19 @@ def test_pcg_config1_trace_matches_oracle():
     er, et = _pose_err(np.stack([p.as_row() for p in res.poses]), final_o)
     assert er <= 1e-5 and et <= 1e-5
     assert math.isfinite(res.records[-1].error)
+
+
+def test_reference_style_config_without_b200_fields():
+    """A config object with only the reference SolverConfig fields (as
+    photoba.solver.SolverConfig has) still solves, with the exact solver."""
+    import dataclasses
+    import types
+
+    extra = {"linear_solver", "pcg_max_iterations", "pcg_tolerance"}
+    ref_cfg = types.SimpleNamespace(**{f.name: getattr(P.SolverConfig(), f.name)
+                                       for f in dataclasses.fields(P.SolverConfig)
+                                       if f.name not in extra})
+    d = F.load(CASES[0])
+    prob, _ = F.single_problem(d)
+    res = P.solve_hierarchical(prob, ref_cfg)
+    _check_trace(res.records, d["trace"])
