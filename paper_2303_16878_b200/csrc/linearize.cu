@@ -326,7 +326,8 @@ __device__ unsigned long long g_sect_count[8];
 template <bool kJac, int kT, int kMinBlocks, int kProbe = 0>
 __global__ void __launch_bounds__(kT, kMinBlocks)
     linearize_kernel(const pba_frame* __restrict__ frames, const pba_pair* __restrict__ pairs,
-                     const int32_t* __restrict__ chunk_table, int chunk_pixels,
+                     const int32_t* __restrict__ chunk_table,
+                     const int32_t* __restrict__ pair_chunk_offsets, int chunk_pixels,
                      const double* __restrict__ poses, const double* __restrict__ exts,
                      pba_config cfg, double* __restrict__ partials) {
   __shared__ PairSetup S;
@@ -669,7 +670,10 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     double s = 0.0;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) s += red[w][threadIdx.x];
-    partials[chunk * kPart + threadIdx.x] = s;
+    // slot of this chunk in its pair's range (the launch order of the chunk
+    // table is free; the per-pair sums always run in chunk order)
+    const long slot = pair_chunk_offsets[pair] + first / chunk_pixels;
+    partials[slot * kPart + threadIdx.x] = s;
   }
 }
 
@@ -826,7 +830,7 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
     }
     const unsigned grid = (unsigned)n_chunks;
 #define PBA_LAUNCH_LIN(J, T, M) \
-  linearize_kernel<J, T, M><<<grid, T, 0, st>>>(frames, pairs, chunk_table, chunk_pixels, poses, extrinsics, *cfg, partials)
+  linearize_kernel<J, T, M><<<grid, T, 0, st>>>(frames, pairs, chunk_table, pair_chunk_offsets, chunk_pixels, poses, extrinsics, *cfg, partials)
     if (want_jacobians) {
       switch (variant) {
         case 1: PBA_LAUNCH_LIN(true, 256, 1); break;
@@ -834,22 +838,22 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
         case 5: PBA_LAUNCH_LIN(true, 512, 1); break;
         case 2: PBA_LAUNCH_LIN(true, 256, 2); break;
         case 20:
-          linearize_kernel<true, 128, 3, 10><<<grid, 128, 0, st>>>(frames, pairs, chunk_table,
+          linearize_kernel<true, 128, 3, 10><<<grid, 128, 0, st>>>(frames, pairs, chunk_table, pair_chunk_offsets,
                                                                  chunk_pixels, poses, extrinsics,
                                                                  *cfg, partials);
           break;
         case 21:
-          linearize_kernel<true, 128, 3, 11><<<grid, 128, 0, st>>>(frames, pairs, chunk_table,
+          linearize_kernel<true, 128, 3, 11><<<grid, 128, 0, st>>>(frames, pairs, chunk_table, pair_chunk_offsets,
                                                                  chunk_pixels, poses, extrinsics,
                                                                  *cfg, partials);
           break;
         case 24:
-          linearize_kernel<true, 128, 3, 13><<<grid, 128, 0, st>>>(frames, pairs, chunk_table,
+          linearize_kernel<true, 128, 3, 13><<<grid, 128, 0, st>>>(frames, pairs, chunk_table, pair_chunk_offsets,
                                                                  chunk_pixels, poses, extrinsics,
                                                                  *cfg, partials);
           break;
         case 9:  // diagnostics: destination gather replaced by a fixed texel
-          linearize_kernel<true, 128, 3, 1><<<grid, 128, 0, st>>>(frames, pairs, chunk_table,
+          linearize_kernel<true, 128, 3, 1><<<grid, 128, 0, st>>>(frames, pairs, chunk_table, pair_chunk_offsets,
                                                                 chunk_pixels, poses, extrinsics,
                                                                 *cfg, partials);
           break;

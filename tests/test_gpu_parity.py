@@ -683,3 +683,15 @@ def test_records_agree_far_below_the_bar(name):
                 scale = max(np.abs(other[:, sl]).max(), 1e-300)
                 assert np.abs(got[:, sl] - other[:, sl]).max() <= 1e-11 * scale
             assert np.array_equal(got[:, 91], other[:, 91])
+
+
+def test_chunk_launch_order_does_not_change_records(monkeypatch):
+    """Partials are slot-addressed, so every CTA launch order (edge order,
+    destination- or source-interleaved) gives bit-identical records."""
+    prob, gt, guess = _room_problem()
+    rows, _ = P.se3.pose_rows(guess)
+    out = {}
+    for order in ("pair", "dst", "src"):
+        monkeypatch.setenv("PBA_CHUNK_ORDER", order)
+        out[order] = _level([prob], 0).linearize(_rows(rows)).cpu().numpy()
+    assert np.array_equal(out["pair"], out["dst"]) and np.array_equal(out["pair"], out["src"])

@@ -213,3 +213,16 @@ def test_shard_ranges_balanced_and_contiguous():
         assert rs[0][0] == 0 and rs[-1][1] == len(px)
         assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
     assert shard_ranges(px, 2) == [(0, 4), (4, 8)]
+
+
+def test_chunk_orders_are_permutations(monkeypatch):
+    from paper_2303_16878_b200.device import order_chunks
+
+    # 3 pairs with 2, 3, 1 chunks of 100 pixels; pairs 0 and 2 share dst frame 5
+    tab = np.array([0, 0, 0, 100, 1, 0, 1, 100, 1, 200, 2, 0], np.int32)
+    src, dst = [1, 1, 2], [5, 6, 5]
+    for order, want in (("pair", [0, 1, 2, 3, 4, 5]), ("dst", [0, 5, 1, 2, 3, 4]),
+                        ("src", [0, 2, 1, 3, 4, 5])):
+        monkeypatch.setenv("PBA_CHUNK_ORDER", order)
+        got = order_chunks(tab.copy(), 6, 100, src, dst).reshape(-1, 2)
+        assert [int(np.nonzero((tab.reshape(-1, 2) == r).all(1))[0][0]) for r in got] == want
