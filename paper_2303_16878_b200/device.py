@@ -69,22 +69,35 @@ def block_rows(slot_of_pose, pose_i, pose_j):
 
 
 def order_chunks(chunk_tab, n_chunks, chunk_pixels, src_of_pair, dst_of_pair):
-    """Launch order of the linearisation CTAs (results do not depend on it:
-    partials are addressed by the chunk's slot in its pair).  PBA_CHUNK_ORDER:
-    "dst" (default: the pairs sharing a destination frame interleaved chunk
-    by chunk, so their gathers hit the same destination image in L2 —
-    c3 linearisation 26.3 -> 21.3 ms, c4 neutral), "pair" (edge order), "src"
-    (interleaved by source frame)."""
+    """Launch order of the linearisation CTAs.  Results do not depend on it:
+    a CTA's partials are stored at its chunk's slot in its pair.
+
+    PBA_CHUNK_ORDER (measured in profiles/r01_chunk_order.json):
+      "blk" (default): pairs tiled by (source frame // B, destination frame // B),
+            B = PBA_CHUNK_BLOCK (16); inside a tile the pairs advance chunk
+            position by chunk position, so the CTAs in flight read the same row
+            band of ~B source and ~B destination images from L2
+            (c4 34.6 -> 32.1 ms, c3 21.1 -> 19.5 ms per linearisation);
+      "dst": pairs sharing a destination frame interleaved chunk by chunk;
+      "src": the same for the source frame;  "pair": edge order.
+    """
     import os
 
-    order = os.environ.get("PBA_CHUNK_ORDER", "dst")
+    order = os.environ.get("PBA_CHUNK_ORDER", "blk")
     if order == "pair" or n_chunks == 0:
         return chunk_tab
     tab = chunk_tab[: 2 * n_chunks].reshape(-1, 2)
     pair = tab[:, 0].astype(np.int64)
     pos = tab[:, 1].astype(np.int64) // chunk_pixels
-    frame = np.asarray(dst_of_pair if order == "dst" else src_of_pair, np.int64)[pair]
-    perm = np.lexsort((pair, pos, frame))
+    src = np.asarray(src_of_pair, np.int64)[pair]
+    dst = np.asarray(dst_of_pair, np.int64)[pair]
+    if order == "blk":
+        blk = max(1, int(os.environ.get("PBA_CHUNK_BLOCK", "16")))
+        perm = np.lexsort((pair, pos, dst // blk, src // blk))
+    elif order in ("dst", "src"):
+        perm = np.lexsort((pair, pos, dst if order == "dst" else src))
+    else:
+        raise ValueError(f"PBA_CHUNK_ORDER={order!r}: expected blk, dst, src or pair")
     return np.ascontiguousarray(tab[perm].reshape(-1), dtype=np.int32)
 
 

@@ -691,7 +691,9 @@ def test_chunk_launch_order_does_not_change_records(monkeypatch):
     prob, gt, guess = _room_problem()
     rows, _ = P.se3.pose_rows(guess)
     out = {}
-    for order in ("pair", "dst", "src"):
+    for order in ("pair", "dst", "src", "blk"):
         monkeypatch.setenv("PBA_CHUNK_ORDER", order)
+        monkeypatch.setenv("PBA_CHUNK_BLOCK", "3")
         out[order] = _level([prob], 0).linearize(_rows(rows)).cpu().numpy()
-    assert np.array_equal(out["pair"], out["dst"]) and np.array_equal(out["pair"], out["src"])
+    for order in ("dst", "src", "blk"):
+        assert np.array_equal(out["pair"], out[order]), order

@@ -226,3 +226,12 @@ def test_chunk_orders_are_permutations(monkeypatch):
         monkeypatch.setenv("PBA_CHUNK_ORDER", order)
         got = order_chunks(tab.copy(), 6, 100, src, dst).reshape(-1, 2)
         assert [int(np.nonzero((tab.reshape(-1, 2) == r).all(1))[0][0]) for r in got] == want
+    # blk with block 2: tiles (src//2, dst//2) = (0,2), (0,3), (1,2) in that order
+    monkeypatch.setenv("PBA_CHUNK_ORDER", "blk")
+    monkeypatch.setenv("PBA_CHUNK_BLOCK", "2")
+    got = order_chunks(tab.copy(), 6, 100, src, dst).reshape(-1, 2)
+    idx = [int(np.nonzero((tab.reshape(-1, 2) == r).all(1))[0][0]) for r in got]
+    assert idx == [0, 1, 2, 3, 4, 5]
+    monkeypatch.setenv("PBA_CHUNK_ORDER", "bogus")
+    with pytest.raises(ValueError):
+        order_chunks(tab.copy(), 6, 100, src, dst)
