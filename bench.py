@@ -236,15 +236,17 @@ def compute_roofline(counts, lin_ms):
 
 def ncu_traffic(name):
     """dram bytes per pixel-pair of the linearisation kernel from the committed
-    ncu --set full summary (profiles/), scaled to this launch; None if absent."""
+    ncu --set full summary (profiles/), scaled to this launch by the caller;
+    None if absent or captured on another workload (it is a per-config
+    figure: spherical c4 and pinhole c3 differ)."""
     p = ROOT / "profiles" / "linearize_traffic.json"
     if not p.exists():
         return None
     try:
         d = json.loads(p.read_text())
-        return d
     except Exception:
         return None
+    return d if d.get("config", "c4") == name else None
 
 
 # ---------------------------------------------------------------------------
