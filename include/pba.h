@@ -210,7 +210,9 @@ int pba_solve_dense(const double* H, const double* b, int32_t dim, double lam,
  * returned as an inexact LM step).  work: pba_pcg_work_bytes(n_free) bytes.
  * status: 0 ok, 1 when a damped diagonal block or the system is not
  * positive definite.  info (device, 3 doubles): iterations, final relative
- * residual, converged flag. */
+ * residual, converged flag.  The iteration vectors live in registers of
+ * co-resident CTAs, so n_free <= 32 x (resident CTAs) (~9,400 poses on a
+ * B200); larger systems return PBA_ERR_ARG (use pba_solve_dense). */
 size_t pba_pcg_work_bytes(int32_t n_free);
 int pba_solve_pcg(const double* H, const double* b, int32_t n_free, double lam,
                   const int32_t* row_ptr, const int32_t* cols, int32_t max_iter, double tol,
