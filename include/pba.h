@@ -151,6 +151,11 @@ int pba_plan_chunks(pba_pair* pairs, int32_t n_pairs, const pba_camera* src_cams
 /* frames, pairs, chunk_table, pair_chunk_offsets, poses (n_poses x 12),
  * extrinsics (n_ext x 12), partials (n_chunks x PBA_PARTIAL_DOUBLES) and records
  * (n_pairs x 92) are device pointers; cfg is a host pointer.
+ * The chunk table's rows may be permuted freely before upload (it is the
+ * CTA launch order; each chunk's partials go to slot
+ * pair_chunk_offsets[pair] + first / chunk_pixels, so records do not
+ * change); the Python host tiles it by (source, destination) frame blocks
+ * for L2 locality (device.order_chunks).
  * want_jacobians = 0 is the cost-only path of total_error
  * (solver.py:655-670): ok_jac is not applied and only cost/count are
  * produced (the H/b fields are zero). */
