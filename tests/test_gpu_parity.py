@@ -578,13 +578,16 @@ from tests import fixtures as F
 d = F.load("pinhole_small")
 prob, _ = F.single_problem(d)
 out = {}
+pcg = P.SolverConfig(linear_solver="pcg")
 res = P.solve_hierarchical(prob, P.SolverConfig())
 out["plain"] = [list(p.as_row()) for p in res.poses]
+out["plain_pcg"] = [list(p.as_row()) for p in P.solve_hierarchical(prob, pcg).poses]
 os.environ["PBA_FORCE_SHARDED"] = "1"
 dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
 res = P.solve_hierarchical(prob, P.SolverConfig())
 out["nccl"] = [list(p.as_row()) for p in res.poses]
 out["trace"] = [(r.level, r.iteration, r.accepted, r.valid_blocks) for r in res.records]
+out["nccl_pcg"] = [list(p.as_row()) for p in P.solve_hierarchical(prob, pcg).poses]
 dist.destroy_process_group()
 print(json.dumps(out))
 """
@@ -605,6 +608,7 @@ def test_sharded_path_over_nccl_matches_single_gpu():
     assert r.returncode == 0, r.stderr[-2000:]
     out = json.loads(r.stdout.strip().splitlines()[-1])
     assert np.array_equal(np.array(out["plain"]), np.array(out["nccl"]))
+    assert np.array_equal(np.array(out["plain_pcg"]), np.array(out["nccl_pcg"]))  # rank-0 PCG
     assert len(out["trace"]) > 0
 
 
