@@ -32,7 +32,9 @@ int ensure_atan_table();
 __device__ __forceinline__ float atan2_guess(float y, float x, bool y_negative) {
   const float ax = fabsf(x), ay = fabsf(y);
   const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
-  const float a = mn * __frcp_rn(mx);
+  // approximate quotient (MUFU.RCP + FMUL, ~2 ulp): the guess only has to
+  // land within the series' reach of a table angle (3e-3 rad of margin)
+  const float a = __fdividef(mn, mx);
   const float s = a * a;
   float r = fmaf(fmaf(fmaf(-0.0464964749f, s, 0.15931422f), s, -0.327622764f), s * a, a);
   if (ay > ax) r = 1.57079637f - r;
