@@ -631,40 +631,32 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     }
   }
 
-  // ---- fixed-order reduction: warp butterfly, then warps in order ----
+  // ---- fixed-order reduction: warp reduce-scatter, then warps in order ----
+  // The 32 partial values (Q 21, beta 6, cost, count, 3 zero pads) are
+  // halved over lanes five times: at offset o a lane keeps the half of its
+  // values selected by its lane bit o and adds the partner's copy of that
+  // half, so after 16+8+4+2+1 = 31 shuffles lane L holds the warp sum of
+  // value L (a butterfly per value would take 29 x 5 = 145).
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double cnt = (double)count;
-  if (kJac) {
+  double v[kPart];
 #pragma unroll
-    for (int k = 0; k < kQ; ++k) {
-      double x = Q[k];
+  for (int k = 0; k < kQ; ++k) v[k] = kJac ? Q[k] : 0.0;
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
-      Q[k] = x;
+  for (int k = 0; k < 6; ++k) v[kQ + k] = kJac ? beta[k] : 0.0;
+  v[27] = cost;
+  v[28] = (double)count;
+  v[29] = v[30] = v[31] = 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const bool upper = (lane & o) != 0;
+#pragma unroll
+    for (int k = 0; k < o; ++k) {
+      const double send = upper ? v[k] : v[k + o];
+      const double keep = upper ? v[k + o] : v[k];
+      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
     }
-#pragma unroll
-    for (int k = 0; k < 6; ++k) {
-      double x = beta[k];
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
-      beta[k] = x;
-    }
   }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    cost += __shfl_xor_sync(0xffffffffu, cost, off);
-    cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
-  }
-  if (lane == 0) {
-    double* r = red[warp];
-#pragma unroll
-    for (int k = 0; k < kQ; ++k) r[k] = kJac ? Q[k] : 0.0;
-#pragma unroll
-    for (int k = 0; k < 6; ++k) r[kQ + k] = kJac ? beta[k] : 0.0;
-    r[27] = cost;
-    r[28] = cnt;
-    r[29] = r[30] = r[31] = 0.0;
-  }
+  red[warp][lane] = v[0];
   __syncthreads();
   if (threadIdx.x < kPart) {
     double s = 0.0;
