@@ -701,3 +701,32 @@ def test_chunk_launch_order_does_not_change_records(monkeypatch):
         out[order] = _level([prob], 0).linearize(_rows(rows)).cpu().numpy()
     for order in ("dst", "src", "blk"):
         assert np.array_equal(out["pair"], out[order]), order
+
+
+@pytest.mark.parametrize("config,frames", [("c3", 4), ("c5", 3)])
+def test_bench_shapes_records_and_trace_match_oracle(config, frames):
+    """The other bench sensor shapes at full resolution against the oracle:
+    c3 (640x480 pinhole on a forward-looking mount) and c5 (coupled OS0-128
+    spherical + 640x480 pinhole in one level problem) — per-pair records of
+    the finest level at the perturbed guess and a short LM trace."""
+    import bench
+
+    problems, guess, gt, meta = bench.build_problem(config, torch.device("cuda", 0), frames)
+    level = meta["level"]
+    rows, gens = P.se3.pose_rows(guess)
+    assert sum(len(p.graph.edges) for p in problems) > 0
+    got = _level(problems, level).linearize(_rows(rows)).cpu().numpy()
+    ref = O.OracleLevel(problems, level, P.SolverConfig()).records(rows)
+    F.compare_records(got, ref)
+    assert ref[:, 91].sum() > 1e4
+    from paper_2303_16878_b200.bundle import _lm_level, _Runtime
+
+    backend = _Runtime().level(problems, level, P.SolverConfig())
+    backend.set_poses(rows, gens)
+    records = _lm_level(backend, level, P.SolverConfig(), 3)
+    lp = O.OracleLevel(problems, level, P.SolverConfig())
+    _, _, o_recs = O.solve_level_multi(lp, rows, gens.astype(np.int64), level, P.SolverConfig(), 3)
+    assert [(r.iteration, r.accepted, r.valid_blocks, r.lam) for r in records] == [
+        (r.iteration, r.accepted, r.valid_blocks, r.lam) for r in o_recs]
+    for a, b in zip(records, o_recs):
+        assert abs(a.error - b.error) <= 1e-6 * b.error
