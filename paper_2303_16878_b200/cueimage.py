@@ -136,6 +136,7 @@ class DeviceCueImage:
         self.device_normals = normals
         self.intrinsics = intrinsics
         self._host: CueImage | None = None
+        self._depth: np.ndarray | None = None
 
     @property
     def shape(self) -> tuple[int, int]:
@@ -157,7 +158,20 @@ class DeviceCueImage:
 
     @property
     def depth(self) -> np.ndarray:
-        return self.host().depth
+        """The clamped depth of CueImage.__post_init__ (out-of-range or
+        non-finite -> 0) without building the whole host image (graph
+        construction only needs depth and depth_valid)."""
+        if self._host is not None:
+            return self._host.depth
+        if self._depth is None:
+            d = np.array(self.device_depth.cpu().numpy(), dtype=float)
+            cam = self.intrinsics
+            with np.errstate(invalid="ignore"):
+                bad = ~np.isfinite(d) | (d < cam.depth_min) | (d > cam.depth_max)
+            d[bad] = 0.0
+            d.flags.writeable = False
+            self._depth = d
+        return self._depth
 
     def __getattr__(self, name):
         if name in _DERIVED or name in ("intensity", "normals"):

@@ -139,6 +139,48 @@ def _prefilter(nodes, crit: MatchCriteria) -> list:
     return out
 
 
+def _gated(nodes, candidates, crit) -> list:
+    """The candidates passing _gates_pass, decided in bulk: rotation angle
+    and translation distance are evaluated vectorised and only values within
+    1e-9 of a threshold are re-decided by the exact per-pair path (the bulk
+    and scalar evaluations can differ in the last bits only)."""
+    if not candidates:
+        return []
+    ab = np.asarray(candidates, dtype=np.int64)
+    r = np.array([np.asarray(nd.pose_guess.rotation, float) for nd in nodes])
+    t = np.array([np.asarray(nd.pose_guess.translation, float) for nd in nodes])
+    ri, rj = r[ab[:, 0]], r[ab[:, 1]]
+    tr = np.einsum("kij,kij->k", rj, ri)  # trace(R_j^T R_i)
+    ang = np.arccos(np.clip(0.5 * (tr - 1.0), -1.0, 1.0))
+    dist = np.linalg.norm(t[ab[:, 0]] - t[ab[:, 1]], axis=1)
+    near = (np.abs(ang - crit.max_angle) <= 1e-9) | (
+        np.abs(dist - crit.max_translation) <= 1e-9 * max(1.0, crit.max_translation))
+    ok = (ang <= crit.max_angle) & (dist <= crit.max_translation)
+    out = []
+    for k, (a, b) in enumerate(candidates):
+        if near[k]:
+            if _gates_pass(nodes[a], nodes[b], crit):
+                out.append((a, b))
+        elif ok[k]:
+            out.append((a, b))
+    return out
+
+
+def _relative_rows(sensor, inv, src, dst):
+    """sensor[dst]^-1 * sensor[src] as (n, 12) rows, batched; None when any
+    composition would reach the re-orthonormalisation generation."""
+    gens = np.array([p.generation for p in sensor]) + np.array([p.generation for p in inv])
+    if gens.max(initial=0) + 1 >= 999:
+        return None
+    rs = np.array([p.rotation for p in sensor])
+    ts = np.array([p.translation for p in sensor])
+    ri = np.array([p.rotation for p in inv])
+    ti = np.array([p.translation for p in inv])
+    rot = np.einsum("kij,kjl->kil", ri[dst], rs[src])
+    trans = np.einsum("kij,kj->ki", ri[dst], ts[src]) + ti[dst]
+    return np.concatenate([rot.reshape(-1, 9), trans], axis=1)
+
+
 def _pose_rows(pose) -> np.ndarray:
     return np.concatenate([np.asarray(pose.rotation, float).reshape(9),
                            np.asarray(pose.translation, float).reshape(3)])
@@ -168,22 +210,25 @@ def _gpu_overlap_verdicts(nodes, candidates, crit, extrinsics, level, stride, ca
     offs = torch.tensor(offsets, dtype=torch.int64, device=dev)
     sensor = [nd.pose_guess.compose(off) for nd in nodes]
     inv = [sp.inverse() for sp in sensor]
-    gated = [ab for ab in candidates if _gates_pass(nodes[ab[0]], nodes[ab[1]], crit)]
+    gated = _gated(nodes, candidates, crit)
     if not gated:
         return {}
-    src, trans, cams = [], [], (N.Camera * (2 * len(gated)))()
-    for k, (a, b) in enumerate(gated):
-        for d, (i, j) in enumerate(((a, b), (b, a))):
-            src.append(i)
-            trans.append(_pose_rows(inv[j].compose(sensor[i])))
-            cams[2 * k + d] = camera_struct(nodes[j].pyramid.levels[level].intrinsics)
-    src_t = torch.tensor(src, dtype=torch.int32, device=dev)
-    trans_t = torch.from_numpy(np.array(trans)).to(dev)
-    cams_t = torch.frombuffer(bytearray(bytes(memoryview(cams).cast("B"))),
-                              dtype=torch.uint8).to(dev)
-    counts = torch.zeros(len(src), dtype=torch.int64, device=dev)
+    # directed entries (a->b, b->a) per gated pair: source frame, sensor_j^-1 *
+    # sensor_i as a 12-double row, destination camera
+    ab = np.asarray(gated, dtype=np.int64)
+    src_np = ab.reshape(-1)                 # a, b, a, b, ...
+    dst_np = ab[:, ::-1].reshape(-1)        # b, a, b, a, ...
+    trans = _relative_rows(sensor, inv, src_np, dst_np)
+    if trans is None:  # a pose near re-orthonormalisation: the scalar compose path
+        trans = np.array([_pose_rows(inv[j].compose(sensor[i])) for i, j in zip(src_np, dst_np)])
+    frame_cams = np.frombuffer(b"".join(bytes(camera_struct(nd.pyramid.levels[level].intrinsics))
+                                        for nd in nodes), dtype=np.uint8).reshape(len(nodes), -1)
+    src_t = torch.from_numpy(src_np.astype(np.int32)).to(dev)
+    trans_t = torch.from_numpy(np.ascontiguousarray(trans, dtype=np.float64)).to(dev)
+    cams_t = torch.from_numpy(np.ascontiguousarray(frame_cams[dst_np]).reshape(-1)).to(dev)
+    counts = torch.zeros(len(src_np), dtype=torch.int64, device=dev)
     N.check(lib.pba_overlap_counts(points.data_ptr(), offs.data_ptr(), src_t.data_ptr(),
-                                   trans_t.data_ptr(), cams_t.data_ptr(), len(src), 1e-6,
+                                   trans_t.data_ptr(), cams_t.data_ptr(), len(src_np), 1e-6,
                                    counts.data_ptr(), torch.cuda.current_stream(dev).cuda_stream),
             "pba_overlap_counts")
     counts = counts.cpu().numpy()

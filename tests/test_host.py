@@ -235,3 +235,50 @@ def test_chunk_orders_are_permutations(monkeypatch):
     monkeypatch.setenv("PBA_CHUNK_ORDER", "bogus")
     with pytest.raises(ValueError):
         order_chunks(tab.copy(), 6, 100, src, dst)
+
+
+def test_bulk_graph_gates_and_transforms_match_scalar_path():
+    """The bulk helpers of the device graph build (pairgraph._gated,
+    _relative_rows) decide exactly like the per-pair reference path and give
+    the same transforms to the last few bits."""
+    from paper_2303_16878_b200 import pairgraph as G
+    from paper_2303_16878_b200 import scenes as S
+
+    gt = S.room_loop(30)
+    poses = S.perturb(gt, 0.3, math.radians(20.0), 5)
+    nodes = [P.FrameNode(k, poses[k], None, 0.1 * k) for k in range(30)]
+    crit = P.MatchCriteria(max_translation=0.6, max_angle=math.radians(25.0))
+    cands = [(a, b) for a in range(30) for b in range(a + 1, 30)]
+    want = [ab for ab in cands if G._gates_pass(nodes[ab[0]], nodes[ab[1]], crit)]
+    assert 0 < len(want) < len(cands)
+    assert G._gated(nodes, cands, crit) == want
+    off = P.Pose(np.eye(3), [0.0, 0.0, 0.1])
+    sensor = [nd.pose_guess.compose(off) for nd in nodes]
+    inv = [sp.inverse() for sp in sensor]
+    src = np.array([a for a, b in want] + [b for a, b in want])
+    dst = np.array([b for a, b in want] + [a for a, b in want])
+    rows = G._relative_rows(sensor, inv, src, dst)
+    ref = np.array([G._pose_rows(inv[j].compose(sensor[i])) for i, j in zip(src, dst)])
+    assert np.allclose(rows, ref, rtol=0, atol=1e-14)
+
+
+def test_device_cue_image_depth_without_host_build():
+    """DeviceCueImage.depth / depth_valid (used by graph construction) equal
+    the host CueImage's clamped depth and mask bit for bit, without building
+    the host image."""
+    torch = pytest.importorskip("torch")
+    from paper_2303_16878_b200.camera import Intrinsics
+    from paper_2303_16878_b200.cueimage import CueImage, DeviceCueImage
+
+    cam = Intrinsics(20.0, 20.0, 8.0, 6.0, 16, 12, P.PINHOLE, 0.5, 4.0)
+    rng = np.random.default_rng(0)
+    d = rng.uniform(0.0, 5.0, (12, 16))
+    d[0, 0], d[1, 1], d[2, 2] = np.nan, np.inf, -1.0
+    inten = rng.uniform(0, 1, (12, 16))
+    nrm = rng.normal(size=(12, 16, 3))
+    dev = DeviceCueImage(torch.from_numpy(inten), torch.from_numpy(d), torch.from_numpy(nrm), cam)
+    ref = CueImage(inten, d, nrm, cam)
+    assert np.array_equal(dev.depth, ref.depth) and dev._host is None
+    assert np.array_equal(dev.depth_valid, ref.depth_valid)
+    assert np.array_equal(dev.normal_valid, ref.normal_valid)  # builds the host image
+    assert np.array_equal(dev.depth, ref.depth)
