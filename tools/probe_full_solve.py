@@ -28,4 +28,5 @@ for rep in range(2):
         levels[r.level] += 1
     err = max(float(abs(p.translation - q.translation).max()) for p, q in zip(res.poses, gt))
     print(f"rep {rep}: solve_hierarchical {t:.2f} s, iterations per level {levels}, "
+          f"level wall times {[(lv, round(s, 3)) for lv, s in res.level_times]}, "
           f"max |t - t_gt| {err:.2e} m (setup {t_setup:.1f} s)")
