@@ -68,16 +68,19 @@ def block_rows(slot_of_pose, pose_i, pose_j):
     return np.cumsum(row_ptr).astype(np.int32), cols.astype(np.int32)
 
 
-def order_chunks(chunk_tab, n_chunks, chunk_pixels, src_of_pair, dst_of_pair):
+def order_chunks(chunk_tab, n_chunks, chunk_pixels, src_of_pair, dst_of_pair,
+                 pinhole_of_pair=None):
     """Launch order of the linearisation CTAs.  Results do not depend on it:
     a CTA's partials are stored at its chunk's slot in its pair.
 
     PBA_CHUNK_ORDER (measured in profiles/r01_chunk_order.json):
       "blk" (default): pairs tiled by (source frame // B, destination frame // B),
-            B = PBA_CHUNK_BLOCK (16); inside a tile the pairs advance chunk
-            position by chunk position, so the CTAs in flight read the same row
-            band of ~B source and ~B destination images from L2
-            (c4 34.6 -> 32.1 ms, c3 21.1 -> 19.5 ms per linearisation);
+            B = 16 for spherical and 32 for pinhole sources (the measured
+            optima; PBA_CHUNK_BLOCK overrides both); inside a tile the pairs
+            advance chunk position by chunk position, so the CTAs in flight
+            read the same row band of ~B source and ~B destination images
+            from L2 (c4/200 34.6 -> 32.1 ms, full c3 linearisation 113.4 ->
+            101.7 ms);
       "dst": pairs sharing a destination frame interleaved chunk by chunk;
       "src": the same for the source frame;  "pair": edge order.
     """
@@ -92,8 +95,12 @@ def order_chunks(chunk_tab, n_chunks, chunk_pixels, src_of_pair, dst_of_pair):
     src = np.asarray(src_of_pair, np.int64)[pair]
     dst = np.asarray(dst_of_pair, np.int64)[pair]
     if order == "blk":
-        blk = max(1, int(os.environ.get("PBA_CHUNK_BLOCK", "16")))
-        perm = np.lexsort((pair, pos, dst // blk, src // blk))
+        pin = (np.zeros(len(src_of_pair), np.int64) if pinhole_of_pair is None
+               else np.asarray(pinhole_of_pair, np.int64))[pair]
+        env = os.environ.get("PBA_CHUNK_BLOCK")
+        blk = (np.full(pair.shape, max(1, int(env)), np.int64) if env
+               else np.where(pin == 1, 32, 16))
+        perm = np.lexsort((pair, pos, dst // blk, src // blk, pin))
     elif order in ("dst", "src"):
         perm = np.lexsort((pair, pos, dst if order == "dst" else src))
     else:
@@ -279,7 +286,9 @@ class DeviceLevel:
                                          ctypes.byref(n_chunks)), "pba_plan_chunks")
         chunk_tab = order_chunks(chunk_tab, self.n_chunks, self.chunk_pixels,
                                  [pairs[k].src for k in range(self.n_pairs)],
-                                 [pairs[k].dst for k in range(self.n_pairs)])
+                                 [pairs[k].dst for k in range(self.n_pairs)],
+                                 [int(src_cams[k].model == N.PBA_PINHOLE)
+                                  for k in range(self.n_pairs)])
         dev = self.device
         self.frames_t = _struct_tensor((N.Frame * max(1, len(frames)))(*frames), dev)
         self.pairs_t = _struct_tensor(pairs, dev)

@@ -232,6 +232,12 @@ def test_chunk_orders_are_permutations(monkeypatch):
     got = order_chunks(tab.copy(), 6, 100, src, dst).reshape(-1, 2)
     idx = [int(np.nonzero((tab.reshape(-1, 2) == r).all(1))[0][0]) for r in got]
     assert idx == [0, 1, 2, 3, 4, 5]
+    # default blocks: spherical sources tile by 16, pinhole by 32, models apart
+    monkeypatch.setenv("PBA_CHUNK_ORDER", "blk")
+    monkeypatch.delenv("PBA_CHUNK_BLOCK")
+    got = order_chunks(tab.copy(), 6, 100, src, dst, [1, 0, 1]).reshape(-1, 2)
+    idx = [int(np.nonzero((tab.reshape(-1, 2) == r).all(1))[0][0]) for r in got]
+    assert idx == [2, 3, 4, 0, 5, 1]  # pair 1 (spherical) first; pinhole pairs 0, 2 interleaved
     monkeypatch.setenv("PBA_CHUNK_ORDER", "bogus")
     with pytest.raises(ValueError):
         order_chunks(tab.copy(), 6, 100, src, dst)
