@@ -222,6 +222,26 @@ __global__ void __launch_bounds__(1024) potrf_inv_kernel(double* __restrict__ A,
 // are identity, so every tile runs the same schedule.
 constexpr int PW = 8;  // panel width
 
+template <bool kRB>
+__global__ void potrf_reg_kernel(double* __restrict__ A, int dim, int k_arg,
+                                 const int32_t* __restrict__ klist, double* __restrict__ Linv,
+                                 int32_t* __restrict__ status);
+
+// PBA_POTRF_RB=0 selects the shared-memory trailing update (comparison).
+bool potrf_rb() {
+  static int v = -1;
+  if (v < 0) {
+    const char* env = getenv("PBA_POTRF_RB");
+    v = !(env && env[0] == '0');
+  }
+  return v == 1;
+}
+
+// kRB: the trailing update runs on register-held 4x4 blocks (thread t owns
+// rows 4(t/16).., cols 4(t%16)..), reading only the 8 panel columns from
+// shared memory; the owners of the next panel's columns publish them to
+// shared memory before warp 0 factors it.
+template <bool kRB>
 __global__ void __launch_bounds__(256) potrf_reg_kernel(double* __restrict__ A, int dim,
                                                         int k_arg,
                                                         const int32_t* __restrict__ klist,
@@ -245,8 +265,25 @@ __global__ void __launch_bounds__(256) potrf_reg_kernel(double* __restrict__ A, 
   }
   if (tid == 0) bad = 0;
   __syncthreads();
+  const int rb = tid >> 4, cb = tid & 15;  // kRB: this thread's 4x4 block
+  double blk[4][4];
+  if (kRB) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) blk[i][j] = a[4 * rb + i][4 * cb + j];
+  }
 #pragma unroll 1
   for (int c0 = 0; c0 < NB; c0 += PW) {
+    if (kRB && c0 > 0) {  // publish the panel's columns (updated in registers)
+      if (4 * cb >= c0 && 4 * cb < c0 + PW && cb <= rb) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) a[4 * rb + i][4 * cb + j] = blk[i][j];
+      }
+      __syncthreads();
+    }
     if (warp == 0) {
       const int hp = c0 >> 5;  // half (row block) the panel's diagonal rows live in
       double v0[PW], v1[PW];
@@ -283,8 +320,34 @@ __global__ void __launch_bounds__(256) potrf_reg_kernel(double* __restrict__ A, 
     }
     __syncthreads();
     if (bad) break;
-    // rank-16 trailing update: a[r][c] -= sum_j a[r][j] a[c][j], c1 <= c <= r
+    // rank-8 trailing update: a[r][c] -= sum_j a[r][j] a[c][j], c1 <= c <= r
     const int c1 = c0 + PW, m = NB - c1;
+    if (kRB) {
+      if (4 * cb >= c1 && cb <= rb) {
+        double pr[4][PW], pc[4][PW];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int q = 0; q < PW; ++q) {
+            pr[i][q] = a[4 * rb + i][c0 + q];
+            pc[i][q] = a[4 * cb + i][c0 + q];
+          }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+            for (int q = 0; q < PW; q += 2) {
+              s0 = fma(pr[i][q], pc[j][q], s0);
+              s1 = fma(pr[i][q + 1], pc[j][q + 1], s1);
+            }
+            blk[i][j] -= s0 + s1;
+          }
+      }
+      __syncthreads();
+      continue;
+    }
     for (int e = tid; e < m * m; e += blockDim.x) {
       const int r = c1 + e / m, c = c1 + e % m;
       if (c <= r) {
@@ -780,15 +843,21 @@ int solve_dissected(const double* H, const double* b, int dim, double lam,
   PBA_LAUNCH_CHECK();
   const int tile_smem = 2 * NB * LD * sizeof(double);
   const int reg_smem = tile_smem + (NB / PW - 1) * PW * (PW + 1) * (int)sizeof(double);
-  PBA_CUDA_TRY(cudaFuncSetAttribute(potrf_reg_kernel,
+  PBA_CUDA_TRY(cudaFuncSetAttribute(potrf_reg_kernel<true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, reg_smem));
+  PBA_CUDA_TRY(cudaFuncSetAttribute(potrf_reg_kernel<false>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, reg_smem));
   PBA_CUDA_TRY(cudaFuncSetAttribute(panel_list_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));
   PBA_CUDA_TRY(cudaFuncSetAttribute(syrk_list_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));
   for (const Launch& L : launches) {
-    potrf_reg_kernel<<<L.nk, 256, reg_smem, st>>>(w.A, D, 0, d_lists + off_k + L.k0, w.Linv,
-                                                  status);
+    if (potrf_rb())
+      potrf_reg_kernel<true><<<L.nk, 256, reg_smem, st>>>(w.A, D, 0, d_lists + off_k + L.k0,
+                                                          w.Linv, status);
+    else
+      potrf_reg_kernel<false><<<L.nk, 256, reg_smem, st>>>(w.A, D, 0, d_lists + off_k + L.k0,
+                                                           w.Linv, status);
     PBA_LAUNCH_CHECK();
     if (L.np) {
       panel_list_kernel<<<L.np, 256, tile_smem, st>>>(w.A, D, d_lists + off_p + 2 * L.p0,
@@ -888,11 +957,15 @@ extern "C" int pba_solve_dense(const double* H, const double* b, int32_t dim, do
   PBA_CUDA_TRY(cudaFuncSetAttribute(potrf_inv_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));
   const int reg_smem = tile_smem + (NB / PW - 1) * PW * (PW + 1) * (int)sizeof(double);
-  PBA_CUDA_TRY(cudaFuncSetAttribute(potrf_reg_kernel,
+  PBA_CUDA_TRY(cudaFuncSetAttribute(potrf_reg_kernel<true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, reg_smem));
+  PBA_CUDA_TRY(cudaFuncSetAttribute(potrf_reg_kernel<false>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, reg_smem));
   for (int k = 0; k < T; ++k) {
-    if (potrf_variant == 1)
-      potrf_reg_kernel<<<1, 256, reg_smem, st>>>(w.A, dim, k, nullptr, w.Linv, status);
+    if (potrf_variant == 1 && potrf_rb())
+      potrf_reg_kernel<true><<<1, 256, reg_smem, st>>>(w.A, dim, k, nullptr, w.Linv, status);
+    else if (potrf_variant == 1)
+      potrf_reg_kernel<false><<<1, 256, reg_smem, st>>>(w.A, dim, k, nullptr, w.Linv, status);
     else
       potrf_inv_kernel<<<1, 1024, tile_smem, st>>>(w.A, dim, k, w.Linv, status);
     PBA_LAUNCH_CHECK();
