@@ -345,21 +345,20 @@ __global__ void __launch_bounds__(256) potrf_reg_kernel(double* __restrict__ A, 
             blk[i][j] -= s0 + s1;
           }
       }
-      __syncthreads();
-      continue;
-    }
-    for (int e = tid; e < m * m; e += blockDim.x) {
-      const int r = c1 + e / m, c = c1 + e % m;
-      if (c <= r) {
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    } else {
+      for (int e = tid; e < m * m; e += blockDim.x) {
+        const int r = c1 + e / m, c = c1 + e % m;
+        if (c <= r) {
+          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
-        for (int j = 0; j < PW; j += 4) {
-          s0 = fma(a[r][c0 + j], a[c][c0 + j], s0);
-          s1 = fma(a[r][c0 + j + 1], a[c][c0 + j + 1], s1);
-          s2 = fma(a[r][c0 + j + 2], a[c][c0 + j + 2], s2);
-          s3 = fma(a[r][c0 + j + 3], a[c][c0 + j + 3], s3);
+          for (int j = 0; j < PW; j += 4) {
+            s0 = fma(a[r][c0 + j], a[c][c0 + j], s0);
+            s1 = fma(a[r][c0 + j + 1], a[c][c0 + j + 1], s1);
+            s2 = fma(a[r][c0 + j + 2], a[c][c0 + j + 2], s2);
+            s3 = fma(a[r][c0 + j + 3], a[c][c0 + j + 3], s3);
+          }
+          a[r][c] -= (s0 + s1) + (s2 + s3);
         }
-        a[r][c] -= (s0 + s1) + (s2 + s3);
       }
     }
     __syncthreads();
