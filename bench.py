@@ -43,6 +43,8 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+METRIC = ("GN iteration throughput: pixel-pair residuals/s (one LM iteration at the finest "
+          "level: solve + pose update + linearise + assemble)")
 BYTES_PER_PIXEL_PAIR = 80  # 5 fp64 cue values source + destination
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 
@@ -52,67 +54,116 @@ FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 # ---------------------------------------------------------------------------
 CONFIGS = {
     "c1": dict(desc="synthetic RGB-D pinhole 10 frames 160x120, 1 level", kind="room", n=10,
-               factors=(1,), max_translation=1.0),
+               factors=(1,), max_translation=1.0, pairs=24, pixel_pairs=460_800,
+               sample_frames=10),
     "c2": dict(desc="synthetic LiDAR spherical 64x1024 (HDL-64), 100 scans, 3 levels",
-               kind="hdl64", n=100, spacing=0.1, factors=(4, 2, 1), max_translation=1.0),
+               kind="hdl64", n=100, spacing=0.1, factors=(4, 2, 1), max_translation=1.0,
+               pairs=722, pixel_pairs=47_316_992, sample_frames=100),
     "c3": dict(desc="synthetic RGB-D pinhole 640x480 (TUM-shaped), 500 frames, 3 levels, "
                     "LM with block-Jacobi PCG", kind="tum", n=500, spacing=0.05,
-               factors=(4, 2, 1), max_translation=1.0, solver="pcg"),
+               factors=(4, 2, 1), max_translation=1.0, solver="pcg", pairs=6212,
+               pixel_pairs=1_684_654_459, sample_frames=24),
     "c4": dict(desc="synthetic OS0-128 128x1024, 1000 scans, 2 km corridor, 3 levels, ~20k pairs",
-               kind="os0", n=1000, spacing=2.0, factors=(4, 2, 1), max_translation=40.0),
+               kind="os0", n=1000, spacing=2.0, factors=(4, 2, 1), max_translation=40.0,
+               pairs=19258, pixel_pairs=2_519_907_096, sample_frames=48),
     "c5": dict(desc="joint LiDAR+RGB-D coupled BA: 500 platform poses x (OS0-128 128x1024 + "
                     "RGB-D 640x480), 3 levels", kind="fused", n=500, spacing=0.5,
-               factors=(4, 2, 1), max_translation=10.0, max_translation_rgbd=1.0),
+               factors=(4, 2, 1), max_translation=10.0, max_translation_rgbd=1.0, pairs=10170,
+               pixel_pairs=1_427_480_623, sample_frames=20),
 }
+# `pairs` / `pixel_pairs`: edge count and sum of depth-valid source pixels at
+# the finest level of each full problem, as the GPU arm measures them live
+# (round-1 bench lines, profiles/r01_bench_c*.json; test_c4_full_size_properties
+# re-checks c4).  The reference arm never builds the full problem — it
+# times a host-built prefix of `sample_frames` frames — so it quotes these.
+
+
+def workload_config(name: str, cam, frames: int, pairs: int, pixel_pairs: int, solver: str) -> dict:
+    """The `config` object of the bench line; both arms emit exactly this."""
+    c = CONFIGS[name]
+    return {"workload": f"{name}: {c['desc']}", "frames": frames, "pairs": pairs,
+            "pixel_pairs_per_iteration": pixel_pairs,
+            "level": f"finest ({cam.height}x{cam.width})", "linear_solver": solver,
+            "data": "synthetic box-corridor renders (seeded), inputs larger than L2"}
 
 # pinhole camera looking along the corridor (+x of the platform): camera z ->
 # platform x, camera x -> platform -y, camera y -> platform -z
 FORWARD_CAMERA = np.array([[0.0, 0.0, 1.0], [-1.0, 0.0, 0.0], [0.0, -1.0, 0.0]])
 
 
-def build_problem(name: str, device, n_override=None, normals: str = "estimate"):
+def host_pyramids_estimated(scene, cam, platform_poses, ext, factors, threads):
+    """Host-only pyramids (no GPU, no libpba_b200): torch-CPU renders, then
+    the numpy pyramid builder (estimate_normals + downscale, bit-exact to the
+    reference's build_pyramid, cues.py:342-375) on a thread pool."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_2303_16878_b200 import cueimage
+    from paper_2303_16878_b200 import scenes as S
+
+    rows = S.sensor_rows(platform_poses, ext)
+    scales = tuple(1.0 / f for f in factors)
+    inten, depth, _ = S.render_batch(scene, cam, rows)
+    inten, depth = inten.numpy(), depth.numpy()
+    with ThreadPoolExecutor(max_workers=max(1, threads)) as pool:
+        return list(pool.map(lambda b: cueimage.build_pyramid(inten[b], depth[b], cam, scales),
+                             range(rows.shape[0])))
+
+
+def build_problem(name: str, device, n_override=None, normals: str = "estimate",
+                  host: bool = False, prefix: int | None = None, threads: int = 8):
+    """The App. C problem of config `name`.  Default: frames rendered and
+    pyramids built on `device` (K6), graph built with K5.  host=True builds
+    everything on the CPU without the product library (the reference arm);
+    `prefix` keeps only the first `prefix` frames of the full trajectory
+    (same scene, same seeded perturbation), whose edges are exactly the full
+    edge list's pairs among those frames."""
     import torch
 
     import paper_2303_16878_b200 as P
     from paper_2303_16878_b200 import scenes as S
 
     c = CONFIGS[name]
-    n = n_override or c["n"]
-    graph_device = device if getattr(device, "type", "cpu") == "cuda" else None
+    n_full = n_override or c["n"]
+    n = min(prefix, n_full) if prefix else n_full
+    graph_device = device if (not host and getattr(device, "type", "cpu") == "cuda") else None
 
     t_graph = 0.0
 
     def sensor_problem(cam, scene, gt, guess, ext, max_translation, sensor_id):
         nonlocal t_graph
-        pyrs = S.device_pyramids(scene, cam, gt, ext, c["factors"], device, normals=normals)
+        gt, guess = gt[:n], guess[:n]
+        if host:
+            pyrs = host_pyramids_estimated(scene, cam, gt, ext, c["factors"], threads)
+        else:
+            pyrs = S.device_pyramids(scene, cam, gt, ext, c["factors"], device, normals=normals)
         nodes = [P.FrameNode(k, guess[k], pyrs[k], 0.1 * k, sensor_id) for k in range(n)]
         crit = P.MatchCriteria(max_translation=max_translation)
         sensor_ext = P.SensorExtrinsics(ext)
         t0 = time.perf_counter()
-        graph = P.build_graph(nodes, crit, extrinsics=sensor_ext, threads=8, device=graph_device)
+        graph = P.build_graph(nodes, crit, extrinsics=sensor_ext, threads=threads, device=graph_device)
         t_graph += time.perf_counter() - t0
         return P.BAProblem(graph, {sensor_id: sensor_ext})
 
     if c["kind"] in ("room", "hdl64", "os0", "tum"):
         if c["kind"] == "room":
-            cam, scene, gt = S.rgbd_160(), S.BoxScene(), S.room_loop(n)
+            cam, scene, gt = S.rgbd_160(), S.BoxScene(), S.room_loop(n_full)
             ext = P.Pose.identity()
         elif c["kind"] == "tum":
             cam = S.tum_640()
-            gt = S.corridor_trajectory(n, c["spacing"])
-            scene = S.corridor_scene(c["spacing"] * n + 20.0)
+            gt = S.corridor_trajectory(n_full, c["spacing"])
+            scene = S.corridor_scene(c["spacing"] * n_full + 20.0)
             ext = P.Pose(FORWARD_CAMERA, [0.0, 0.0, 0.1])
         else:
             cam = S.hdl64() if c["kind"] == "hdl64" else S.lidar_os0_128()
-            gt = S.corridor_trajectory(n, c["spacing"])
-            scene = S.corridor_scene(c["spacing"] * n + 20.0)
+            gt = S.corridor_trajectory(n_full, c["spacing"])
+            scene = S.corridor_scene(c["spacing"] * n_full + 20.0)
             ext = P.Pose.identity() if c["kind"] == "hdl64" else P.Pose(np.eye(3), [0.0, 0.0, -0.05])
         guess = S.perturb(gt, 0.05, math.radians(2.0), 11)
         problems = [sensor_problem(cam, scene, gt, guess, ext, c["max_translation"], "sensor0")]
     else:  # fused: one platform trajectory, a LiDAR and a forward RGB-D camera
         cam = S.lidar_os0_128()
-        gt = S.corridor_trajectory(n, c["spacing"])
-        scene = S.corridor_scene(c["spacing"] * n + 20.0)
+        gt = S.corridor_trajectory(n_full, c["spacing"])
+        scene = S.corridor_scene(c["spacing"] * n_full + 20.0)
         guess = S.perturb(gt, 0.05, math.radians(2.0), 11)
         problems = [
             sensor_problem(cam, scene, gt, guess, P.Pose(np.eye(3), [0.0, 0.0, -0.05]),
@@ -120,7 +171,7 @@ def build_problem(name: str, device, n_override=None, normals: str = "estimate")
             sensor_problem(S.tum_640(), scene, gt, guess, P.Pose(FORWARD_CAMERA, [0.1, 0.0, 0.1]),
                            c["max_translation_rgbd"], "rgbd0"),
         ]
-    return problems, guess, gt, dict(name=name, desc=c["desc"], frames=n, cam=cam,
+    return problems, guess[:n], gt[:n], dict(name=name, desc=c["desc"], frames=n, cam=cam,
                                      level=len(c["factors"]) - 1, graph_seconds=t_graph)
 
 
@@ -250,79 +301,122 @@ def ncu_traffic(name):
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the oracle port on a bounded sample
+# CPU baseline / reference arm: the oracle port on a host-built sample
 # ---------------------------------------------------------------------------
-def cpu_baseline(problems, guess, level, total_pp, target_seconds=12.0, threads=None):
-    """The oracle C port on all host cores over a bounded prefix of every
-    problem's pairs, extrapolated by pixel count, + the full dense LU solve."""
-    import paper_2303_16878_b200 as P
-    from oracle import oracle as O
+class ReferenceSample:
+    """A bounded sample of config `name` for the reference CPU path, built
+    entirely on the host (torch-CPU renders, numpy pyramids, host
+    build_graph; libpba_b200 is never loaded): the first `sample_frames`
+    frames of the full trajectory, whose edges are the full edge list's pairs
+    among them.  One step = what the reference does per LM iteration
+    (solver.py:505-537): linearise every sampled pair with the oracle C port
+    on all host cores (PairContext.evaluate + _edge_term), assemble them
+    densely in edge order (solver.py:428-449), solve the damped dense system
+    of the FULL dimension 6(N-1) with np.linalg.solve (solver.py:510-512) and
+    apply the step to all N poses (solver.py:451-460).  The full-iteration
+    time is extrapolated from the sample by pixel count (linearisation) and
+    pair count (assembly); c1 and c2 are sampled whole (no extrapolation)."""
 
-    threads = threads or os.cpu_count() or 1
-    cfg = P.SolverConfig()
-    rows, _ = P.se3.pose_rows(guess)
+    def __init__(self, name: str, frames: int | None = None, threads: int | None = None):
+        import paper_2303_16878_b200 as P
+        from oracle import oracle as O
 
-    def sub_problem(prob, k):
-        g = P.MatchGraph(prob.graph.nodes, prob.graph.edges[:k])
-        return P.BAProblem(g, prob.extrinsics, prob.gauge_index)
-
-    t_lin_total, parts = 0.0, []
-    for prob in problems:
-        budget = target_seconds / len(problems)
-        # calibrate on a few pairs, then size the sample to the budget
-        k = min(4, len(prob.graph.edges))
-        lp = O.OracleLevel([sub_problem(prob, k)], level, cfg)
+        c = CONFIGS[name]
+        self.name = name
+        self.threads = threads or os.cpu_count() or 1
+        n_full = frames or c["n"]
+        m = min(c["sample_frames"], n_full)
         t0 = time.perf_counter()
-        lp.records(rows, True, threads)
-        dt = max(time.perf_counter() - t0, 1e-6)
-        per_pair = dt / k * min(k, threads) / threads if k < threads else dt / k
-        k2 = int(max(k, min(len(prob.graph.edges), budget / max(per_pair, 1e-6))))
-        k2 = max(min(threads, len(prob.graph.edges)), min(k2, len(prob.graph.edges)))
-        lp = O.OracleLevel([sub_problem(prob, k2)], level, cfg)
-        sample_pp = valid_pixel_pairs(sub_problem(prob, k2), level)
+        problems, guess, _, meta = build_problem(name, None, n_full, host=True, prefix=m,
+                                                 threads=self.threads)
+        self.setup_seconds = time.perf_counter() - t0
+        self.level = meta["level"]
+        self.cam = meta["cam"]
+        self.cfg = P.SolverConfig()
+        self.rows, _ = P.se3.pose_rows(guess)
+        self.lp = O.OracleLevel(problems, self.level, self.cfg)
+        self.sample_frames = m
+        self.sample_pairs = sum(len(p.graph.edges) for p in problems)
+        self.sample_pp = problems_pixel_pairs(problems, self.level)
+        full = n_full == c["n"]
+        self.n_full = n_full
+        self.full_pairs = c["pairs"] if full else None
+        self.full_pp = c["pixel_pairs"] if full else None
+        if m == n_full:  # sampled whole
+            self.full_pairs, self.full_pp = self.sample_pairs, self.sample_pp
+        dim = 6 * (n_full - 1)
+        rng = np.random.default_rng(0)
+        A = rng.normal(size=(dim, 64))
+        self.H = A @ A.T + np.eye(dim)  # SPD stand-in of the assembled H (LU cost is data-independent)
+        self.b = rng.normal(size=dim)
+        reps = -(-n_full // m)
+        self.full_rows = np.ascontiguousarray(np.tile(self.rows, (reps, 1))[:n_full])
+        self.full_gens = np.zeros(n_full, np.int64)
+
+    def extrapolate(self, full_pairs, full_pp):
+        self.full_pairs, self.full_pp = full_pairs, full_pp
+
+    def step(self):
+        """One reference LM iteration on the sample; returns the timings (s)."""
+        from oracle import oracle as O
+
         t0 = time.perf_counter()
-        lp.records(rows, True, threads)
-        t_lin = time.perf_counter() - t0
-        full_pp = valid_pixel_pairs(prob, level)
-        t_lin_total += t_lin * (full_pp / max(sample_pp, 1))
-        parts.append(f"the first {k2} of {len(prob.graph.edges)} pairs ({sample_pp} pixel-pairs, "
-                     f"{t_lin:.2f} s)")
-    # dense LU of the reference (np.linalg.solve on dim 6(N-1)), timed in full
-    n = len(problems[0].graph.nodes)
-    dim = 6 * (n - 1)
-    rng = np.random.default_rng(0)
-    A = rng.normal(size=(dim, 64))
-    H = A @ A.T + np.eye(dim)
-    b = rng.normal(size=dim)
-    t0 = time.perf_counter()
-    np.linalg.solve(H + 1e-3 * np.diag(np.diag(H)), -b)
-    t_solve = time.perf_counter() - t0
-    gens = np.zeros(n, np.int64)
-    t0 = time.perf_counter()
-    lp.apply_step(rows, gens, np.zeros(dim))
-    t_upd = time.perf_counter() - t0
-    t_iter = t_lin_total + t_solve + t_upd
-    # one-thread rate on a small sample (BASELINE.md asks for T = 1 and T = all)
-    prob0 = problems[0]
-    k1 = min(2, len(prob0.graph.edges))
-    lp1 = O.OracleLevel([sub_problem(prob0, k1)], level, cfg)
-    pp1 = valid_pixel_pairs(sub_problem(prob0, k1), level)
-    t0 = time.perf_counter()
-    lp1.records(rows, True, 1)
-    per_px_1 = (time.perf_counter() - t0) / max(pp1, 1)
-    t_iter_1 = per_px_1 * total_pp + t_solve + t_upd
-    return {
-        "value": total_pp / t_iter,
-        "unit": "pixel-pairs/s",
-        "cores": threads,
-        "kind": "port",
-        "sample": (f"oracle C port (OpenMP {threads} threads) linearising " + "; ".join(parts) +
-                   f", extrapolated by pixel count to {total_pp}; + full np.linalg.solve dim "
-                   f"{dim} ({t_solve:.2f} s) + apply_step ({t_upd * 1e3:.1f} ms)"),
-        "gn_iteration_ms_extrapolated": t_iter * 1e3,
-        "value_1_thread": total_pp / t_iter_1,
-        "sample_1_thread": f"first {k1} pairs ({pp1} pixel-pairs) on one thread, extrapolated",
-    }
+        recs = self.lp.records(self.rows, True, self.threads)
+        t1 = time.perf_counter()
+        self.lp.assemble(recs)
+        t2 = time.perf_counter()
+        lam = self.cfg.lm_initial_lambda
+        delta = np.linalg.solve(self.H + lam * np.diag(np.diag(self.H)), -self.b)
+        t3 = time.perf_counter()
+        O.apply_step(self.full_rows, self.full_gens, 1e-9 * delta, 0)
+        t4 = time.perf_counter()
+        return {"lin": t1 - t0, "asm": t2 - t1, "solve": t3 - t2, "update": t4 - t3,
+                "wall": t4 - t0}
+
+    def iteration_seconds(self, t) -> float:
+        """Full-problem LM iteration time extrapolated from one sample step."""
+        return (t["lin"] * self.full_pp / max(self.sample_pp, 1)
+                + t["asm"] * self.full_pairs / max(self.sample_pairs, 1)
+                + t["solve"] + t["update"])
+
+    def one_thread_rate(self) -> tuple:
+        """Linearisation rate of one thread over the first two pairs."""
+        k = min(2, len(self.lp.pairs))
+        t0 = time.perf_counter()
+        self.lp.records(self.rows, True, 1, pair_subset=list(range(k)))
+        dt = time.perf_counter() - t0
+        pp = sum(self._pair_pixels(p) for p in range(k))
+        return pp / max(dt, 1e-9), f"first {k} pairs ({pp} pixel-pairs) on one thread"
+
+    def _pair_pixels(self, p) -> int:
+        src = self.lp.images[self.lp.pairs[p][2]]
+        return int(np.asarray(src.depth_valid).sum())
+
+    def describe(self, t) -> str:
+        ext = ("" if self.sample_pp == self.full_pp else
+               f", extrapolated by pixel count to {self.full_pp} ({self.full_pairs} pairs)")
+        return (f"oracle C port (OpenMP {self.threads} threads): host-built first "
+                f"{self.sample_frames} of {self.n_full} frames, {self.sample_pairs} pairs, "
+                f"{self.sample_pp} pixel-pairs linearised in {t['lin']:.2f} s + dense assembly "
+                f"{t['asm'] * 1e3:.1f} ms{ext}; + np.linalg.solve dim {6 * (self.n_full - 1)} "
+                f"({t['solve']:.2f} s) + apply_step of {self.n_full} poses "
+                f"({t['update'] * 1e3:.1f} ms)")
+
+
+def cpu_baseline(name, frames, full_pairs, full_pp):
+    """cpu_baseline object of the GPU arm's line: one warm sample step."""
+    smp = ReferenceSample(name, frames)
+    smp.extrapolate(full_pairs, full_pp)
+    smp.step()
+    t = smp.step()
+    it = smp.iteration_seconds(t)
+    rate1, desc1 = smp.one_thread_rate()
+    lin_full_1 = full_pp / rate1
+    it1 = (lin_full_1 + t["asm"] * full_pairs / max(smp.sample_pairs, 1) + t["solve"]
+           + t["update"])
+    return {"value": full_pp / it, "unit": "pixel-pairs/s", "cores": smp.threads, "kind": "port",
+            "sample": smp.describe(t), "gn_iteration_ms_extrapolated": it * 1e3,
+            "value_1_thread": full_pp / it1, "sample_1_thread": desc1 + ", extrapolated"}
 
 
 # ---------------------------------------------------------------------------
@@ -474,8 +568,7 @@ def run_ours(args):
     if trafficd and trafficd.get("dram_bytes_per_pixel_pair"):
         traffic = trafficd["dram_bytes_per_pixel_pair"] * shard_pp
     line = {
-        "metric": "GN iteration throughput: pixel-pair residuals/s (one LM iteration at the "
-                  "finest level: solve + pose update + linearise + assemble)",
+        "metric": METRIC,
         "value": total_pp / (ms_per_step / 1e3),
         "unit": "pixel-pairs/s",
         "n_gpus": world,
@@ -487,17 +580,13 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
-        "config": {
-            "workload": f"{args.config}: {meta['desc']}",
-            "frames": meta["frames"],
-            "pairs": n_pairs,
-            "pixel_pairs_per_iteration": total_pp,
-            "level": f"finest ({meta['cam'].height}x{meta['cam'].width})",
-            "parallelism": f"pair-sharded x{world}" if world > 1 else "single GPU",
+        "config": workload_config(args.config, meta["cam"], meta["frames"], n_pairs, total_pp,
+                                  solver),
+        "parallelism": f"pair-sharded x{world}" if world > 1 else "single GPU",
+        "setup": {
             "l2": "inputs larger than L2: %.1f GB of resident texels" % (store.texel_bytes() / 1e9),
             "precision": "fp64 throughout (geometry, residuals, Jacobians, H/b/cost sums)",
             "gn_iteration_ms": ms_per_step,
-            "linear_solver": solver,
             "setup_seconds": round(t_setup, 2),
             "graph_seconds": round(meta["graph_seconds"], 2),
             "initial_cost": cost0,
@@ -525,7 +614,7 @@ def run_ours(args):
         "clocks": clocks.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(problems, guess, level, total_pp)
+        line["cpu_baseline"] = cpu_baseline(args.config, args.frames, n_pairs, total_pp)
     print(json.dumps(line), flush=True)
     if dist.is_initialized():
         dist.destroy_process_group()
@@ -544,42 +633,52 @@ def valid_pixel_pairs_shard(prob, level, local_level):
 # reference arm: the oracle port on the host cores (rank 0 only)
 # ---------------------------------------------------------------------------
 def run_reference(args):
+    """`--impl reference`: the reference path on the host cores (the oracle C
+    port, since the reference itself is numpy and cannot run on the GPU box),
+    on a host-built bounded sample (ReferenceSample) — no GPU, no product
+    library.  ms_per_step is the measured wall time of each sample step;
+    value is the full-iteration throughput extrapolated from it."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
-    import torch
-
-    device = torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
-    problems, guess, gt, meta = build_problem(args.config, device, args.frames)
-    level = meta["level"]
-    total_pp = problems_pixel_pairs(problems, level)
-    vals = []
-    for k in range(args.warmup + args.steps):
-        cb = cpu_baseline(problems, guess, level, total_pp, target_seconds=args.ref_seconds)
-        if k >= args.warmup:
-            vals.append(cb)
-    v = statistics.median(c["value"] for c in vals)
-    ms = statistics.median(c["gn_iteration_ms_extrapolated"] for c in vals)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    smp = ReferenceSample(args.config, args.frames)
+    c = CONFIGS[args.config]
+    if smp.full_pp is None:  # --frames override: no committed constants for that size
+        raise SystemExit("--impl reference needs the configured frame count (or a whole sample)")
+    for _ in range(args.warmup):
+        smp.step()
+    ts = [smp.step() for _ in range(args.steps)]
+    walls = [t["wall"] for t in ts]
+    its = [smp.iteration_seconds(t) for t in ts]
+    it = statistics.median(its)
+    v = smp.full_pp / it
+    t_med = ts[its.index(sorted(its)[len(its) // 2])]
+    solver = args.solver or c.get("solver", "cholesky")
     line = {
         "impl": "reference",
-        "metric": "GN iteration throughput: pixel-pair residuals/s (one LM iteration at the "
-                  "finest level: solve + pose update + linearise + assemble)",
+        "metric": METRIC,
         "value": v,
         "unit": "pixel-pairs/s",
-        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": ms,
+        "ms_per_step": statistics.mean(walls) * 1e3,
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"{args.config}: {meta['desc']}", "frames": meta["frames"],
-                   "pairs": sum(len(p.graph.edges) for p in problems),
-                   "pixel_pairs_per_iteration": total_pp},
-        "cpu_baseline": {"value": v, "unit": "pixel-pairs/s", "cores": vals[-1]["cores"],
-                         "kind": "port", "sample": vals[-1]["sample"]},
+        "config": workload_config(args.config, smp.cam, smp.n_full, smp.full_pairs, smp.full_pp,
+                                  solver),
+        "parallelism": f"host cores ({smp.threads} threads)",
+        "gn_iteration_ms_extrapolated": it * 1e3,
+        "sample_step_ms": {k: statistics.mean(t[k] for t in ts) * 1e3
+                           for k in ("lin", "asm", "solve", "update", "wall")},
+        "setup": {"setup_seconds": round(smp.setup_seconds, 2),
+                  "inputs": "host-built: torch-CPU renders, numpy pyramids, host build_graph"},
+        "cpu_baseline": {"value": v, "unit": "pixel-pairs/s", "cores": smp.threads,
+                         "kind": "port", "sample": smp.describe(t_med)},
         "e2e": {"value": v, "unit": "pixel-pairs/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -598,7 +697,6 @@ def main():
     ap.add_argument("--solver", default=None, choices=["cholesky", "pcg"],
                     help="damped-system solver (default: pcg for c3, cholesky otherwise)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-seconds", type=float, default=4.0)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -324,20 +324,25 @@ class OracleLevel:
         return total, count, h, b
 
     def apply_step(self, pose_arr, gens, delta):
-        out = pose_arr.copy()
-        g_out = gens.copy()
-        s = 0
-        for k in range(self.n_poses):
-            if k == self.gauge:
-                continue
-            R = pose_arr[k, :9].reshape(3, 3)
-            t = pose_arr[k, 9:]
-            R2, t2, g2 = boxplus(R, t, int(gens[k]), delta[s:s + 6])
-            out[k, :9] = R2.reshape(9)
-            out[k, 9:] = t2
-            g_out[k] = g2
-            s += 6
-        return out, g_out
+        return apply_step(pose_arr, gens, delta, self.gauge)
+
+
+def apply_step(pose_arr, gens, delta, gauge):
+    """_LevelProblem.apply_step (solver.py:451-460): boxplus every non-gauge pose."""
+    out = pose_arr.copy()
+    g_out = gens.copy()
+    s = 0
+    for k in range(pose_arr.shape[0]):
+        if k == gauge:
+            continue
+        R = pose_arr[k, :9].reshape(3, 3)
+        t = pose_arr[k, 9:]
+        R2, t2, g2 = boxplus(R, t, int(gens[k]), delta[s:s + 6])
+        out[k, :9] = R2.reshape(9)
+        out[k, 9:] = t2
+        g_out[k] = g2
+        s += 6
+    return out, g_out
 
 
 @dataclass
