@@ -442,8 +442,6 @@ def run_ours(args):
 
     t_setup = time.perf_counter()
     problems, guess, gt, meta = build_problem(args.config, device, args.frames)
-    if len(problems) > 1 and (world > 1 or os.environ.get("PBA_FORCE_SHARDED") == "1"):
-        raise SystemExit("fused (multi-sensor) configs are benchmarked on one GPU")
     level = meta["level"]
     solver = args.solver or CONFIGS[args.config].get("solver", "cholesky")
     cfg = P.SolverConfig(linear_solver=solver)
@@ -560,8 +558,7 @@ def run_ours(args):
 
     peak, peak_kind = measured_peak_hbm()
     lin_avg_ms = statistics.mean(lin_ms) if lin_ms else float("nan")
-    my_pp = getattr(local_level, "pixels_shard", None)
-    shard_pp = total_pp if world == 1 else valid_pixel_pairs_shard(problems[0], level, local_level)
+    shard_pp = total_pp if world == 1 else valid_pixel_pairs_shard(problems, level, local_level)
     achieved = shard_pp * BYTES_PER_PIXEL_PAIR / (lin_avg_ms / 1e3) / 1e9
     trafficd = ncu_traffic(args.config)
     traffic = None
@@ -621,12 +618,22 @@ def run_ours(args):
     return line
 
 
-def valid_pixel_pairs_shard(prob, level, local_level):
+def valid_pixel_pairs_shard(problems, level, local_level):
+    """Depth-valid source pixels of this rank's slice [pair_lo, pair_hi) of
+    the concatenated edge list (problem 0's edges, then problem 1's: the
+    DeviceLevel pair order, so fused c5 shards like the others)."""
     import paper_2303_16878_b200 as P
 
     lo, hi = local_level.pair_lo, local_level.pair_hi
-    g = P.MatchGraph(prob.graph.nodes, prob.graph.edges[lo:hi])
-    return valid_pixel_pairs(P.BAProblem(g, prob.extrinsics, prob.gauge_index), level)
+    total, base = 0, 0
+    for prob in problems:
+        n = len(prob.graph.edges)
+        a, b = max(lo - base, 0), min(hi - base, n)
+        if b > a:
+            g = P.MatchGraph(prob.graph.nodes, prob.graph.edges[a:b])
+            total += valid_pixel_pairs(P.BAProblem(g, prob.extrinsics, prob.gauge_index), level)
+        base += n
+    return total
 
 
 # ---------------------------------------------------------------------------

@@ -189,11 +189,14 @@ class _Runtime:
         torch.cuda.set_device(self.device)
         self.store = FrameStore(self.device)
 
-    def level(self, problems, level, cfg, tolerance_override=None):
+    def level(self, problems, level, cfg, tolerance_override=None, need_solver=True):
+        """The level backend; need_solver=False (the cost-only path) skips the
+        assembly plan and the dense H / Cholesky buffers (O(N^2) memory)."""
         from . import distributed
 
         return distributed.make_level(problems, level, cfg, self.store, self.group,
-                                      tolerance_override=tolerance_override)
+                                      tolerance_override=tolerance_override,
+                                      need_solver=need_solver)
 
 
 def _lm_level(backend, level: int, cfg: SolverConfig, max_iterations: int):
@@ -249,6 +252,7 @@ def _hierarchical(problems, cfg, initial, levels, runtime=None) -> SolveResult:
     records, level_times = [], []
     for pos, level in enumerate(schedule):
         t0 = time.perf_counter()
+        backend = None  # free the previous level's solver buffers before allocating the next
         backend = rt.level(problems, level, cfg)
         backend.set_poses(rows, gens)
         records.extend(_lm_level(backend, level, cfg, caps[pos]))
@@ -306,6 +310,7 @@ def total_error(problem: BAProblem, poses=None, level: int = 0, cfg: SolverConfi
         poses = [n.pose_guess for n in problem.graph.nodes]
     rt = _Runtime()
     backend = rt.level([problem], level, cfg,
-                       tolerance_override=None if suppress_occlusions else float("inf"))
+                       tolerance_override=None if suppress_occlusions else float("inf"),
+                       need_solver=False)
     rows, gens = pose_rows(poses)
     return backend.cost_only(rows)

@@ -211,15 +211,16 @@ __global__ void __launch_bounds__(1024) potrf_inv_kernel(double* __restrict__ A,
   }
 }
 
-// Register-panel variant of potrf_inv (256 threads).  The tile is factored
-// in four 16-column panels; warp 0 factors a panel with the panel rows in
-// registers (lane l owns rows l and l + 32, 2 x 16 doubles), pivots and
-// column entries exchanged by shuffles, so a column step is a shuffle, an
-// rsqrt and one FMA wave with no shared-memory round trip.  All eight warps
-// then apply the rank-16 trailing update.  The inverse is blocked 16x16:
-// the four diagonal-block inverses in parallel (one warp each), then the
-// three block rows below with two barriers each.  Rows past the matrix end
-// are identity, so every tile runs the same schedule.
+// Register-panel variant of potrf_inv (256 threads).  The NB = 64 tile is
+// factored in NB / PW = 8 panels of PW = 8 columns; warp 0 factors a panel
+// with the panel rows in registers (lane l owns rows l and l + 32, 2 x PW
+// doubles), pivots and column entries exchanged by shuffles, so a column
+// step is a shuffle, an rsqrt and one FMA wave with no shared-memory round
+// trip.  All eight warps then apply the rank-PW trailing update.  The
+// inverse is blocked PW x PW: the NB / PW diagonal-block inverses in
+// parallel (warp w < NB / PW inverts block w, lanes < PW own its columns),
+// then the NB / PW - 1 block rows below with two barriers each.  Rows past
+// the matrix end are identity, so every tile runs the same schedule.
 constexpr int PW = 8;  // panel width
 
 template <bool kRB>
@@ -367,7 +368,7 @@ __global__ void __launch_bounds__(256) potrf_reg_kernel(double* __restrict__ A, 
     if (tid == 0) *status = 1;
     return;
   }
-  // inverse, diagonal blocks: warp b < 4 inverts L_bb, lane c < 16 owns column c
+  // inverse, diagonal blocks: warp b < NB / PW inverts L_bb, lane c < PW owns column c
   if (warp < NB / PW && lane < PW) {
     const int o = warp * PW, c = lane;
     for (int i = 0; i < PW; ++i) {
@@ -377,7 +378,7 @@ __global__ void __launch_bounds__(256) potrf_reg_kernel(double* __restrict__ A, 
     }
   }
   __syncthreads();
-  // block rows i = 1..3: T_ij = sum_{k=j}^{i-1} L_ik X_kj, then X_ij = -X_ii T_ij
+  // block rows i = 1 .. NB/PW - 1: T_ij = sum_{k=j}^{i-1} L_ik X_kj, then X_ij = -X_ii T_ij
   for (int bi = 1; bi < NB / PW; ++bi) {
     const int oi = bi * PW;
     for (int e = tid; e < bi * PW * PW; e += blockDim.x) {

@@ -23,7 +23,8 @@ import torch
 from . import native as N
 from .camera import PINHOLE, ray_table
 
-THREADS_PER_CHUNK = 256
+PIXELS_PER_CHUNK_UNIT = 256  # chunk sizes are multiples of this
+MAX_CHUNK_UNITS = 32         # <= 8192 pixels per chunk: 64 per thread of K1's 128-thread CTA
 SM_COUNT = 148
 
 
@@ -43,12 +44,14 @@ def _struct_tensor(arr, device) -> torch.Tensor:
 
 
 def chunk_pixels_for(total_pixels: int) -> int:
-    """Source pixels per CTA.  Chosen from the whole level problem (never
-    from a shard) so per-pair sums are identical for any GPU count: enough
-    CTAs for ~4 waves of 148 SMs, at most 32 pixels per thread."""
-    ppt = total_pixels // (THREADS_PER_CHUNK * SM_COUNT * 4)
-    ppt = max(1, min(32, int(ppt)))
-    return THREADS_PER_CHUNK * ppt
+    """Source pixels per K1 CTA (chunk).  Chosen from the whole level problem
+    (never from a shard) so per-pair sums are identical for any GPU count:
+    enough chunks for ~4 waves over 148 SMs, in multiples of 256 pixels, at
+    most 8192 (the measured optimum on c4: 64 pixels per thread of the
+    128-thread CTA, DESIGN.md §3 K1)."""
+    units = total_pixels // (PIXELS_PER_CHUNK_UNIT * SM_COUNT * 4)
+    units = max(1, min(MAX_CHUNK_UNITS, int(units)))
+    return PIXELS_PER_CHUNK_UNIT * units
 
 
 def block_rows(slot_of_pose, pose_i, pose_j):

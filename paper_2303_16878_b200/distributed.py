@@ -6,7 +6,7 @@ contiguous ranges balanced by source-pixel count; every rank keeps all
 frames and poses resident and linearises only its range.  Per LM
 evaluation the exchange is:
 
-  rank r: records of its pairs (|E_r| x 92 fp64)  --all_gather-->  rank 0
+  rank r: records of its pairs (|E_r| x 92 fp64)  --gather-->  rank 0
   rank 0: fixed-edge-order assembly (identical to the single-GPU order),
           damped solve, pose update
   rank 0 --broadcast--> candidate poses (N x 12 fp64) + scalars
@@ -87,17 +87,25 @@ class ShardedLevel:
         self.max_local = max(1, max(hi - lo for lo, hi in ranges))
         dev = local.device
         self._send = torch.zeros((self.max_local, 92), dtype=torch.float64, device=dev)
-        self._gather = torch.zeros((self.world * self.max_local, 92), dtype=torch.float64,
-                                   device=dev)
-        self._full = torch.zeros((max(1, ranges[-1][1]), 92), dtype=torch.float64, device=dev)
+        # receive buffer on rank 0 only (the other ranks never read records)
+        self._gather = torch.zeros((self.world * self.max_local if self.rank == 0 else 1, 92),
+                                   dtype=torch.float64, device=dev)
+        self._full = torch.zeros((max(1, ranges[-1][1]) if self.rank == 0 else 1, 92),
+                                 dtype=torch.float64, device=dev)
 
     # -- helpers ---------------------------------------------------------------
     def _gather_records(self, recs: torch.Tensor) -> torch.Tensor:
+        """Records of every shard to rank 0 only (dist.gather: each rank
+        sends max_local x 92 doubles, only rank 0 receives), then placed in
+        edge order on rank 0."""
         n = recs.shape[0]
-        self._send.zero_()
         if n:
             self._send[:n].copy_(recs)
-        dist.all_gather_into_tensor(self._gather, self._send, group=self.group)
+        if n < self.max_local:
+            self._send[n:].zero_()
+        parts = (list(self._gather.view(self.world, self.max_local, 92).unbind(0))
+                 if self.rank == 0 else None)
+        dist.gather(self._send, parts, dst=0, group=self.group)
         if self.rank != 0:
             return self._full
         for r, (lo, hi) in enumerate(self.ranges):
@@ -168,15 +176,18 @@ def pair_pixels(problems, level, cfg) -> list:
     return out
 
 
-def make_level(problems, level, cfg, store, group, tolerance_override=None):
-    """Single-GPU DeviceLevel, or a ShardedLevel over the process group."""
+def make_level(problems, level, cfg, store, group, tolerance_override=None, need_solver=True):
+    """Single-GPU DeviceLevel, or a ShardedLevel over the process group.
+    need_solver=False builds no assembly plan / solve buffers (cost-only)."""
     from .device import DeviceLevel
 
     if group is None:
-        return DeviceLevel(problems, level, cfg, store, tolerance_override=tolerance_override)
+        return DeviceLevel(problems, level, cfg, store, assemble=need_solver,
+                           tolerance_override=tolerance_override)
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     ranges = shard_ranges(pair_pixels(problems, level, cfg), world)
     local = DeviceLevel(problems, level, cfg, store, pair_range=ranges[rank],
-                        assemble=(rank == 0), tolerance_override=tolerance_override)
+                        assemble=(rank == 0 and need_solver),
+                        tolerance_override=tolerance_override)
     return ShardedLevel(local, group, ranges)

@@ -1,7 +1,7 @@
-"""Multi-rank host logic on CPU: world_size 2 over gloo.
+"""Multi-rank host logic on CPU: world sizes 2 and 3 over gloo.
 
 The product's multi-GPU backend (`distributed.ShardedLevel`) shards the
-edge-ordered pair list, all-gathers per-pair records to rank 0, assembles
+edge-ordered pair list, gathers per-pair records to rank 0, assembles
 and solves there and broadcasts poses and scalars.  Here each rank's
 per-pair compute is the oracle (injected by this test through the same
 interface `device.DeviceLevel` provides), so the sharding, gather order,
@@ -106,7 +106,13 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, name, out_q):
+def _uneven_ranges(n_pairs, world):
+    """A deliberately unbalanced split with an empty shard in the middle."""
+    cut = max(1, n_pairs // 5)
+    return [(0, cut)] + [(cut, cut)] * (world - 2) + [(cut, n_pairs)]
+
+
+def _worker(rank, world, port, name, out_q, gauge=0, uneven=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -116,12 +122,15 @@ def _worker(rank, world, port, name, out_q):
 
         d = F.load(name)
         prob, _ = F.single_problem(d)
+        prob.gauge_index = gauge
         cfg = P.SolverConfig()
         n_levels = len(d["scales"])
         rows, gens = P.se3.pose_rows(F.poses(d["guess"]))
         records = []
         for level in range(n_levels):
             ranges = D.shard_ranges(D.pair_pixels([prob], level, cfg), world)
+            if uneven:
+                ranges = _uneven_ranges(len(prob.graph.edges), world)
             local = OracleShard([prob], level, cfg, ranges[rank], solver=(rank == 0))
             backend = D.ShardedLevel(local, dist.group.WORLD, ranges)
             backend.set_poses(rows, gens)
@@ -138,12 +147,18 @@ def _worker(rank, world, port, name, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name", ["pinhole_small", "spherical_small"])
-def test_two_rank_gloo_solve_equals_single_process(name):
+@pytest.mark.parametrize("name,world,gauge,uneven", [
+    ("pinhole_small", 2, 0, False), ("spherical_small", 2, 0, False),
+    ("pinhole_small", 3, 2, True), ("spherical_small", 3, 3, False)])
+def test_multi_rank_gloo_solve_equals_single_process(name, world, gauge, uneven):
+    """2 and 3 ranks, balanced and unbalanced shards (one of them empty),
+    gauge 0 and non-zero: every rank ends with the same poses and LM trace,
+    bit-identical to the single-process oracle solve."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, q, gauge, uneven))
+             for r in range(world)]
     for p in procs:
         p.start()
     results = [q.get(timeout=300) for _ in procs]
@@ -151,21 +166,37 @@ def test_two_rank_gloo_solve_equals_single_process(name):
         p.join(timeout=60)
         assert p.exitcode == 0
     results.sort(key=lambda t: t[0])
-    (_, rows0, recs0), (_, rows1, recs1) = results
-    assert np.array_equal(rows0, rows1)          # every rank ends with the same poses
-    assert recs0 == recs1                        # and took the same LM decisions
+    _, rows0, recs0 = results[0]
+    for _, rows_r, recs_r in results[1:]:
+        assert np.array_equal(rows0, rows_r)     # every rank ends with the same poses
+        assert recs0 == recs_r                   # and took the same LM decisions
 
     # single-process oracle run (same LM restatement, no sharding)
     import paper_2303_16878_b200 as P
 
     d = F.load(name)
     prob, _ = F.single_problem(d)
+    prob.gauge_index = gauge
     final, ref_records = O.hierarchical([prob], P.SolverConfig())
     lm = [r for r in recs0 if r[0] != "total"]
     assert [(r[0], r[1], r[5], r[4]) for r in lm] == [
         (r.level, r.iteration, r.accepted, r.valid_blocks) for r in ref_records]
     assert [r[3] for r in lm] == [r.error for r in ref_records]  # bit-identical costs
     assert np.array_equal(rows0, final)
-    # and the reference's own trace (golden)
-    trace = d["trace"]
-    assert [(r[0], r[1], int(r[5])) for r in lm] == [(int(t[0]), int(t[1]), int(t[5])) for t in trace]
+    if gauge:
+        assert np.array_equal(rows0[gauge], P.se3.pose_rows(F.poses(d["guess"]))[0][gauge])
+    else:  # and the reference's own trace (golden)
+        trace = d["trace"]
+        assert [(r[0], r[1], int(r[5])) for r in lm] == [
+            (int(t[0]), int(t[1]), int(t[5])) for t in trace]
+
+
+def test_shard_ranges_balanced_and_contiguous():
+    from paper_2303_16878_b200 import distributed as D
+
+    px = [100] * 7 + [400] * 3
+    for world in (1, 2, 3, 4, 8, 16):
+        r = D.shard_ranges(px, world)
+        assert len(r) == world and r[0][0] == 0 and r[-1][1] == len(px)
+        assert all(a[1] == b[0] for a, b in zip(r, r[1:]))
+    assert D.shard_ranges(px, 2) == [(0, 8), (8, 10)]
