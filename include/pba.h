@@ -259,10 +259,19 @@ size_t pba_normals_scratch_bytes(const pba_camera* cam, int32_t n_frames);
  * camera (device (n, H, W) fp64, raw: non-finite and out-of-range pixels are
  * invalid) -> observer-facing unit normals (device (n, H, W, 3), zero where
  * no plane fits).  ray_table: pba_ray_table_doubles(cam) doubles (device).
- * Bit-equal to the reference up to the 3x3 eigenproblem (see pyramid.cu). */
+ * Bit-equal to the reference up to the 3x3 eigenproblem (cues.py:239,
+ * numpy.linalg.eigh), which is solved by Jacobi; every pixel whose gates
+ * or normal could differ under LAPACK is left zero and listed in `recheck`
+ * (device, recheck_capacity records of PBA_NORMALS_RECHECK_DOUBLES doubles:
+ * [flat pixel index f*H*W + p, S00, S11, S22, S10, S20, S21, x, y, z]) for
+ * the caller to decide with eigh; *recheck_count (device int32) receives
+ * the number of such pixels (records beyond the capacity are dropped: call
+ * again with a larger buffer). */
+#define PBA_NORMALS_RECHECK_DOUBLES 10
 int pba_estimate_normals(const pba_camera* cam, const double* ray_table, const double* depth,
                          int32_t n_frames, const pba_normal_config* cfg, double* normals,
-                         void* scratch, void* stream);
+                         void* scratch, double* recheck, int32_t recheck_capacity,
+                         int32_t* recheck_count, void* stream);
 /* _downscale_cues (cues.py:278-326) of n_frames full-resolution cue sets
  * (cam = full-resolution camera; depth already cleaned of non-finite values
  * as build_pyramid does) to one level of scale s: out_h/out_w must equal

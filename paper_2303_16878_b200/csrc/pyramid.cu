@@ -162,12 +162,22 @@ __device__ __forceinline__ double sat_at(const double* __restrict__ s, int W, in
   return (R == 0 || C == 0) ? 0.0 : s[(int64_t)(R - 1) * W + (C - 1)];
 }
 
+// A pixel whose decision (planarity, grazing, orientation) or normal value
+// could come out differently under LAPACK's eigensolver is written as zero
+// and listed for the host, which re-decides it with numpy.linalg.eigh on the
+// same (bit-equal) scatter matrix: record = [pixel index, S00, S11, S22,
+// S10, S20, S21, x, y, z] (the lower triangle eigh reads, and the point).
+constexpr int kRecheckDoubles = 10;
+
 __global__ void __launch_bounds__(128, 6) normals_kernel(pba_camera cam,
                                                       const double* __restrict__ tab,
                                                       const double* __restrict__ depth,
                                                       const double* __restrict__ sat,
                                                       pba_normal_config cfg,
-                                                      double* __restrict__ normals) {
+                                                      double* __restrict__ normals,
+                                                      double* __restrict__ recheck,
+                                                      int recheck_cap,
+                                                      int* __restrict__ recheck_count) {
   const int W = cam.width, H = cam.height;
   const int64_t plane = (int64_t)H * W;
   const int64_t px = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -206,6 +216,7 @@ __global__ void __launch_bounds__(128, 6) normals_kernel(pba_camera cam,
   double o01 = __dsub_rn(win[4], __dmul_rn(c1, mu0));
   double o02 = __dsub_rn(win[5], __dmul_rn(c2, mu0));
   double o12 = __dsub_rn(win[7], __dmul_rn(c2, mu1));
+  const double s00 = dg[0], s11 = dg[1], s22 = dg[2], s10 = o01, s20 = o02, s21 = o12;
   double V[3][3] = {{1.0, 0.0, 0.0}, {0.0, 1.0, 0.0}, {0.0, 0.0, 1.0}};
   for (int sweep = 0; sweep < 12; ++sweep) {
     if (o01 == 0.0 && o02 == 0.0 && o12 == 0.0) break;
@@ -221,14 +232,38 @@ __global__ void __launch_bounds__(128, 6) normals_kernel(pba_camera cam,
   if (lb > lc) { const double t = lb; lb = lc; lc = t; const int u = i1; i1 = i2; i2 = u; }
   if (la > lb) { const double t = la; la = lb; lb = t; const int u = i0; i0 = i1; i1 = u; }
   auto pick = [](double a, double b, double c, int i) { return i == 0 ? a : (i == 1 ? b : c); };
-  const bool planar = lb > fmax(__dmul_rn(cfg.degeneracy_ratio, lc), 0.0);
+  const double thr = fmax(__dmul_rn(cfg.degeneracy_ratio, lc), 0.0);
   double n0 = pick(V[0][0], V[0][1], V[0][2], i0);
   double n1 = pick(V[1][0], V[1][1], V[1][2], i0);
   double n2 = pick(V[2][0], V[2][1], V[2][2], i0);
   const double facing = __dadd_rn(__dadd_rn(__dmul_rn(n0, x), __dmul_rn(n1, y)), __dmul_rn(n2, z));
   if (facing > 0.0) n0 = -n0, n1 = -n1, n2 = -n2;
-  if (planar && fabs(facing) > 1e-12 && isfinite(n0) && isfinite(n1) && isfinite(n2)) {
+  // Certainty margins against any backward-stable 3x3 eigensolver (LAPACK
+  // dsyevd or this Jacobi; both within ~10 eps ||S||): eigenvalues within
+  // m_l = 1e-12 ||S||, the eigenvector within err_n = 1e-12 ||S|| / gap,
+  // so facing = n . p within m_f = 4 |p| err_n (+ rounding).  Outside the
+  // margins the gates decide identically and the normal agrees to <= 1e-10.
+  const double snorm = fmax(fabs(la), fabs(lc));
+  const double m_l = 1e-12 * snorm;
+  const double gap = lb - la;
+  const double err_n = gap > 0.0 ? 1e-12 * snorm / gap + 1e-15 : INFINITY;
+  const double pn = sqrt(x * x + y * y + z * z);
+  const double m_f = 4.0 * pn * err_n + 1e-15 * pn;
+  const double af = fabs(facing);
+  const bool finite = isfinite(n0) && isfinite(n1) && isfinite(n2);
+  const bool surely_not = lb < thr - m_l || af < 1e-12 - m_f;
+  const bool surely = lb > thr + m_l && af > 1e-12 + m_f && err_n <= 1e-10 && finite;
+  if (surely_not) return;
+  if (surely) {
     out[0] = n0, out[1] = n1, out[2] = n2;
+    return;
+  }
+  const int k = atomicAdd(recheck_count, 1);
+  if (k < recheck_cap) {
+    double* rec = recheck + (int64_t)k * kRecheckDoubles;
+    rec[0] = (double)(f * plane + px);
+    rec[1] = s00, rec[2] = s11, rec[3] = s22, rec[4] = s10, rec[5] = s20, rec[6] = s21;
+    rec[7] = x, rec[8] = y, rec[9] = z;
   }
 }
 
@@ -331,13 +366,17 @@ extern "C" size_t pba_normals_scratch_bytes(const pba_camera* cam, int32_t n_fra
 extern "C" int pba_estimate_normals(const pba_camera* cam, const double* ray_table,
                                     const double* depth, int32_t n_frames,
                                     const pba_normal_config* cfg, double* normals, void* scratch,
-                                    void* stream) {
+                                    double* recheck, int32_t recheck_capacity,
+                                    int32_t* recheck_count, void* stream) {
   PBA_ARG_CHECK(cam && cfg, "NULL camera/config");
   PBA_ARG_CHECK(n_frames >= 0, "n_frames < 0");
+  PBA_ARG_CHECK(recheck_count && recheck_capacity >= 0 && (recheck || recheck_capacity == 0),
+                "bad recheck buffer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  PBA_CUDA_TRY(cudaMemsetAsync(recheck_count, 0, sizeof(int32_t), st));
   if (n_frames == 0 || cam->width == 0 || cam->height == 0) return PBA_OK;
   PBA_ARG_CHECK(n_frames <= 65535, "n_frames > 65535 per call");
   PBA_ARG_CHECK(ray_table && depth && normals && scratch, "NULL buffer");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
   double* sat = static_cast<double*>(scratch);
   const int W = cam->width, H = cam->height;
   moment_colscan_kernel<<<dim3((W + 127) / 128, n_frames), 128, 0, st>>>(*cam, ray_table, depth,
@@ -348,7 +387,7 @@ extern "C" int pba_estimate_normals(const pba_camera* cam, const double* ray_tab
   PBA_LAUNCH_CHECK();
   const int64_t plane = (int64_t)H * W;
   normals_kernel<<<dim3((unsigned)((plane + 127) / 128), n_frames), 128, 0, st>>>(
-      *cam, ray_table, depth, sat, *cfg, normals);
+      *cam, ray_table, depth, sat, *cfg, normals, recheck, recheck_capacity, recheck_count);
   PBA_LAUNCH_CHECK();
   return PBA_OK;
 }

@@ -323,15 +323,24 @@ def estimate_normals(depth: np.ndarray, cam: Intrinsics, cfg: NormalConfig | Non
     # lower triangle is what the symmetric eigensolver reads)
     S = win[:, (3, 4, 5, 4, 6, 7, 5, 7, 8)].reshape(-1, 3, 3)
     S = S - (cnt[:, None] * mu)[:, :, None] * mu[:, None, :]
+    n, ok = plane_normals(S, pts[rr, cc], cfg.degeneracy_ratio)
+    out[rr[ok], cc[ok]] = n[ok]
+    return out
+
+
+def plane_normals(S: np.ndarray, p: np.ndarray, degeneracy_ratio: float):
+    """The eigen step and gates of estimate_normals (cues.py:239-245) for a
+    stack of scatter matrices S (k, 3, 3; eigh reads the lower triangle) and
+    their points p (k, 3): the observer-facing smallest eigenvector and
+    whether it passes the planarity, grazing and finiteness gates.  The GPU
+    builder (pyramid_device.py) calls this for the pixels it cannot decide."""
     lam, vec = np.linalg.eigh(S)
     n = vec[:, :, 0]
-    planar = lam[:, 1] > np.maximum(cfg.degeneracy_ratio * lam[:, 2], 0.0)
-    p = pts[rr, cc]
+    planar = lam[:, 1] > np.maximum(degeneracy_ratio * lam[:, 2], 0.0)
     facing = np.einsum("ij,ij->i", n, p)
     n = np.where(facing[:, None] > 0.0, -n, n)
     ok = planar & (np.abs(facing) > 1e-12) & np.isfinite(n).all(axis=1)
-    out[rr[ok], cc[ok]] = n[ok]
-    return out
+    return n, ok
 
 
 def build_cue_image(intensity, depth, cam: Intrinsics, cfg: NormalConfig | None = None,

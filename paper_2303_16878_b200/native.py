@@ -25,6 +25,7 @@ PBA_RASTER_U16_DEPTH = 2
 PBA_PINHOLE = 0
 PBA_SPHERICAL = 1
 RECORD_DOUBLES = 92
+NORMALS_RECHECK_DOUBLES = 10
 PARTIAL_DOUBLES = 32
 
 # symbols declared in include/pba.h, in header order
@@ -105,7 +106,8 @@ _SIGNATURES = {
     "pba_overlap_counts": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _dbl, _vp, _vp]),
     "pba_normals_scratch_bytes": (_sz, [ctypes.POINTER(Camera), _i32]),
     "pba_estimate_normals": (ctypes.c_int, [ctypes.POINTER(Camera), _vp, _vp, _i32,
-                                            ctypes.POINTER(NormalConfigC), _vp, _vp, _vp]),
+                                            ctypes.POINTER(NormalConfigC), _vp, _vp, _vp, _i32,
+                                            _vp, _vp]),
     "pba_downscale_cues": (ctypes.c_int, [ctypes.POINTER(Camera), _dbl, _i32, _vp, _vp, _vp,
                                           _i32, _i32, _vp, _vp, _vp, _vp]),
     "pba_decode_raster": (ctypes.c_int, [_vp, _i64, _i32, _dbl, _vp, _vp]),

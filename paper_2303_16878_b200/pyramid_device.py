@@ -8,17 +8,20 @@ in HBM and come out as `DeviceCueImage` levels, which the device frame store
 turns into texels without a host round trip.
 
 Parity: intensity, depth and the downscale are bit-equal to the reference;
-normals agree to the eigen-solver's precision (Jacobi vs LAPACK), see
-pyramid.cu and DESIGN.md.
+normal validity is bit-exact (knife-edge pixels re-decided with eigh on the
+host) and the normals agree to <= 1e-10 (Jacobi vs LAPACK), see pyramid.cu
+and DESIGN.md.
 """
 
 from __future__ import annotations
 
+import numpy as np
 import torch
 
 from . import native as N
 from .camera import Intrinsics, ray_table
-from .cueimage import CuePyramid, DeviceCueImage, NormalConfig, footprint_index, validate_scales
+from .cueimage import (CuePyramid, DeviceCueImage, NormalConfig, footprint_index, plane_normals,
+                       validate_scales)
 from .device import camera_struct
 
 _SCRATCH_BUDGET = 1 << 30  # bytes of moment table per batch
@@ -48,11 +51,23 @@ def _frames_per_batch(lib, cs, n: int) -> int:
     return max(1, min(n, 65535, _SCRATCH_BUDGET // max(per, 1)))
 
 
+last_recheck_count = 0  # pixels re-decided on the host by the last call (diagnostics)
+
+
 def estimate_normals_device(depth, cam: Intrinsics, cfg: NormalConfig | None = None,
-                            device=None) -> torch.Tensor:
+                            device=None, recheck_capacity: int | None = None) -> torch.Tensor:
     """estimate_normals (cues.py:187-246) of (H, W) or (n, H, W) depth/range
-    images on the GPU; returns (.., H, W, 3) fp64 normals on the device."""
+    images on the GPU; returns (.., H, W, 3) fp64 normals on the device.
+
+    The 3x3 eigenproblem runs as Jacobi on the device; the pixels whose
+    gates or normal could differ under numpy.linalg.eigh (reported by the
+    kernel with their bit-equal scatter matrix) are decided here by the
+    reference's own eigh expressions (cueimage.plane_normals), so validity
+    is bit-exact and every normal matches to <= 1e-10.  recheck_capacity
+    sizes the first recheck buffer (it grows to fit; tests shrink it)."""
+    global last_recheck_count
     lib = N.load()
+    cfg = cfg or NormalConfig()
     device = torch.device(device or (depth.device if torch.is_tensor(depth) and depth.is_cuda
                                      else "cuda"))
     squeeze = torch.as_tensor(depth).dim() == 2
@@ -67,12 +82,43 @@ def estimate_normals_device(depth, cam: Intrinsics, cfg: NormalConfig | None = N
     step = _frames_per_batch(lib, cs, n)
     scratch = torch.empty(int(lib.pba_normals_scratch_bytes(cs, min(step, n))) or 8,
                           dtype=torch.uint8, device=device)
+    count = torch.zeros(1, dtype=torch.int32, device=device)
+    cap = recheck_capacity if recheck_capacity is not None else 4096 + (min(step, n) * H * W) // 256
+    last_recheck_count = 0
+    recheck = torch.empty((max(cap, 1), N.NORMALS_RECHECK_DOUBLES), dtype=torch.float64,
+                          device=device)
     for f0 in range(0, n, step):
         k = min(step, n - f0)
-        N.check(lib.pba_estimate_normals(cs, tab.data_ptr(), d[f0].data_ptr(), k, cfg_c,
-                                         out[f0].data_ptr(), scratch.data_ptr(), _stream(device)),
-                "pba_estimate_normals")
+        while True:
+            N.check(lib.pba_estimate_normals(cs, tab.data_ptr(), d[f0].data_ptr(), k, cfg_c,
+                                             out[f0].data_ptr(), scratch.data_ptr(),
+                                             recheck.data_ptr(), cap, count.data_ptr(),
+                                             _stream(device)), "pba_estimate_normals")
+            got = int(count.item())
+            if got <= cap:
+                break
+            cap = got
+            recheck = torch.empty((cap, N.NORMALS_RECHECK_DOUBLES), dtype=torch.float64,
+                                  device=device)
+        if got:
+            _decide_on_host(recheck[:got], out[f0:f0 + k], cfg)
+        last_recheck_count += got
     return out[0] if squeeze else out
+
+
+def _decide_on_host(recheck: torch.Tensor, out: torch.Tensor, cfg: NormalConfig) -> None:
+    """Re-decide the listed pixels with numpy.linalg.eigh (cues.py:239-245)."""
+    rec = recheck.cpu().numpy()
+    idx = rec[:, 0].astype(np.int64)
+    S = np.empty((rec.shape[0], 3, 3))
+    S[:, 0, 0], S[:, 1, 1], S[:, 2, 2] = rec[:, 1], rec[:, 2], rec[:, 3]
+    S[:, 1, 0] = S[:, 0, 1] = rec[:, 4]
+    S[:, 2, 0] = S[:, 0, 2] = rec[:, 5]
+    S[:, 2, 1] = S[:, 1, 2] = rec[:, 6]
+    nrm, ok = plane_normals(S, np.ascontiguousarray(rec[:, 7:10]), cfg.degeneracy_ratio)
+    vals = np.where(ok[:, None], nrm, 0.0)
+    flat = out.view(-1, 3)
+    flat[torch.from_numpy(idx).to(out.device)] = torch.from_numpy(vals).to(out.device)
 
 
 def downscale_cues_device(intensity: torch.Tensor, depth: torch.Tensor, normals: torch.Tensor,
