@@ -13,7 +13,8 @@ from .se3 import (InvalidPerturbationError, PerturbationVector, Pose, boxplus, e
 from .camera import (PINHOLE, SPHERICAL, Intrinsics, SensorExtrinsics, project,
                      projective_jacobian, unproject)
 from .cueimage import (CueImage, CuePyramid, DeviceCueImage, NormalConfig, PyramidConfigError,
-                       build_cue_image, build_pyramid, estimate_normals, footprint_index)
+                       build_cue_image, build_pyramid, estimate_normals, footprint_index,
+                       sample)
 from .pyramid_device import build_pyramids_device, estimate_normals_device
 from .evaluation import (AteReport, DegenerateAlignmentError, NoAssociationError, associate,
                          ate_rmse, evaluate_ate, horn_align)
@@ -27,7 +28,7 @@ from .pairgraph import (COVISIBILITY, ODOMETRY, Edge, FrameNode, GraphConfigErro
                         MatchGraph, build_graph, dump_edges, overlap_ratio)
 from .bundle import (CONSECUTIVE, COUPLED, BAProblem, FusionConfigError, IterationRecord,
                      SolveResult, SolverConfig, UnderConstrainedError, check_connectivity,
-                     solve_fusion, solve_hierarchical, solve_level, total_error)
+                     reproject, solve_fusion, solve_hierarchical, solve_level, total_error)
 
 __version__ = "0.1.0"
 
@@ -45,6 +46,7 @@ __all__ = [
     "NormalConfig", "ODOMETRY", "PINHOLE", "PerturbationVector", "Pose", "PyramidConfigError", "SPHERICAL",
     "SensorExtrinsics", "SolveResult", "SolverConfig", "UnderConstrainedError", "boxplus",
     "build_cue_image", "build_graph", "build_pyramid", "build_pyramids_device", "check_connectivity", "dump_edges", "estimate_normals", "estimate_normals_device", "exp", "footprint_index",
-    "overlap_ratio", "project", "projective_jacobian", "relative", "rotation_angle", "skew",
+    "overlap_ratio", "project", "projective_jacobian", "relative", "reproject", "rotation_angle",
+    "sample", "skew",
     "solve_fusion", "solve_hierarchical", "solve_level", "total_error", "unproject",
 ]

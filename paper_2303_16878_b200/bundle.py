@@ -4,7 +4,7 @@ Same names, arguments, results and errors as the reference solver module
 (pkg/src/photoba/solver.py): `SolverConfig` (:56-91), `BAProblem` (:94-103),
 `IterationRecord` (:106-122), `SolveResult` (:125-140), `solve_level`
 (:555-567), `solve_hierarchical` (:609-616), `solve_fusion` (:619-652),
-`total_error` (:655-670), `check_connectivity` (:463-486) and the
+`total_error` (:655-670), `reproject` (:154-176), `check_connectivity` (:463-486) and the
 `UnderConstrainedError` / `FusionConfigError` exceptions.
 
 The Levenberg-Marquardt control flow of `_solve_level_multi`
@@ -25,6 +25,24 @@ import numpy as np
 from .pairgraph import MatchGraph
 from .camera import SensorExtrinsics
 from .se3 import InvalidPerturbationError, Pose, pose_rows
+
+
+def reproject(uv, depth, x_i: Pose, x_j: Pose, ext: SensorExtrinsics, cam_src, cam_dst):
+    """Source pixels with depth -> destination pixels (the reference's public
+    `reproject`, solver.py:154-176): (uv_dst, p_bar, valid), p_bar being the
+    point in the destination sensor frame and valid the projection test of
+    `project`.  The same chain K1 evaluates per pixel — unproject, into the
+    platform frame of i, into platform j, into sensor j, project — as host
+    numpy for callers outside the solve loop."""
+    from .camera import project, unproject
+
+    p = unproject(cam_src, np.asarray(uv, dtype=float), np.asarray(depth, dtype=float))
+    r_o, t_o = ext.offset.rotation, ext.offset.translation
+    in_i = p @ r_o.T + t_o                                                    # platform i
+    rel = in_i @ x_i.rotation.T + (x_i.translation - x_j.translation)
+    p_bar = (rel @ x_j.rotation - t_o) @ r_o                                  # sensor j
+    uv_dst, valid = project(cam_dst, p_bar)
+    return uv_dst, p_bar, valid
 
 
 class UnderConstrainedError(RuntimeError):

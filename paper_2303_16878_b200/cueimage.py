@@ -256,6 +256,58 @@ def downscale_cues(intensity, depth, normals, depth_ok, normal_ok, s):
     return out_i.reshape(out_h, out_w), out_d.reshape(out_h, out_w), unit.reshape(out_h, out_w, 3)
 
 
+SAMPLE_CHANNELS = ("intensity", "depth", "normals")
+
+
+def _footprint(img, uv: np.ndarray):
+    """Bilinear footprint of continuous pixels (cues.py:397-405): inside iff
+    0 <= x <= W-1 and 0 <= y <= H-1; top-left corner clipped to W-2 / H-2 so
+    the last row / column interpolate with weight 1; outside points read
+    corner (0, 0) with zero weights."""
+    h, w = img.shape
+    x, y = uv[..., 0], uv[..., 1]
+    inside = (x >= 0.0) & (x <= w - 1.0) & (y >= 0.0) & (y <= h - 1.0)
+    cx = np.clip(np.floor(np.where(inside, x, 0.0)).astype(int), 0, w - 2)
+    cy = np.clip(np.floor(np.where(inside, y, 0.0)).astype(int), 0, h - 2)
+    fx = np.where(inside, x - cx, 0.0)
+    fy = np.where(inside, y - cy, 0.0)
+    return inside, cx, cy, fx, fy
+
+
+def _interp(arr: np.ndarray, cx, cy, fx, fy) -> np.ndarray:
+    """(1-fy)((1-fx) a00 + fx a01) + fy((1-fx) a10 + fx a11), broadcast over
+    trailing channel axes (cues.py:385-394, same association)."""
+    a00, a01 = arr[cy, cx], arr[cy, cx + 1]
+    a10, a11 = arr[cy + 1, cx], arr[cy + 1, cx + 1]
+    tail = (1,) * (a00.ndim - np.ndim(fx))
+    fx = np.reshape(fx, np.shape(fx) + tail)
+    fy = np.reshape(fy, np.shape(fy) + tail)
+    return (1.0 - fy) * ((1.0 - fx) * a00 + fx * a01) + fy * ((1.0 - fx) * a10 + fx * a11)
+
+
+def sample(img, uv, channel: str):
+    """Bilinear value and gradient of one cue channel at continuous pixels
+    (the reference's public `sample`, cues.py:412-430): (value, gradient,
+    valid).  The gradient interpolates the precomputed central-difference
+    image; a lookup is valid only when it is inside and all four corners
+    are sampleable for that channel.  A single (2,) pixel returns scalars
+    (a bool validity).  Host numpy, like the reference: this is a per-call
+    utility, not part of the per-iteration path (which samples in K1)."""
+    if channel not in SAMPLE_CHANNELS:
+        raise ValueError(f"unknown channel {channel!r}")
+    pts = np.asarray(uv, dtype=float)
+    one = pts.ndim == 1
+    pts = np.atleast_2d(pts)
+    inside, cx, cy, fx, fy = _footprint(img, pts)
+    ok_map = getattr(img, "sampleable_" + channel)
+    ok = inside & ok_map[cy, cx] & ok_map[cy, cx + 1] & ok_map[cy + 1, cx] & ok_map[cy + 1, cx + 1]
+    val = _interp(getattr(img, channel), cx, cy, fx, fy)
+    grad = _interp(getattr(img, "grad_" + channel), cx, cy, fx, fy)
+    if one:
+        return val[0], grad[0], bool(ok[0])
+    return val, grad, ok
+
+
 @dataclass(frozen=True)
 class NormalConfig:
     """Plane-fit normal estimation parameters (cues.py:26-39): Chebyshev

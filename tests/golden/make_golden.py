@@ -340,18 +340,71 @@ def dataset_case():
     print("dataset", len(d["files"]), "files", (OUT / "dataset.npz").stat().st_size, "bytes")
 
 
+def utility_case():
+    """The reference's public utilities beside the solver: reproject
+    (solver.py:154-176) and sample (cues.py:412-430), on a rendered cue image
+    with holes and random continuous pixels (inside, on the border, outside)."""
+    from photoba.cues import CueImage, sample
+    from photoba.geometry import PerturbationVector, exp
+    from photoba.solver import reproject
+
+    rng = np.random.default_rng(77)
+    d = {}
+    pin = rgbd_cam()
+    sph = lidar_cam(256, 32)
+    for tag, cam in (("pin", pin), ("sph", sph)):
+        d[f"{tag}_cam"] = cam_row(cam)
+        m = 400
+        uv = np.stack([rng.uniform(0, cam.width - 1, m), rng.uniform(0, cam.height - 1, m)], -1)
+        depth = rng.uniform(cam.depth_min, min(cam.depth_max, 8.0), m)
+        xi = exp(PerturbationVector(rng.normal(0, 0.3, 3), rng.normal(0, 0.1, 3)))
+        xj = exp(PerturbationVector(rng.normal(0, 0.3, 3), rng.normal(0, 0.1, 3)))
+        off = exp(PerturbationVector(rng.normal(0, 0.05, 3), rng.normal(0, 0.05, 3)))
+        uv_dst, p_bar, valid = reproject(uv, depth, xi, xj, SensorExtrinsics(off), cam, cam)
+        d[f"{tag}_uv"], d[f"{tag}_depth"] = uv, depth
+        d[f"{tag}_xi"], d[f"{tag}_xj"], d[f"{tag}_off"] = pose_rows([xi]), pose_rows([xj]), pose_rows([off])
+        d[f"{tag}_uv_dst"], d[f"{tag}_p_bar"], d[f"{tag}_valid"] = uv_dst, p_bar, valid
+    # sample: one rendered RGB-D view with estimated normals and punched holes
+    r = render_view(box_room_scene(), pin, Pose(np.eye(3), [-0.4, 0.2, -0.5]))
+    pyr = build_pyramid(r.intensity, r.depth, pin, (1.0,))
+    img0 = pyr.levels[0]
+    depth = img0.depth.copy()
+    depth[rng.random(depth.shape) < 0.03] = 0.0
+    img = CueImage(img0.intensity, depth, img0.normals, pin)
+    d["img_I"], d["img_D"], d["img_N"] = img.intensity, img.depth, img.normals
+    m = 600
+    uv = np.stack([rng.uniform(-2, pin.width + 1, m), rng.uniform(-2, pin.height + 1, m)], -1)
+    uv[:20] = np.floor(uv[:20])                              # exact pixel centres
+    uv[20:30, 0] = pin.width - 1.0                           # right border (wx = 1)
+    uv[30:40, 1] = pin.height - 1.0                          # bottom border
+    d["sample_uv"] = uv
+    for ch in ("intensity", "depth", "normals"):
+        v, g, ok = sample(img, uv, ch)
+        d[f"sample_{ch}_v"], d[f"sample_{ch}_g"], d[f"sample_{ch}_ok"] = v, g, ok
+        v1, g1, ok1 = sample(img, uv[5], ch)                  # single-point form
+        d[f"sample1_{ch}_v"], d[f"sample1_{ch}_g"], d[f"sample1_{ch}_ok"] = v1, g1, ok1
+    np.savez_compressed(OUT / "utility.npz", **d)
+    print("utility", (OUT / "utility.npz").stat().st_size, "bytes")
+
+
 if __name__ == "__main__":
-    pin = Intrinsics(40.0, 40.0, 32.0, 24.0, 64, 48, PINHOLE, 0.1, 50.0)
-    single_sensor_case("pinhole_small", pin, 4, (1.0,), [0.0, 0.0, 0.1], 51, 0.04,
-                       math.radians(1.5))
-    sph = Intrinsics(128 / (2 * math.pi), 24 / (math.pi / 2), 64.0, 12.0, 128, 24, "spherical",
-                     0.2, 80.0)
-    single_sensor_case("spherical_small", sph, 4, (0.5, 1.0), [0.0, 0.0, -0.05], 52, 0.04,
-                       math.radians(1.5))
-    fusion_case()
-    footprint_case()
-    pyramid_case()
-    dataset_case()
-    evaluation_case()
-    behaviour_case()
-    acceptance_case()
+    cases = set(sys.argv[1:])  # empty: regenerate everything
+
+    def want(name):
+        return not cases or name in cases
+
+    if want("pinhole_small"):
+        pin = Intrinsics(40.0, 40.0, 32.0, 24.0, 64, 48, PINHOLE, 0.1, 50.0)
+        single_sensor_case("pinhole_small", pin, 4, (1.0,), [0.0, 0.0, 0.1], 51, 0.04,
+                           math.radians(1.5))
+    if want("spherical_small"):
+        sph = Intrinsics(128 / (2 * math.pi), 24 / (math.pi / 2), 64.0, 12.0, 128, 24,
+                         "spherical", 0.2, 80.0)
+        single_sensor_case("spherical_small", sph, 4, (0.5, 1.0), [0.0, 0.0, -0.05], 52, 0.04,
+                           math.radians(1.5))
+    for name, fn in (("fusion", fusion_case), ("footprint", footprint_case),
+                     ("pyramid", pyramid_case), ("dataset", dataset_case),
+                     ("evaluation", evaluation_case), ("behaviour", behaviour_case),
+                     ("acceptance", acceptance_case), ("utility", utility_case)):
+        if want(name):
+            fn()
