@@ -122,6 +122,8 @@ size_t pba_ray_table_doubles(const pba_camera* cam);
 const char* pba_version(void);
 /* Message of the last failing call on this thread. */
 const char* pba_last_error(void);
+/* 1 in the bounds-checked build (libpba_b200_checked.so, -DPBA_CHECKED), else 0. */
+int32_t pba_build_checked(void);
 /* Number of kernels this library has launched in this process (diagnostics;
  * bench.py reports it per timed step). */
 uint64_t pba_kernel_launches(void);

@@ -19,6 +19,10 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OUT_DIR = PKG / "_lib"
 LIB = OUT_DIR / "libpba_b200.so"
+# bounds-checked variant (-DPBA_CHECKED): device index assertions in place of
+# compute-sanitizer memcheck, which is closed on the GPU pool; PBA_CHECKED=1
+# makes native.load() pick it (tests/test_gpu_checked.py)
+LIB_CHECKED = OUT_DIR / "libpba_b200_checked.so"
 SOURCES = ["capi.cu", "texels.cu", "linearize.cu", "assemble.cu", "solve.cu", "pcg.cu", "update.cu",
            "overlap.cu", "pyramid.cu", "rasters.cu"]
 GENCODE = "-gencode=arch=compute_100a,code=sm_100a"
@@ -31,26 +35,29 @@ def nvcc_path() -> str:
     raise RuntimeError("nvcc not found; the CUDA toolkit is required to build libpba_b200.so")
 
 
-def _stale() -> bool:
-    if not LIB.exists():
+def _stale(lib: Path = LIB) -> bool:
+    if not lib.exists():
         return True
-    mtime = LIB.stat().st_mtime
+    mtime = lib.stat().st_mtime
     deps = [CSRC / s for s in SOURCES] + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "pba.h"]
     return any(p.stat().st_mtime > mtime for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
-        return LIB
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> Path:
+    lib = LIB_CHECKED if checked else LIB
+    if not force and not _stale(lib):
+        return lib
     OUT_DIR.mkdir(exist_ok=True)
     nvcc = nvcc_path()
     objs = []
+    tag = "_checked" if checked else ""
     for src in SOURCES:
-        obj = OUT_DIR / (Path(src).stem + ".o")
+        obj = OUT_DIR / (Path(src).stem + tag + ".o")
         cmd = [
             nvcc, GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
             "-Xptxas", "-v" if verbose else "-O3",
             "-I", str(ROOT / "include"), "-I", str(CSRC),
+            *(["-DPBA_CHECKED"] if checked else []),
             "-c", str(CSRC / src), "-o", str(obj),
         ]
         res = subprocess.run(cmd, capture_output=True, text=True)
@@ -59,16 +66,17 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         if verbose:
             sys.stderr.write(res.stderr)
         objs.append(str(obj))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [nvcc, GENCODE, "-shared", "-o", str(tmp), *objs, "-lcudart"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc link failed:\n{res.stdout}\n{res.stderr}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     for o in objs:
         Path(o).unlink(missing_ok=True)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv,
+                checked="--checked" in sys.argv))

@@ -50,7 +50,7 @@ __global__ void assemble_kernel(const double* __restrict__ rec, int n_free,
         const double* r = rec + (long)(item >> 1) * kRec;
         acc += upper_get(r + ((item & 1) ? PBA_REC_HJJ : PBA_REC_HII), k, l);
       }
-      H[(6L * s + k) * dim + 6L * s + l] = acc;
+      H[PBA_DCHECK_INDEX((6L * s + k) * dim + 6L * s + l, dim * dim)] = acc;
     } else {
       const int k = e - 36;
       for (int it = i0; it < i1; ++it) {
@@ -73,8 +73,8 @@ __global__ void assemble_kernel(const double* __restrict__ rec, int n_free,
     acc += (item & 1) ? hij[6 * l + k] : hij[6 * k + l];
   }
   const long r = off_rc[2 * o], c = off_rc[2 * o + 1];
-  H[(6 * r + k) * dim + 6 * c + l] = acc;
-  H[(6 * c + l) * dim + 6 * r + k] = acc;
+  H[PBA_DCHECK_INDEX((6 * r + k) * dim + 6 * c + l, dim * dim)] = acc;
+  H[PBA_DCHECK_INDEX((6 * c + l) * dim + 6 * r + k, dim * dim)] = acc;
 }
 
 // cost and count summed over pairs: each thread a contiguous edge range in

@@ -28,3 +28,11 @@ extern "C" uint64_t pba_kernel_launches(void) { return pba::g_launches.load(); }
 extern "C" const char* pba_version(void) { return "paper_2303_16878_b200 pba 0.1 (sm_100a)"; }
 
 extern "C" const char* pba_last_error(void) { return pba::g_last_error; }
+
+extern "C" int32_t pba_build_checked(void) {
+#ifdef PBA_CHECKED
+  return 1;
+#else
+  return 0;
+#endif
+}

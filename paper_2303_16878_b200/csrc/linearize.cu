@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
   // two dependent round trips (source texel, destination texels), not four.
   double2 nx0 = make_double2(0.0, 0.0), nx2 = make_double2(0.0, 0.0);
   if (first + (int)threadIdx.x < last) {
-    const double2* t = S.src_tex + gr * stride * sW + gcol * stride;
+    const double2* t = S.src_tex + PBA_DCHECK_INDEX(gr * stride * sW + gcol * stride, S.src_np);
     nx0 = __ldg(t);
     nx2 = __ldg(t + kPairNzM * S.src_np);
   }
@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     ngcol = gcol;
     advance_pixel(ngr, ngcol, gw, kT);
     if (idx + kT < last) {
-      const double2* t = S.src_tex + ngr * stride * sW + ngcol * stride;
+      const double2* t = S.src_tex + PBA_DCHECK_INDEX(ngr * stride * sW + ngcol * stride, S.src_np);
       nx0 = __ldg(t);
       nx2 = __ldg(t + kPairNzM * S.src_np);
     }
@@ -405,6 +405,10 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     // ---- source cue values and unprojection (sensors.py:133-154) ----
     const double d = s_id.y;
     double ps[3];
+#ifdef PBA_CHECKED
+    PBA_DCHECK_INDEX(col, sW);
+    PBA_DCHECK_INDEX(row, sH);
+#endif
     if (src_sph) {
       const double ca = __ldg(S.src_ray + col), sa = __ldg(S.src_ray + sW + col);
       const double ce = __ldg(S.src_ray + 2 * sW + row), se = __ldg(S.src_ray + 2 * sW + sH + row);
@@ -483,8 +487,10 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     y0 = min(max(y0, 0), dH - 2);
     const double wx = u - x0, wy = v - y0;
     // kProbe 1 (diagnostics only): every sample reads the same texel block
-    const int dp = kProbe == 1 ? (dH / 2) * dW + dW / 2 : y0 * dW + x0;
     const int dnp = S.dst_np;
+    // the four corners dp, dp + 1, dp + W, dp + W + 1 lie in the plane
+    const int dp = PBA_DCHECK_INDEX(kProbe == 1 ? (dH / 2) * dW + dW / 2 : y0 * dW + x0,
+                                    dnp - dW - 1);
     const double2* t00 = S.dst_tex + dp;  // pair k of corner (r, c): t00[k * dnp + r * dW + c]
     const double2* t10 = t00 + dW;
     // (I, D) and (nz, mask) of the four corners in one round trip
@@ -529,12 +535,24 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     }
 
     // ---- per-cue Huber (solver.py:317-337) ----
-    const double sI = fabs(e0) * sqw0;  // = sqrt(e0^2 w0) up to one rounding
-    const double sD = fabs(e1) * sqw1;
+    // Fast norms (|e| sqrt(w); t * rsqrt(t)) are within a few ulp of the
+    // reference's sqrt((e*e)*w) / sqrt(((e2 + e3) + e4)); the "small"
+    // decision s <= delta is re-taken with the reference's exact roundings
+    // whenever a fast norm lies within 1e-14 relative of its threshold.
+    double sI = fabs(e0) * sqw0;
+    double sD = fabs(e1) * sqw1;
     const double tN = (e2 * e2 * cfg.omega[2] + e3 * e3 * cfg.omega[3]) + e4 * e4 * cfg.omega[4];
     const double inv_sN = tN > 1e-300 ? rsqrt(tN) : 0.0;
-    const double sN = tN > 1e-300 ? tN * inv_sN : sqrt(tN);
+    double sN = tN > 1e-300 ? tN * inv_sN : sqrt(tN);
     const double dI = cfg.huber_delta[0], dD = cfg.huber_delta[1], dN = cfg.huber_delta[2];
+    if (fabs(sI - dI) <= 1e-14 * dI)
+      sI = __dsqrt_rn(__dmul_rn(__dmul_rn(e0, e0), cfg.omega[0]));
+    if (fabs(sD - dD) <= 1e-14 * dD)
+      sD = __dsqrt_rn(__dmul_rn(__dmul_rn(e1, e1), cfg.omega[1]));
+    if (fabs(sN - dN) <= 1e-14 * dN)
+      sN = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(e2, e2), cfg.omega[2]),
+                                          __dmul_rn(__dmul_rn(e3, e3), cfg.omega[3])),
+                                __dmul_rn(__dmul_rn(e4, e4), cfg.omega[4])));
     const bool smI = sI <= dI, smD = sD <= dD, smN = sN <= dN;
     cost += (smI ? sI * sI : dI * (2.0 * sI - dI)) + (smD ? sD * sD : dD * (2.0 * sD - dD)) +
             (smN ? sN * sN : dN * (2.0 * sN - dN));
@@ -664,7 +682,8 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     for (int w = 0; w < kWarps; ++w) s += red[w][threadIdx.x];
     // slot of this chunk in its pair's range (the launch order of the chunk
     // table is free; the per-pair sums always run in chunk order)
-    const long slot = pair_chunk_offsets[pair] + first / chunk_pixels;
+    const long slot = PBA_DCHECK_INDEX(pair_chunk_offsets[pair] + first / chunk_pixels,
+                                       pair_chunk_offsets[pair + 1]);
     partials[slot * kPart + threadIdx.x] = s;
   }
 }

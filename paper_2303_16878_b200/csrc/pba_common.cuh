@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include "pba.h"
 
@@ -29,6 +30,25 @@ enum TexelPair : int {
   kTexelPairs = 8
 };
 constexpr int kTexelBytes = 16 * kTexelPairs;
+
+// Checked build (-DPBA_CHECKED -> _lib/libpba_b200_checked.so, selected by
+// PBA_CHECKED=1): device-side bounds assertions standing in for
+// compute-sanitizer memcheck, which is closed on this GPU pool.  A failed
+// check prints one "PBA_CHECK" line and clamps the index, so the kernel
+// never touches memory outside the buffer it was checking.
+#ifdef PBA_CHECKED
+__device__ __forceinline__ long long checked_index(long long i, long long n, const char* file,
+                                                   int line) {
+  if (i < 0 || i >= n) {
+    printf("PBA_CHECK %s:%d index %lld outside [0, %lld)\n", file, line, i, n);
+    return i < 0 ? 0 : (n > 0 ? n - 1 : 0);
+  }
+  return i;
+}
+#define PBA_DCHECK_INDEX(idx, n) ::pba::checked_index((long long)(idx), (long long)(n), __FILE__, __LINE__)
+#else
+#define PBA_DCHECK_INDEX(idx, n) (idx)
+#endif
 
 // Thread-local error message for pba_last_error().
 void set_error(const char* fmt, ...);

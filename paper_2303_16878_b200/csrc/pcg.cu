@@ -149,7 +149,7 @@ __device__ __forceinline__ double row_part(const double* __restrict__ H, long di
   const int e1 = row_ptr[br + 1];
 #pragma unroll 2
   for (int e = row_ptr[br] + sp; e < e1; e += kSplit) {
-    const int c = __ldg(cols + e);
+    const int c = PBA_DCHECK_INDEX(__ldg(cols + e), dim / 6);
     const double* hb = h + 6L * c;
     const double* vb = v + 6L * c;
 #pragma unroll

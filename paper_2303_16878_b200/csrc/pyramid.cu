@@ -239,14 +239,15 @@ __global__ void __launch_bounds__(128, 6) normals_kernel(pba_camera cam,
   const double facing = __dadd_rn(__dadd_rn(__dmul_rn(n0, x), __dmul_rn(n1, y)), __dmul_rn(n2, z));
   if (facing > 0.0) n0 = -n0, n1 = -n1, n2 = -n2;
   // Certainty margins against any backward-stable 3x3 eigensolver (LAPACK
-  // dsyevd or this Jacobi; both within ~10 eps ||S||): eigenvalues within
-  // m_l = 1e-12 ||S||, the eigenvector within err_n = 1e-12 ||S|| / gap,
-  // so facing = n . p within m_f = 4 |p| err_n (+ rounding).  Outside the
-  // margins the gates decide identically and the normal agrees to <= 1e-10.
+  // dsyevd or this Jacobi; both within ~10 eps ||S|| = 2.2e-15 ||S||):
+  // eigenvalues within m_l = 2e-14 ||S||, the eigenvector within
+  // err_n = 2e-14 ||S|| / gap (9x those bounds), so facing = n . p within
+  // m_f = 4 |p| err_n (+ rounding).  Outside the margins the gates decide
+  // identically and the normal agrees to <= 1e-10.
   const double snorm = fmax(fabs(la), fabs(lc));
-  const double m_l = 1e-12 * snorm;
+  const double m_l = 2e-14 * snorm;
   const double gap = lb - la;
-  const double err_n = gap > 0.0 ? 1e-12 * snorm / gap + 1e-15 : INFINITY;
+  const double err_n = gap > 0.0 ? 2e-14 * snorm / gap + 1e-15 : INFINITY;
   const double pn = sqrt(x * x + y * y + z * z);
   const double m_f = 4.0 * pn * err_n + 1e-15 * pn;
   const double af = fabs(facing);

@@ -350,12 +350,26 @@ def estimate_normals(depth: np.ndarray, cam: Intrinsics, cfg: NormalConfig | Non
     """
     cfg = cfg or NormalConfig()
     depth = np.asarray(depth, dtype=float)
+    out = np.zeros(depth.shape + (3,))
+    rr, cc, S, p = window_scatter(depth, cam, cfg)
+    if rr.size == 0:
+        return out
+    n, ok = plane_normals(S, p, cfg.degeneracy_ratio)
+    out[rr[ok], cc[ok]] = n[ok]
+    return out
+
+
+def window_scatter(depth: np.ndarray, cam: Intrinsics, cfg: NormalConfig):
+    """Pixels with enough valid window neighbours (rows, cols), their window
+    scatter matrices S (k, 3, 3) and points p (k, 3) — estimate_normals up
+    to the eigen step (cues.py:187-238)."""
+    depth = np.asarray(depth, dtype=float)
     h, w = depth.shape
-    out = np.zeros((h, w, 3))
+    empty = (np.zeros(0, np.int64), np.zeros(0, np.int64), np.zeros((0, 3, 3)), np.zeros((0, 3)))
     with np.errstate(invalid="ignore"):
         valid = np.isfinite(depth) & (depth >= cam.depth_min) & (depth <= cam.depth_max)
     if not valid.any():
-        return out
+        return empty
     pts = np.zeros((h, w, 3))
     rr, cc = np.nonzero(valid)
     pts[rr, cc] = unproject(cam, np.stack([cc.astype(float), rr.astype(float)], axis=-1),
@@ -369,15 +383,13 @@ def estimate_normals(depth: np.ndarray, cam: Intrinsics, cfg: NormalConfig | Non
     use = cnt >= cfg.min_points
     rr, cc, win, cnt = rr[use], cc[use], win[use], cnt[use]
     if rr.size == 0:
-        return out
+        return empty
     mu = win[:, 0:3] / cnt[:, None]
     # scatter[i][j] = S_ij - (count * mu_i) * mu_j, entry by entry (the
     # lower triangle is what the symmetric eigensolver reads)
     S = win[:, (3, 4, 5, 4, 6, 7, 5, 7, 8)].reshape(-1, 3, 3)
     S = S - (cnt[:, None] * mu)[:, :, None] * mu[:, None, :]
-    n, ok = plane_normals(S, pts[rr, cc], cfg.degeneracy_ratio)
-    out[rr[ok], cc[ok]] = n[ok]
-    return out
+    return rr, cc, S, pts[rr, cc]
 
 
 def plane_normals(S: np.ndarray, p: np.ndarray, degeneracy_ratio: float):

@@ -31,6 +31,7 @@ PARTIAL_DOUBLES = 32
 # symbols declared in include/pba.h, in header order
 EXPORTED = (
     "pba_texel_bytes", "pba_ray_table_doubles", "pba_version", "pba_last_error",
+    "pba_build_checked",
     "pba_kernel_launches",
     "pba_build_texels_scratch_bytes", "pba_build_texels", "pba_plan_chunks", "pba_linearize",
     "pba_plan_assembly", "pba_assemble", "pba_sum_totals", "pba_solve_work_bytes",
@@ -83,6 +84,7 @@ _SIGNATURES = {
     "pba_ray_table_doubles": (_sz, [ctypes.POINTER(Camera)]),
     "pba_version": (ctypes.c_char_p, []),
     "pba_last_error": (ctypes.c_char_p, []),
+    "pba_build_checked": (_i32, []),
     "pba_kernel_launches": (ctypes.c_uint64, []),
     "pba_build_texels_scratch_bytes": (_sz, [ctypes.POINTER(Camera)]),
     "pba_build_texels": (ctypes.c_int, [ctypes.POINTER(Camera), _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
@@ -120,8 +122,14 @@ class NativeError(RuntimeError):
     """A CUDA / argument failure reported by libpba_b200."""
 
 
+def _checked() -> bool:
+    import os
+
+    return os.environ.get("PBA_CHECKED") == "1"
+
+
 def library_path() -> Path:
-    return _build.LIB
+    return _build.LIB_CHECKED if _checked() else _build.LIB
 
 
 def load(build_if_missing: bool = True) -> ctypes.CDLL:
@@ -129,11 +137,11 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    path = _build.LIB
+    path = library_path()
     if not path.exists():
         if not build_if_missing:
             raise NativeError(f"{path} is missing; run paper_2303_16878_b200._build.build()")
-        _build.build()
+        _build.build(checked=_checked())
     lib = ctypes.CDLL(str(path))
     for name, (res, args) in _SIGNATURES.items():
         fn = getattr(lib, name)

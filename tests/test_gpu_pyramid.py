@@ -148,10 +148,13 @@ def test_device_normals_on_rgbd_scans_match_host():
 def test_device_normals_knife_edge_inputs_rechecked(seed):
     """Depth images built to sit on the gates: planes with noise at many
     scales (near-degenerate scatter), line-like strips, grazing views and
-    holes.  Pixels the device cannot decide go to the host's eigh; the
-    result has zero validity flips, including with a tiny first recheck
-    buffer (the grow-and-rerun path)."""
+    holes — and, for each image, NormalConfigs whose degeneracy ratio is set
+    to the exact eigenvalue ratio lam1 / lam2 of chosen pixels, so those
+    pixels' planarity test is decided by the last bits of the eigensolver.
+    The device must hand them to the host's eigh: zero validity flips,
+    including with a tiny first recheck buffer (the grow-and-rerun path)."""
     from paper_2303_16878_b200 import pyramid_device as PD
+    from paper_2303_16878_b200.cueimage import NormalConfig, window_scatter
 
     rng = np.random.default_rng(seed)
     H, W = 48, 64
@@ -170,10 +173,22 @@ def test_device_normals_knife_edge_inputs_rechecked(seed):
             d[rng.random((H, W)) < 0.3] = 0.0
         batch.append(d)
     depth = np.stack(batch)
-    dev = P.estimate_normals_device(torch.from_numpy(depth).cuda(), cam,
-                                    recheck_capacity=1).cpu().numpy()
-    _assert_normals_equal_host(depth, cam, dev)
-    assert PD.last_recheck_count > 0  # the host path was exercised
+    _, _, S, _ = window_scatter(depth[0], cam, NormalConfig())
+    lam = np.linalg.eigvalsh(S)
+    ratio = lam[:, 1] / lam[:, 2]
+    picks = rng.choice(np.nonzero((ratio > 1e-6) & (ratio < 0.5))[0], 3, replace=False)
+    rechecked = 0
+    for cfg in [NormalConfig()] + [NormalConfig(degeneracy_ratio=float(ratio[i])) for i in picks]:
+        dev = P.estimate_normals_device(torch.from_numpy(depth).cuda(), cam, cfg,
+                                        recheck_capacity=1).cpu().numpy()
+        for b in range(depth.shape[0]):
+            host = P.estimate_normals(depth[b], cam, cfg)
+            assert np.array_equal(_valid(host), _valid(dev[b]))
+            vh = _valid(host)
+            if vh.any():
+                assert np.abs(host[vh] - dev[b][vh]).max() <= 1e-10
+        rechecked += PD.last_recheck_count
+    assert rechecked > 0  # the host path was exercised
 
 
 @pytest.mark.parametrize("config", ["c4", "c5"])
