@@ -43,22 +43,26 @@ def _stale(lib: Path = LIB) -> bool:
     return any(p.stat().st_mtime > mtime for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False, checked: bool = False) -> Path:
-    lib = LIB_CHECKED if checked else LIB
+def build(force: bool = False, verbose: bool = False, checked: bool = False,
+          out: Path | None = None, csrc: Path | None = None) -> Path:
+    """Compile csrc/*.cu into the library (`out`/`csrc` redirect an A/B
+    build of another source tree, e.g. tools/ab_build.sh)."""
+    lib = Path(out) if out else (LIB_CHECKED if checked else LIB)
+    src_dir = Path(csrc) if csrc else CSRC
     if not force and not _stale(lib):
         return lib
-    OUT_DIR.mkdir(exist_ok=True)
+    lib.parent.mkdir(parents=True, exist_ok=True)
     nvcc = nvcc_path()
     objs = []
     tag = "_checked" if checked else ""
     for src in SOURCES:
-        obj = OUT_DIR / (Path(src).stem + tag + ".o")
+        obj = lib.parent / (Path(src).stem + tag + ".o")
         cmd = [
             nvcc, GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
             "-Xptxas", "-v" if verbose else "-O3",
-            "-I", str(ROOT / "include"), "-I", str(CSRC),
+            "-I", str(ROOT / "include"), "-I", str(src_dir),
             *(["-DPBA_CHECKED"] if checked else []),
-            "-c", str(CSRC / src), "-o", str(obj),
+            "-c", str(src_dir / src), "-o", str(obj),
         ]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:

@@ -157,7 +157,88 @@ struct PairSetup {
   pba_camera src_cam, dst_cam;
   int grid_w, n_px, stride;
   int src_np, dst_np;  // pixels per texel plane
+  pba_config cfg;      // the launch's config (read through SV in the loop)
+  double sqw0, sqw1;   // sqrt(omega_I), sqrt(omega_D)
+  // kLean: the three 3x3 maps as 16-byte-aligned rows of four, read as two
+  // 16-byte shared loads per row: [R_o | t_o], [M_i | cpb], [rot_n | 0]
+  alignas(16) double RoT[12];
+  alignas(16) double MiC[12];
+  alignas(16) double Rn[12];
+  // kLean: scalars the pixel loop reads together, paired for 16-byte loads
+  alignas(16) double fx_cx[2], fy_cy[2], fx_fy[2], range[2], wh[2];
+  alignas(16) double sqw0_dI[2], sqw1_dD[2], om01[2], om23[2], om4_dN[2];
+  alignas(8) int dwh[2], np_sd[2];
 };
+
+// Loop reads of the CTA's pair setup.  kLean: every use is a volatile
+// shared-memory load, so the compiler cannot keep the ~30 loop-invariant
+// setup values (cameras, config, pointers) in registers across the pixel
+// loop; the LDS latency is short and the registers go to occupancy.
+template <bool kLean>
+struct SetupRead {
+  template <typename T>
+  __device__ __forceinline__ static T get(const T& x) { return x; }
+};
+template <>
+struct SetupRead<true> {
+  __device__ __forceinline__ static double get(const double& x) {
+    double v;
+    asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(v) : "r"((unsigned)__cvta_generic_to_shared(&x)));
+    return v;
+  }
+  __device__ __forceinline__ static int get(const int& x) {
+    int v;
+    asm volatile("ld.volatile.shared.s32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(&x)));
+    return v;
+  }
+  template <typename T>
+  __device__ __forceinline__ static T* get(T* const& x) {
+    unsigned long long v;
+    asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(v) : "r"((unsigned)__cvta_generic_to_shared(&x)));
+    return reinterpret_cast<T*>(v);
+  }
+};
+#define SV(x) (SetupRead<kLean>::get(x))
+
+// A 16-byte-aligned double pair / 8-byte-aligned int pair of the setup as one
+// volatile shared load (kLean).
+__device__ __forceinline__ double2 setup_pair(const double* p) {
+  double2 v;
+  asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];"
+               : "=d"(v.x), "=d"(v.y) : "r"((unsigned)__cvta_generic_to_shared(p)));
+  return v;
+}
+template <bool kLean>
+__device__ __forceinline__ double2 pair_rd(const double* p) {
+  if constexpr (kLean) return setup_pair(p);
+  return make_double2(p[0], p[1]);
+}
+__device__ __forceinline__ int2 setup_pair(const int* p);
+template <bool kLean>
+__device__ __forceinline__ int2 pair_rd(const int* p) {
+  if constexpr (kLean) return setup_pair(p);
+  return make_int2(p[0], p[1]);
+}
+#define SP(f) (pair_rd<kLean>(S.f))
+__device__ __forceinline__ int2 setup_pair(const int* p) {
+  int2 v;
+  asm volatile("ld.volatile.shared.v2.s32 {%0, %1}, [%2];"
+               : "=r"(v.x), "=r"(v.y) : "r"((unsigned)__cvta_generic_to_shared(p)));
+  return v;
+}
+
+struct Row4 {
+  double2 a, b;  // (r0, r1), (r2, extra)
+};
+// One 4-double row of the setup (16-byte aligned) as two volatile 16-byte
+// shared loads.
+__device__ __forceinline__ Row4 setup_row(const double* p) {
+  Row4 r;
+  const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+  asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r.a.x), "=d"(r.a.y) : "r"(a));
+  asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r.b.x), "=d"(r.b.y) : "r"(a + 16));
+  return r;
+}
 
 __device__ __forceinline__ void matmul3(const double* A, const double* B, double* C) {
 #pragma unroll
@@ -200,6 +281,16 @@ __device__ void build_setup(PairSetup& S, const pba_frame* frames, const pba_pai
   }
   for (int k = 0; k < 3; ++k)
     S.cpb[k] = S.Ro[k] * tmp[0] + S.Ro[3 + k] * tmp[1] + S.Ro[6 + k] * tmp[2];
+  for (int k = 0; k < 3; ++k) {
+    for (int c = 0; c < 3; ++c) {
+      S.RoT[4 * k + c] = S.Ro[3 * k + c];
+      S.MiC[4 * k + c] = S.Mi[3 * k + c];
+      S.Rn[4 * k + c] = S.rotn[3 * k + c];
+    }
+    S.RoT[4 * k + 3] = S.to[k];
+    S.MiC[4 * k + 3] = S.cpb[k];
+    S.Rn[4 * k + 3] = 0.0;
+  }
   S.occ_tol = P.occ_tol;
   const pba_frame& fs = frames[P.src];
   const pba_frame& fd = frames[P.dst];
@@ -263,6 +354,14 @@ __device__ __forceinline__ uint32_t mask_word(const double2& v) {
 
 __device__ __forceinline__ int upper_idx(int k, int l) { return k * 6 - (k * (k - 1)) / 2 + (l - k); }
 
+// A 16-byte read-only load kept in program order with the other volatile
+// asm (kLean's channel-by-channel gradient gathers).
+__device__ __forceinline__ double2 ldg2_ordered(const double2* p) {
+  double2 v;
+  asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+
 // Bilinear interpolation of a (d/dcol, d/drow) gradient pair with corner weights.
 __device__ __forceinline__ double2 bil4(double2 g00, double2 g01, double2 g10, double2 g11,
                                         double w00, double w01, double w10, double w11) {
@@ -323,7 +422,7 @@ __device__ unsigned long long g_sect_count[8];
 // kProbe (diagnostics only, K1 ablations): 0 normal; 1 every
 // sample reads one fixed destination texel; 10 no gradient gathers; 11 a
 // 7-sum stand-in for the 27-sum accumulation.
-template <bool kJac, int kT, int kMinBlocks, int kProbe = 0>
+template <bool kJac, int kT, int kMinBlocks, int kProbe = 0, bool kLean = false>
 __global__ void __launch_bounds__(kT, kMinBlocks)
     linearize_kernel(const pba_frame* __restrict__ frames, const pba_pair* __restrict__ pairs,
                      const int32_t* __restrict__ chunk_table,
@@ -337,7 +436,24 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
   const long chunk = blockIdx.x;
   const int pair = chunk_table[2 * chunk];
   const int first = chunk_table[2 * chunk + 1];
-  if (threadIdx.x == 0) build_setup(S, frames, pairs[pair], poses, exts, cfg.pixel_stride);
+  if (threadIdx.x == 0) {
+    build_setup(S, frames, pairs[pair], poses, exts, cfg.pixel_stride);
+    S.cfg = cfg;
+    S.sqw0 = sqrt(cfg.omega[0]);
+    S.sqw1 = sqrt(cfg.omega[1]);
+    const pba_camera& dc = S.dst_cam;
+    S.fx_cx[0] = dc.fx, S.fx_cx[1] = dc.cx, S.fy_cy[0] = dc.fy, S.fy_cy[1] = dc.cy;
+    S.fx_fy[0] = dc.fx, S.fx_fy[1] = dc.fy;
+    S.range[0] = dc.depth_min, S.range[1] = dc.depth_max;
+    S.wh[0] = (double)dc.width, S.wh[1] = (double)dc.height;
+    S.sqw0_dI[0] = S.sqw0, S.sqw0_dI[1] = cfg.huber_delta[0];
+    S.sqw1_dD[0] = S.sqw1, S.sqw1_dD[1] = cfg.huber_delta[1];
+    S.om01[0] = cfg.omega[0], S.om01[1] = cfg.omega[1];
+    S.om23[0] = cfg.omega[2], S.om23[1] = cfg.omega[3];
+    S.om4_dN[0] = cfg.omega[4], S.om4_dN[1] = cfg.huber_delta[2];
+    S.dwh[0] = dc.width, S.dwh[1] = dc.height;
+    S.np_sd[0] = S.src_np, S.np_sd[1] = S.dst_np;
+  }
   __syncthreads();
 
   double Q[kQ];
@@ -385,19 +501,30 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
   }
   for (int idx = first + (int)threadIdx.x; idx < last; idx += kT, gr = ngr, gcol = ngcol) {
     PBA_SECT(7)  // tail of the previous iteration (rejected pixels: their last section)
-    const int row = gr * stride;
-    const int col = gcol * stride;
-    const int sp = row * sW + col;
+    const int row = gr * SV(S.stride);
+    const int col = gcol * SV(S.stride);
+    const int sp = row * SV(S.src_cam.width) + col;
+    // kLean: the source texel is loaded when its pixel starts (no prefetch:
+    // the registers go to forming the projective Jacobian while the first
+    // destination gather is in flight, kEarlyMP)
+    constexpr bool kNoPrefetch = kLean;
+    constexpr bool kEarlyMP = kLean;
+    if constexpr (kNoPrefetch) {
+      const double2* t = SV(S.src_tex) + sp;
+      nx0 = __ldg(t);
+      nx2 = __ldg(t + kPairNzM * SV(S.src_np));
+    }
     const double2 s_id = nx0;  // I, D
     const uint32_t sm = mask_word(nx2);
     const double mask_src_nz = nx2.x;
+
     ngr = gr;
     ngcol = gcol;
-    advance_pixel(ngr, ngcol, gw, kT);
-    if (idx + kT < last) {
-      const double2* t = S.src_tex + PBA_DCHECK_INDEX(ngr * stride * sW + ngcol * stride, S.src_np);
+    advance_pixel(ngr, ngcol, SV(S.grid_w), kT);
+    if (!kNoPrefetch && idx + kT < last) {
+      const double2* t = SV(S.src_tex) + PBA_DCHECK_INDEX(ngr * SV(S.stride) * SV(S.src_cam.width) + ngcol * SV(S.stride), SV(S.src_np));
       nx0 = __ldg(t);
-      nx2 = __ldg(t + kPairNzM * S.src_np);
+      nx2 = __ldg(t + kPairNzM * SV(S.src_np));
     }
     if (!(sm & PBA_MASK_DEPTH_VALID)) continue;  // PairContext.build: usable = depth_valid
     PBA_SECT(0)  // source texel + next-texel prefetch
@@ -406,36 +533,47 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     const double d = s_id.y;
     double ps[3];
 #ifdef PBA_CHECKED
-    PBA_DCHECK_INDEX(col, sW);
-    PBA_DCHECK_INDEX(row, sH);
+    PBA_DCHECK_INDEX(col, SV(S.src_cam.width));
+    PBA_DCHECK_INDEX(row, SV(S.src_cam.height));
 #endif
-    if (src_sph) {
-      const double ca = __ldg(S.src_ray + col), sa = __ldg(S.src_ray + sW + col);
-      const double ce = __ldg(S.src_ray + 2 * sW + row), se = __ldg(S.src_ray + 2 * sW + sH + row);
+    if ((SV(S.src_cam.model) == PBA_SPHERICAL)) {
+      const double ca = __ldg(SV(S.src_ray) + col), sa = __ldg(SV(S.src_ray) + SV(S.src_cam.width) + col);
+      const double ce = __ldg(SV(S.src_ray) + 2 * SV(S.src_cam.width) + row), se = __ldg(SV(S.src_ray) + 2 * SV(S.src_cam.width) + SV(S.src_cam.height) + row);
       ps[0] = (ce * ca) * d;
       ps[1] = (ce * sa) * d;
       ps[2] = se * d;
     } else {
-      ps[0] = __ldg(S.src_ray + col) * d;
-      ps[1] = __ldg(S.src_ray + 2 * sW + row) * d;
+      ps[0] = __ldg(SV(S.src_ray) + col) * d;
+      ps[1] = __ldg(SV(S.src_ray) + 2 * SV(S.src_cam.width) + row) * d;
       ps[2] = d;
     }
     // p_u = R_o p + t_o (solver.py:215)
     double pu[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k)
-      pu[k] = S.Ro[3 * k + 0] * ps[0] + S.Ro[3 * k + 1] * ps[1] + S.Ro[3 * k + 2] * ps[2] + S.to[k];
+      if constexpr (kLean) {
+        const Row4 r = setup_row(&S.RoT[4 * k]);
+        pu[k] = r.a.x * ps[0] + r.a.y * ps[1] + r.b.x * ps[2] + r.b.y;
+      } else {
+        pu[k] = S.Ro[3 * k + 0] * ps[0] + S.Ro[3 * k + 1] * ps[1] + S.Ro[3 * k + 2] * ps[2] + S.to[k];
+      }
     // p_bar = R_o^T (R_j^T (R_i p_u + t_i - t_j) - t_o) = M_i p_u + cpb  (solver.py:235-236)
     double pb[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k)
-      pb[k] = S.Mi[3 * k + 0] * pu[0] + S.Mi[3 * k + 1] * pu[1] + S.Mi[3 * k + 2] * pu[2] + S.cpb[k];
+      if constexpr (kLean) {
+        const Row4 r = setup_row(&S.MiC[4 * k]);
+        pb[k] = r.a.x * pu[0] + r.a.y * pu[1] + r.b.x * pu[2] + r.b.y;
+      } else {
+        pb[k] = S.Mi[3 * k + 0] * pu[0] + S.Mi[3 * k + 1] * pu[1] + S.Mi[3 * k + 2] * pu[2] + S.cpb[k];
+      }
 
     // ---- project into the destination (sensors.py:95-130) ----
     // Two independent rsqrt give rho = hypot(x, y), the range and every
     // reciprocal needed below (inv = 1/rho, 1/range; pinhole: 1/z).
     double u, v, dist, rho = 0.0, inv_rho = 0.0, inv_dist;
-    if (dst_sph) {
+    const bool dsph = SV(S.dst_cam.model) == PBA_SPHERICAL;
+    if (dsph) {
       // The reference's roundings are reproduced where they decide validity:
       // range = sqrt((x^2 + y^2) + z^2) with separately rounded terms
       // (np.linalg.norm), hypot(x, y) correctly rounded (np.hypot), and
@@ -445,7 +583,10 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
       const double rr = __dadd_rn(xx, yy);
       const double r2 = __dadd_rn(rr, __dmul_rn(pb[2], pb[2]));
       dist = __dsqrt_rn(r2);
-      if (!(dist >= S.dst_cam.depth_min && dist <= S.dst_cam.depth_max)) continue;
+      {
+        const double2 rg = SP(range);
+        if (!(dist >= rg.x && dist <= rg.y)) continue;
+      }
       inv_dist = rsqrt(r2);
       double az;
       if (rr > 1e-60) {
@@ -464,49 +605,89 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
         az = atan2(pb[1], pb[0]);
       }
       const double el = atan2_tab_r(pb[2], rho, inv_dist);
-      u = py_mod(__dadd_rn(__dmul_rn(S.dst_cam.fx, az), S.dst_cam.cx), dWd);
-      v = __dadd_rn(__dmul_rn(S.dst_cam.fy, el), S.dst_cam.cy);
+      const double2 fc = SP(fx_cx), fyc = SP(fy_cy);
+      u = py_mod(__dadd_rn(__dmul_rn(fc.x, az), fc.y), SP(wh).x);
+      v = __dadd_rn(__dmul_rn(fyc.x, el), fyc.y);
     } else {
       if (!(pb[2] > 0.0)) continue;
       // u, v with true IEEE division and separate roundings, exactly as the
       // reference (sensors.py:114-115): self-projections land on integer
       // pixels where a last-bit difference would move floor() and flip validity.
-      u = __dadd_rn(__ddiv_rn(__dmul_rn(S.dst_cam.fx, pb[0]), pb[2]), S.dst_cam.cx);
-      v = __dadd_rn(__ddiv_rn(__dmul_rn(S.dst_cam.fy, pb[1]), pb[2]), S.dst_cam.cy);
+      const double2 fc = SP(fx_cx), fyc = SP(fy_cy);
+      u = __dadd_rn(__ddiv_rn(__dmul_rn(fc.x, pb[0]), pb[2]), fc.y);
+      v = __dadd_rn(__ddiv_rn(__dmul_rn(fyc.x, pb[1]), pb[2]), fyc.y);
       inv_dist = __drcp_rn(pb[2]);  // Jacobian only
       dist = pb[2];
     }
-    if (!(dist >= S.dst_cam.depth_min && dist <= S.dst_cam.depth_max)) continue;
-    if (!(u >= 0.0 && u < dWd && v >= 0.0 && v < dHd)) continue;
+    {
+      const double2 rg = SP(range);
+      if (!(dist >= rg.x && dist <= rg.y)) continue;
+    }
+    const double2 whd = SP(wh);
+    if (!(u >= 0.0 && u < whd.x && v >= 0.0 && v < whd.y)) continue;
 
     PBA_SECT(1)  // unprojection + warp + projection
     // ---- bilinear footprint and validity (cues.py:397-409, 451-456) ----
-    if (!(u <= dWd - 1.0 && v <= dHd - 1.0)) continue;  // inside (u, v >= 0 already)
+    if (!(u <= whd.x - 1.0 && v <= whd.y - 1.0)) continue;  // inside (u, v >= 0 already)
+    const int2 dwh = SP(dwh);
     int x0 = (int)floor(u), y0 = (int)floor(v);
-    x0 = min(max(x0, 0), dW - 2);
-    y0 = min(max(y0, 0), dH - 2);
+    x0 = min(max(x0, 0), dwh.x - 2);
+    y0 = min(max(y0, 0), dwh.y - 2);
     const double wx = u - x0, wy = v - y0;
     // kProbe 1 (diagnostics only): every sample reads the same texel block
-    const int dnp = S.dst_np;
+    const int dnp = SV(S.dst_np);
     // the four corners dp, dp + 1, dp + W, dp + W + 1 lie in the plane
-    const int dp = PBA_DCHECK_INDEX(kProbe == 1 ? (dH / 2) * dW + dW / 2 : y0 * dW + x0,
-                                    dnp - dW - 1);
-    const double2* t00 = S.dst_tex + dp;  // pair k of corner (r, c): t00[k * dnp + r * dW + c]
-    const double2* t10 = t00 + dW;
+    const int dp = PBA_DCHECK_INDEX(kProbe == 1 ? (dwh.y / 2) * dwh.x + dwh.x / 2 : y0 * dwh.x + x0,
+                                    dnp - dwh.x - 1);
+    const double2* t00 = SV(S.dst_tex) + dp;  // pair k of corner (r, c): t00[k * dnp + r * W + c]
+    const double2* t10 = t00 + dwh.x;
     // (I, D) and (nz, mask) of the four corners in one round trip
     const double2 a00 = __ldg(t00), a01 = __ldg(t00 + 1), a10 = __ldg(t10), a11 = __ldg(t10 + 1);
     const double2 m00 = __ldg(t00 + kPairNzM * dnp), m01 = __ldg(t00 + kPairNzM * dnp + 1);
     const double2 m10 = __ldg(t10 + kPairNzM * dnp), m11 = __ldg(t10 + kPairNzM * dnp + 1);
+    double MP0[3], MP1[3], ud[3];
+    double rho2 = 0.0;
+    if constexpr (kEarlyMP && kJac) {
+      if (dsph) rho2 = pb[0] * pb[0] + pb[1] * pb[1];
+      // ---- projective Jacobian folded with M_i (sensors.py:157-188) ----
+      // (kEarlyMP: formed while the corner loads are in flight)
+      // MP0 = M_i^T P[0,:], MP1 = M_i^T P[1,:], ud = M_i^T (depth-cue direction)
+      const Row4 q0 = setup_row(&S.MiC[0]), q1 = setup_row(&S.MiC[4]), q2 = setup_row(&S.MiC[8]);
+      const double Mr[9] = {q0.a.x, q0.a.y, q0.b.x, q1.a.x, q1.a.y, q1.b.x, q2.a.x, q2.a.y, q2.b.x};
+      const double2 ff = SP(fx_fy);
+      if (dsph) {
+        const double iz = inv_dist;  // 1/|p_bar| = 1/zeta
+        const double f0 = ff.x * (inv_rho * inv_rho);         // fx / rho^2
+        const double f1 = ff.y * (inv_rho * (iz * iz));       // fy / (rho r^2)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const double m0 = Mr[k], m1 = Mr[3 + k], m2 = Mr[6 + k];
+          MP0[k] = f0 * (pb[0] * m1 - pb[1] * m0);
+          MP1[k] = f1 * (rho2 * m2 - pb[2] * (pb[0] * m0 + pb[1] * m1));
+          ud[k] = iz * (pb[0] * m0 + pb[1] * m1 + pb[2] * m2);
+        }
+      } else {
+        const double iz = inv_dist;  // 1/z
+        const double f0 = ff.x * iz, f1 = ff.y * iz;
+        const double xz = pb[0] * iz, yz = pb[1] * iz;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const double m2 = Mr[6 + k];
+          MP0[k] = f0 * (Mr[k] - xz * m2);
+          MP1[k] = f1 * (Mr[3 + k] - yz * m2);
+          ud[k] = m2;
+        }
+      }
+    }
     const uint32_t mk = mask_word(m00) & mask_word(m01) & mask_word(m10) & mask_word(m11);
     if (!(mk & PBA_MASK_SAMP_CORE)) continue;  // core_ok
     const double Dd = bil(a00.y, a01.y, a10.y, a11.y, wx, wy);
     // zeta_d: range for spherical, z for pinhole (solver.py:240)
-    const double zeta = dst_sph ? dist : pb[2];
+    const double zeta = dsph ? dist : pb[2];
     const double e1 = zeta - Dd;
-    if (e1 > S.occ_tol) continue;  // occluded (solver.py:254-258)
-    double rho2 = 0.0;
-    if (kJac && dst_sph) {
-      rho2 = pb[0] * pb[0] + pb[1] * pb[1];
+    if (e1 > SV(S.occ_tol)) continue;  // occluded (solver.py:254-258)
+    if (kJac && dsph) {
+      if (!kEarlyMP) rho2 = pb[0] * pb[0] + pb[1] * pb[1];
       if (!(rho2 > 0.0)) continue;  // ok_jac (sensors.py:173-175; solver.py:262-263)
     }
     const double e0 = s_id.x - bil(a00.x, a01.x, a10.x, a11.x, wx, wy);
@@ -516,21 +697,34 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     double e2 = 0.0, e3 = 0.0, e4 = 0.0;
     double no[3] = {0.0, 0.0, 0.0};  // R_o n_src
     if (normal_on) {
-      const double2 s_n01 = __ldg(S.src_tex + kPairNxy * S.src_np + sp);  // source nx, ny
+      const double2 s_n01 = __ldg(SV(S.src_tex) + kPairNxy * SV(S.src_np) + sp);  // source nx, ny
       const double ns2 = mask_src_nz;
       const double2 b00 = __ldg(t00 + kPairNxy * dnp), b01 = __ldg(t00 + kPairNxy * dnp + 1);
       const double2 b10 = __ldg(t10 + kPairNxy * dnp), b11 = __ldg(t10 + kPairNxy * dnp + 1);
       // rot_n n_src (solver.py:241-248)
-      const double m0 = s_n01.x * S.rotn[0] + s_n01.y * S.rotn[1] + ns2 * S.rotn[2];
-      const double m1 = s_n01.x * S.rotn[3] + s_n01.y * S.rotn[4] + ns2 * S.rotn[5];
-      const double m2 = s_n01.x * S.rotn[6] + s_n01.y * S.rotn[7] + ns2 * S.rotn[8];
+      double m0, m1, m2;
+      if constexpr (kLean) {
+        const Row4 r0 = setup_row(&S.Rn[0]), r1 = setup_row(&S.Rn[4]), r2 = setup_row(&S.Rn[8]);
+        m0 = s_n01.x * r0.a.x + s_n01.y * r0.a.y + ns2 * r0.b.x;
+        m1 = s_n01.x * r1.a.x + s_n01.y * r1.a.y + ns2 * r1.b.x;
+        m2 = s_n01.x * r2.a.x + s_n01.y * r2.a.y + ns2 * r2.b.x;
+      } else {
+        m0 = s_n01.x * S.rotn[0] + s_n01.y * S.rotn[1] + ns2 * S.rotn[2];
+        m1 = s_n01.x * S.rotn[3] + s_n01.y * S.rotn[4] + ns2 * S.rotn[5];
+        m2 = s_n01.x * S.rotn[6] + s_n01.y * S.rotn[7] + ns2 * S.rotn[8];
+      }
       e2 = m0 - bil(b00.x, b01.x, b10.x, b11.x, wx, wy);
       e3 = m1 - bil(b00.y, b01.y, b10.y, b11.y, wx, wy);
       e4 = m2 - bil(m00.x, m01.x, m10.x, m11.x, wx, wy);
       if (kJac) {
 #pragma unroll
         for (int k = 0; k < 3; ++k)
-          no[k] = S.Ro[3 * k + 0] * s_n01.x + S.Ro[3 * k + 1] * s_n01.y + S.Ro[3 * k + 2] * ns2;
+          if constexpr (kLean) {
+            const Row4 r = setup_row(&S.RoT[4 * k]);
+            no[k] = r.a.x * s_n01.x + r.a.y * s_n01.y + r.b.x * ns2;
+          } else {
+            no[k] = S.Ro[3 * k + 0] * s_n01.x + S.Ro[3 * k + 1] * s_n01.y + S.Ro[3 * k + 2] * ns2;
+          }
       }
     }
 
@@ -539,20 +733,21 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     // reference's sqrt((e*e)*w) / sqrt(((e2 + e3) + e4)); the "small"
     // decision s <= delta is re-taken with the reference's exact roundings
     // whenever a fast norm lies within 1e-14 relative of its threshold.
-    double sI = fabs(e0) * sqw0;
-    double sD = fabs(e1) * sqw1;
-    const double tN = (e2 * e2 * cfg.omega[2] + e3 * e3 * cfg.omega[3]) + e4 * e4 * cfg.omega[4];
+    const double2 hI = SP(sqw0_dI), hD = SP(sqw1_dD), o23 = SP(om23), o4 = SP(om4_dN);
+    double sI = fabs(e0) * hI.x;
+    double sD = fabs(e1) * hD.x;
+    const double tN = (e2 * e2 * o23.x + e3 * e3 * o23.y) + e4 * e4 * o4.x;
     const double inv_sN = tN > 1e-300 ? rsqrt(tN) : 0.0;
     double sN = tN > 1e-300 ? tN * inv_sN : sqrt(tN);
-    const double dI = cfg.huber_delta[0], dD = cfg.huber_delta[1], dN = cfg.huber_delta[2];
+    const double dI = hI.y, dD = hD.y, dN = o4.y;
     if (fabs(sI - dI) <= 1e-14 * dI)
-      sI = __dsqrt_rn(__dmul_rn(__dmul_rn(e0, e0), cfg.omega[0]));
+      sI = __dsqrt_rn(__dmul_rn(__dmul_rn(e0, e0), SV(S.cfg.omega[0])));
     if (fabs(sD - dD) <= 1e-14 * dD)
-      sD = __dsqrt_rn(__dmul_rn(__dmul_rn(e1, e1), cfg.omega[1]));
+      sD = __dsqrt_rn(__dmul_rn(__dmul_rn(e1, e1), SV(S.cfg.omega[1])));
     if (fabs(sN - dN) <= 1e-14 * dN)
-      sN = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(e2, e2), cfg.omega[2]),
-                                          __dmul_rn(__dmul_rn(e3, e3), cfg.omega[3])),
-                                __dmul_rn(__dmul_rn(e4, e4), cfg.omega[4])));
+      sN = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(e2, e2), o23.x),
+                                          __dmul_rn(__dmul_rn(e3, e3), o23.y)),
+                                __dmul_rn(__dmul_rn(e4, e4), o4.x)));
     const bool smI = sI <= dI, smD = sD <= dD, smN = sN <= dN;
     cost += (smI ? sI * sI : dI * (2.0 * sI - dI)) + (smD ? sD * sD : dD * (2.0 * sD - dD)) +
             (smN ? sN * sN : dN * (2.0 * sN - dN));
@@ -562,32 +757,34 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
 
     // ---- projective Jacobian folded with M_i (sensors.py:157-188) ----
     // MP0 = M_i^T P[0,:], MP1 = M_i^T P[1,:], ud = M_i^T (depth-cue direction)
-    double MP0[3], MP1[3], ud[3];
-    if (dst_sph) {
+    if constexpr (!kEarlyMP) {
+    if (dsph) {
       const double iz = inv_dist;  // 1/|p_bar| = 1/zeta
-      const double f0 = S.dst_cam.fx * (inv_rho * inv_rho);         // fx / rho^2
-      const double f1 = S.dst_cam.fy * (inv_rho * (iz * iz));       // fy / (rho r^2)
+      const double f0 = SV(S.dst_cam.fx) * (inv_rho * inv_rho);         // fx / rho^2
+      const double f1 = SV(S.dst_cam.fy) * (inv_rho * (iz * iz));       // fy / (rho r^2)
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        const double m0 = S.Mi[k], m1 = S.Mi[3 + k], m2 = S.Mi[6 + k];
+        const double m0 = SV(S.Mi[k]), m1 = SV(S.Mi[3 + k]), m2 = SV(S.Mi[6 + k]);
         MP0[k] = f0 * (pb[0] * m1 - pb[1] * m0);
         MP1[k] = f1 * (rho2 * m2 - pb[2] * (pb[0] * m0 + pb[1] * m1));
         ud[k] = iz * (pb[0] * m0 + pb[1] * m1 + pb[2] * m2);
       }
     } else {
       const double iz = inv_dist;  // 1/z
-      const double f0 = S.dst_cam.fx * iz, f1 = S.dst_cam.fy * iz;
+      const double f0 = SV(S.dst_cam.fx) * iz, f1 = SV(S.dst_cam.fy) * iz;
       const double xz = pb[0] * iz, yz = pb[1] * iz;
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        const double m2 = S.Mi[6 + k];
-        MP0[k] = f0 * (S.Mi[k] - xz * m2);
-        MP1[k] = f1 * (S.Mi[3 + k] - yz * m2);
+        const double m2 = SV(S.Mi[6 + k]);
+        MP0[k] = f0 * (SV(S.Mi[k]) - xz * m2);
+        MP1[k] = f1 * (SV(S.Mi[3 + k]) - yz * m2);
         ud[k] = m2;
       }
     }
-    const double wI = smI ? cfg.omega[0] : cfg.omega[0] * (dI * __drcp_rn(sI));
-    const double wD = smD ? cfg.omega[1] : cfg.omega[1] * (dD * __drcp_rn(sD));
+    }
+    const double2 o01 = SP(om01);
+    const double wI = smI ? o01.x : o01.x * (dI * __drcp_rn(sI));
+    const double wD = smD ? o01.y : o01.y * (dD * __drcp_rn(sD));
     const double wN = smN ? 1.0 : dN * inv_sN;
     // Gradients of the four corners, fetched in two batches (the lines are in
     // L1 after the value loads) and interpolated with the corner weights;
@@ -596,47 +793,83 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     const double w10 = (1.0 - wx) * wy, w11 = wx * wy;
     const double2* g00p = t00 + kPairGI * dnp;  // gradient pair k at g..p + k * dnp
     const double2* g01p = g00p + 1;
-    const double2* g10p = g00p + dW;
+    const double2* g10p = g00p + dwh.x;
     const double2* g11p = g10p + 1;
-    double2 gI, gD;
-    if (kProbe == 10) {  // ablation (diagnostics only): no gradient loads
-      gI = make_double2(a00.x * w00, a01.x * w01);
-      gD = make_double2(a10.y * w10, a11.y * w11);
-    } else {
-      const double2 i00 = __ldg(g00p), i01 = __ldg(g01p), i10 = __ldg(g10p), i11 = __ldg(g11p);
-      const double2 d00 = __ldg(g00p + dnp), d01 = __ldg(g01p + dnp), d10 = __ldg(g10p + dnp),
-                    d11 = __ldg(g11p + dnp);
-      gI = bil4(i00, i01, i10, i11, w00, w01, w10, w11);
-      gD = bil4(d00, d01, d10, d11, w00, w01, w10, w11);
-    }
-    PBA_SECT(4)  // projective Jacobian, weights, I/D gradient gathers
-    double* QA = Q;
-    double* bA = beta;
-    if (kProbe == 11) {
-      accumulate_cheap(QA, bA, gI, MP0, MP1, wI, e0);
-      accumulate_cheap(QA, bA, gD, MP0, MP1, wD, e1);
+    if constexpr (kLean) {
+      // Channel by channel: the four corner loads of one gradient plane are
+      // issued (volatile, so not hoisted together) only when that channel is
+      // accumulated — fewer load destinations live at once, traded for
+      // latency that the extra resident warps cover.
+      auto grad_at = [&](int plane) {
+        const double2* p0 = g00p + plane * dnp;
+        const double2* p1 = g10p + plane * dnp;
+        return bil4(ldg2_ordered(p0), ldg2_ordered(p0 + 1), ldg2_ordered(p1), ldg2_ordered(p1 + 1),
+                    w00, w01, w10, w11);
+      };
+      accumulate_channel(Q, beta, grad_at(0), MP0, MP1, nullptr, pu, nullptr, wI, e0);
+      accumulate_channel(Q, beta, grad_at(1), MP0, MP1, ud, pu, nullptr, wD, e1);
       if (normal_on) {
-        accumulate_cheap(QA, bA, make_double2(no[0], no[1]), MP0, MP1, wN, e2 + e3 + e4);
-      }
-      continue;
-    }
-    accumulate_channel(QA, bA, gI, MP0, MP1, nullptr, pu, nullptr, wI, e0);
-    accumulate_channel(QA, bA, gD, MP0, MP1, ud, pu, nullptr, wD, e1);
-    if (normal_on) {
-      double2 gN[3];
+        double xn[3];
 #pragma unroll
-      for (int k = 0; k < 3; ++k)
-        gN[k] = kProbe == 10 ? make_double2(gI.x * (k + 1), gD.y * k)
-                             : bil4(__ldg(g00p + (2 + k) * dnp), __ldg(g01p + (2 + k) * dnp),
-                                    __ldg(g10p + (2 + k) * dnp), __ldg(g11p + (2 + k) * dnp), w00,
-                                    w01, w10, w11);
-      double xn[3];
-      cross3(&S.Mi[0], no, xn);
-      accumulate_channel(QA, bA, gN[0], MP0, MP1, nullptr, pu, xn, wN * cfg.omega[2], e2);
-      cross3(&S.Mi[3], no, xn);
-      accumulate_channel(QA, bA, gN[1], MP0, MP1, nullptr, pu, xn, wN * cfg.omega[3], e3);
-      cross3(&S.Mi[6], no, xn);
-      accumulate_channel(QA, bA, gN[2], MP0, MP1, nullptr, pu, xn, wN * cfg.omega[4], e4);
+        for (int k = 0; k < 3; ++k) {
+          const Row4 r = setup_row(&S.MiC[4 * k]);
+          const double mr[3] = {r.a.x, r.a.y, r.b.x};
+          cross3(mr, no, xn);
+          accumulate_channel(Q, beta, grad_at(2 + k), MP0, MP1, nullptr, pu, xn,
+                             wN * (k == 0 ? o23.x : (k == 1 ? o23.y : o4.x)),
+                             k == 0 ? e2 : (k == 1 ? e3 : e4));
+        }
+      }
+    } else {
+      double2 gI, gD;
+      if (kProbe == 10) {  // ablation (diagnostics only): no gradient loads
+        gI = make_double2(a00.x * w00, a01.x * w01);
+        gD = make_double2(a10.y * w10, a11.y * w11);
+      } else {
+        const double2 i00 = __ldg(g00p), i01 = __ldg(g01p), i10 = __ldg(g10p), i11 = __ldg(g11p);
+        const double2 d00 = __ldg(g00p + dnp), d01 = __ldg(g01p + dnp), d10 = __ldg(g10p + dnp),
+                      d11 = __ldg(g11p + dnp);
+        gI = bil4(i00, i01, i10, i11, w00, w01, w10, w11);
+        gD = bil4(d00, d01, d10, d11, w00, w01, w10, w11);
+      }
+      PBA_SECT(4)  // projective Jacobian, weights, I/D gradient gathers
+      double* QA = Q;
+      double* bA = beta;
+      if (kProbe == 11) {
+        accumulate_cheap(QA, bA, gI, MP0, MP1, wI, e0);
+        accumulate_cheap(QA, bA, gD, MP0, MP1, wD, e1);
+        if (normal_on) {
+          accumulate_cheap(QA, bA, make_double2(no[0], no[1]), MP0, MP1, wN, e2 + e3 + e4);
+        }
+        continue;
+      }
+      accumulate_channel(QA, bA, gI, MP0, MP1, nullptr, pu, nullptr, wI, e0);
+      accumulate_channel(QA, bA, gD, MP0, MP1, ud, pu, nullptr, wD, e1);
+      if (normal_on) {
+        double2 gN[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+          gN[k] = kProbe == 10 ? make_double2(gI.x * (k + 1), gD.y * k)
+                               : bil4(__ldg(g00p + (2 + k) * dnp), __ldg(g01p + (2 + k) * dnp),
+                                      __ldg(g10p + (2 + k) * dnp), __ldg(g11p + (2 + k) * dnp), w00,
+                                      w01, w10, w11);
+        double xn[3];
+        {
+          const double mr[3] = {SV(S.Mi[0]), SV(S.Mi[1]), SV(S.Mi[2])};
+          cross3(mr, no, xn);
+        }
+        accumulate_channel(QA, bA, gN[0], MP0, MP1, nullptr, pu, xn, wN * SV(S.cfg.omega[2]), e2);
+        {
+          const double mr[3] = {SV(S.Mi[3]), SV(S.Mi[4]), SV(S.Mi[5])};
+          cross3(mr, no, xn);
+        }
+        accumulate_channel(QA, bA, gN[1], MP0, MP1, nullptr, pu, xn, wN * SV(S.cfg.omega[3]), e3);
+        {
+          const double mr[3] = {SV(S.Mi[6]), SV(S.Mi[7]), SV(S.Mi[8])};
+          cross3(mr, no, xn);
+        }
+        accumulate_channel(QA, bA, gN[2], MP0, MP1, nullptr, pu, xn, wN * SV(S.cfg.omega[4]), e4);
+      }
     }
     PBA_SECT(5)  // q rows + accumulation (incl. normal-gradient gathers)
   }
@@ -828,16 +1061,17 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
   if (int rc = ensure_atan_table()) return rc;
   if (n_chunks > 0) {
     // CTA-size / occupancy variant (PBA_LIN_VARIANT overrides):
+    //   6 (default): lean, 128 thr, 168 regs (12 warps/SM), no spills
     //   1: 256 thr, <=255 regs (8 warps/SM)    2: 256 thr, 128 regs (16 warps/SM)
-    //   3: 128 thr, 128 regs (16 warps/SM)     4: 128 thr, 168 regs (12 warps/SM)
+    //   3: 128 thr, 128 regs (16 warps/SM)     4: round-1 kernel, 128 thr, 168 regs
     //   5: 512 thr, 128 regs (16 warps/SM)
     //   9 / 20 / 21: diagnostics (fixed destination texel / no gradient
     //   gathers / reduced accumulation), see kProbe
     static int variant = -1;
     if (variant < 0) {
       const char* env = getenv("PBA_LIN_VARIANT");
-      variant = env ? atoi(env) : 4;
-      if (variant < 1 || variant > 24) variant = 4;
+      variant = env ? atoi(env) : 6;
+      if (variant < 1 || variant > 24) variant = 6;
     }
     const unsigned grid = (unsigned)n_chunks;
 #define PBA_LAUNCH_LIN(J, T, M) \
@@ -868,7 +1102,11 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
                                                                 chunk_pixels, poses, extrinsics,
                                                                 *cfg, partials);
           break;
-        default: PBA_LAUNCH_LIN(true, 128, 3); break;
+        case 4: PBA_LAUNCH_LIN(true, 128, 3); break;  // round-1 kernel (comparison)
+        default:  // 6: lean (DESIGN.md §3 K1)
+          linearize_kernel<true, 128, 3, 0, true><<<grid, 128, 0, st>>>(frames, pairs, chunk_table, pair_chunk_offsets,
+                                                                      chunk_pixels, poses, extrinsics, *cfg, partials);
+          break;
       }
     } else {
       // Cost-only (total_error) path: no accumulators, so it fits 96

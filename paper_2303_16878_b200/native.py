@@ -129,6 +129,11 @@ def _checked() -> bool:
 
 
 def library_path() -> Path:
+    import os
+
+    override = os.environ.get("PBA_LIBRARY")  # A/B experiments: another build of the same ABI
+    if override:
+        return Path(override)
     return _build.LIB_CHECKED if _checked() else _build.LIB
 
 
