@@ -168,6 +168,9 @@ struct PairSetup {
   alignas(16) double fx_cx[2], fy_cy[2], fx_fy[2], range[2], wh[2];
   alignas(16) double sqw0_dI[2], sqw1_dD[2], om01[2], om23[2], om4_dN[2];
   alignas(8) int dwh[2], np_sd[2];
+  alignas(16) int src_geo[4];      // stride, source width, source plane size, grid width
+  alignas(8) int src_mh[2];        // source model, source height
+  alignas(16) const void* src_ptrs[2];  // source texels, source ray table
 };
 
 // Loop reads of the CTA's pair setup.  kLean: every use is a volatile
@@ -220,6 +223,20 @@ __device__ __forceinline__ int2 pair_rd(const int* p) {
   return make_int2(p[0], p[1]);
 }
 #define SP(f) (pair_rd<kLean>(S.f))
+__device__ __forceinline__ int4 setup_quad(const int* p) {
+  int4 v;
+  asm volatile("ld.volatile.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"((unsigned)__cvta_generic_to_shared(p)));
+  return v;
+}
+__device__ __forceinline__ void setup_ptrs(const void* const* p, const double2*& a, const double*& b) {
+  unsigned long long x, y;
+  asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];"
+               : "=l"(x), "=l"(y) : "r"((unsigned)__cvta_generic_to_shared(p)));
+  a = reinterpret_cast<const double2*>(x);
+  b = reinterpret_cast<const double*>(y);
+}
 __device__ __forceinline__ int2 setup_pair(const int* p) {
   int2 v;
   asm volatile("ld.volatile.shared.v2.s32 {%0, %1}, [%2];"
@@ -453,6 +470,10 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     S.om4_dN[0] = cfg.omega[4], S.om4_dN[1] = cfg.huber_delta[2];
     S.dwh[0] = dc.width, S.dwh[1] = dc.height;
     S.np_sd[0] = S.src_np, S.np_sd[1] = S.dst_np;
+    S.src_geo[0] = S.stride, S.src_geo[1] = S.src_cam.width, S.src_geo[2] = S.src_np;
+    S.src_geo[3] = S.grid_w;
+    S.src_mh[0] = S.src_cam.model, S.src_mh[1] = S.src_cam.height;
+    S.src_ptrs[0] = S.src_tex, S.src_ptrs[1] = S.src_ray;
   }
   __syncthreads();
 
@@ -501,18 +522,29 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
   }
   for (int idx = first + (int)threadIdx.x; idx < last; idx += kT, gr = ngr, gcol = ngcol) {
     PBA_SECT(7)  // tail of the previous iteration (rejected pixels: their last section)
-    const int row = gr * SV(S.stride);
-    const int col = gcol * SV(S.stride);
-    const int sp = row * SV(S.src_cam.width) + col;
+    // source geometry: stride, width, plane size, grid width (kLean: one 16-byte load)
+    const int4 sg = kLean ? setup_quad(S.src_geo)
+                          : make_int4(S.stride, S.src_cam.width, S.src_np, S.grid_w);
+    const int row = gr * sg.x;
+    const int col = gcol * sg.x;
+    const int sp = row * sg.y + col;
+    const double2* s_tex;
+    const double* s_ray;
+    if constexpr (kLean) {
+      setup_ptrs(S.src_ptrs, s_tex, s_ray);
+    } else {
+      s_tex = S.src_tex;
+      s_ray = S.src_ray;
+    }
     // kLean: the source texel is loaded when its pixel starts (no prefetch:
     // the registers go to forming the projective Jacobian while the first
     // destination gather is in flight, kEarlyMP)
     constexpr bool kNoPrefetch = kLean;
     constexpr bool kEarlyMP = kLean;
     if constexpr (kNoPrefetch) {
-      const double2* t = SV(S.src_tex) + sp;
+      const double2* t = s_tex + sp;
       nx0 = __ldg(t);
-      nx2 = __ldg(t + kPairNzM * SV(S.src_np));
+      nx2 = __ldg(t + kPairNzM * sg.z);
     }
     const double2 s_id = nx0;  // I, D
     const uint32_t sm = mask_word(nx2);
@@ -520,11 +552,11 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
 
     ngr = gr;
     ngcol = gcol;
-    advance_pixel(ngr, ngcol, SV(S.grid_w), kT);
+    advance_pixel(ngr, ngcol, sg.w, kT);
     if (!kNoPrefetch && idx + kT < last) {
-      const double2* t = SV(S.src_tex) + PBA_DCHECK_INDEX(ngr * SV(S.stride) * SV(S.src_cam.width) + ngcol * SV(S.stride), SV(S.src_np));
+      const double2* t = s_tex + PBA_DCHECK_INDEX(ngr * sg.x * sg.y + ngcol * sg.x, sg.z);
       nx0 = __ldg(t);
-      nx2 = __ldg(t + kPairNzM * SV(S.src_np));
+      nx2 = __ldg(t + kPairNzM * sg.z);
     }
     if (!(sm & PBA_MASK_DEPTH_VALID)) continue;  // PairContext.build: usable = depth_valid
     PBA_SECT(0)  // source texel + next-texel prefetch
@@ -532,19 +564,20 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     // ---- source cue values and unprojection (sensors.py:133-154) ----
     const double d = s_id.y;
     double ps[3];
+    const int2 smh = kLean ? setup_pair(S.src_mh) : make_int2(S.src_cam.model, S.src_cam.height);
 #ifdef PBA_CHECKED
-    PBA_DCHECK_INDEX(col, SV(S.src_cam.width));
-    PBA_DCHECK_INDEX(row, SV(S.src_cam.height));
+    PBA_DCHECK_INDEX(col, sg.y);
+    PBA_DCHECK_INDEX(row, smh.y);
 #endif
-    if ((SV(S.src_cam.model) == PBA_SPHERICAL)) {
-      const double ca = __ldg(SV(S.src_ray) + col), sa = __ldg(SV(S.src_ray) + SV(S.src_cam.width) + col);
-      const double ce = __ldg(SV(S.src_ray) + 2 * SV(S.src_cam.width) + row), se = __ldg(SV(S.src_ray) + 2 * SV(S.src_cam.width) + SV(S.src_cam.height) + row);
+    if (smh.x == PBA_SPHERICAL) {
+      const double ca = __ldg(s_ray + col), sa = __ldg(s_ray + sg.y + col);
+      const double ce = __ldg(s_ray + 2 * sg.y + row), se = __ldg(s_ray + 2 * sg.y + smh.y + row);
       ps[0] = (ce * ca) * d;
       ps[1] = (ce * sa) * d;
       ps[2] = se * d;
     } else {
-      ps[0] = __ldg(SV(S.src_ray) + col) * d;
-      ps[1] = __ldg(SV(S.src_ray) + 2 * SV(S.src_cam.width) + row) * d;
+      ps[0] = __ldg(s_ray + col) * d;
+      ps[1] = __ldg(s_ray + 2 * sg.y + row) * d;
       ps[2] = d;
     }
     // p_u = R_o p + t_o (solver.py:215)
@@ -697,7 +730,7 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     double e2 = 0.0, e3 = 0.0, e4 = 0.0;
     double no[3] = {0.0, 0.0, 0.0};  // R_o n_src
     if (normal_on) {
-      const double2 s_n01 = __ldg(SV(S.src_tex) + kPairNxy * SV(S.src_np) + sp);  // source nx, ny
+      const double2 s_n01 = __ldg(s_tex + kPairNxy * sg.z + sp);  // source nx, ny
       const double ns2 = mask_src_nz;
       const double2 b00 = __ldg(t00 + kPairNxy * dnp), b01 = __ldg(t00 + kPairNxy * dnp + 1);
       const double2 b10 = __ldg(t10 + kPairNxy * dnp), b11 = __ldg(t10 + kPairNxy * dnp + 1);
