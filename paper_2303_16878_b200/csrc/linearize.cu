@@ -642,7 +642,10 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
       u = py_mod(__dadd_rn(__dmul_rn(fc.x, az), fc.y), SP(wh).x);
       v = __dadd_rn(__dmul_rn(fyc.x, el), fyc.y);
     } else {
-      if (!(pb[2] > 0.0)) continue;
+      {  // z > 0 and the depth range (sensors.py:112-113, 125) before the divisions
+        const double2 rg = SP(range);
+        if (!(pb[2] > 0.0 && pb[2] >= rg.x && pb[2] <= rg.y)) continue;
+      }
       // u, v with true IEEE division and separate roundings, exactly as the
       // reference (sensors.py:114-115): self-projections land on integer
       // pixels where a last-bit difference would move floor() and flip validity.
@@ -652,16 +655,15 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
       inv_dist = __drcp_rn(pb[2]);  // Jacobian only
       dist = pb[2];
     }
-    {
-      const double2 rg = SP(range);
-      if (!(dist >= rg.x && dist <= rg.y)) continue;
-    }
+    // (the depth range was checked in each model's branch)
+    // project's bounds 0 <= u < W, 0 <= v < H (sensors.py:126-127) and
+    // sample's inside test u <= W - 1, v <= H - 1 (cues.py:400) in one test:
+    // u <= W - 1 implies u < W
     const double2 whd = SP(wh);
-    if (!(u >= 0.0 && u < whd.x && v >= 0.0 && v < whd.y)) continue;
+    if (!(u >= 0.0 && v >= 0.0 && u <= whd.x - 1.0 && v <= whd.y - 1.0)) continue;
 
     PBA_SECT(1)  // unprojection + warp + projection
-    // ---- bilinear footprint and validity (cues.py:397-409, 451-456) ----
-    if (!(u <= whd.x - 1.0 && v <= whd.y - 1.0)) continue;  // inside (u, v >= 0 already)
+    // ---- bilinear footprint (cues.py:397-409, 451-456) ----
     const int2 dwh = SP(dwh);
     int x0 = (int)floor(u), y0 = (int)floor(v);
     x0 = min(max(x0, 0), dwh.x - 2);
@@ -718,11 +720,12 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     // zeta_d: range for spherical, z for pinhole (solver.py:240)
     const double zeta = dsph ? dist : pb[2];
     const double e1 = zeta - Dd;
-    if (e1 > SV(S.occ_tol)) continue;  // occluded (solver.py:254-258)
-    if (kJac && dsph) {
-      if (!kEarlyMP) rho2 = pb[0] * pb[0] + pb[1] * pb[1];
-      if (!(rho2 > 0.0)) continue;  // ok_jac (sensors.py:173-175; solver.py:262-263)
+    if constexpr (!kEarlyMP) {
+      if (kJac && dsph) rho2 = pb[0] * pb[0] + pb[1] * pb[1];
     }
+    // occluded (solver.py:254-258), or no Jacobian (ok_jac, sensors.py:173-175,
+    // solver.py:262-263; the Jacobian path only)
+    if (e1 > SV(S.occ_tol) || (kJac && dsph && !(rho2 > 0.0))) continue;
     const double e0 = s_id.x - bil(a00.x, a01.x, a10.x, a11.x, wx, wy);
 
     PBA_SECT(2)  // footprint, first destination gather, masks, occlusion
@@ -773,14 +776,17 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     const double inv_sN = tN > 1e-300 ? rsqrt(tN) : 0.0;
     double sN = tN > 1e-300 ? tN * inv_sN : sqrt(tN);
     const double dI = hI.y, dD = hD.y, dN = o4.y;
-    if (fabs(sI - dI) <= 1e-14 * dI)
-      sI = __dsqrt_rn(__dmul_rn(__dmul_rn(e0, e0), SV(S.cfg.omega[0])));
-    if (fabs(sD - dD) <= 1e-14 * dD)
-      sD = __dsqrt_rn(__dmul_rn(__dmul_rn(e1, e1), SV(S.cfg.omega[1])));
-    if (fabs(sN - dN) <= 1e-14 * dN)
-      sN = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(e2, e2), o23.x),
-                                          __dmul_rn(__dmul_rn(e3, e3), o23.y)),
-                                __dmul_rn(__dmul_rn(e4, e4), o4.x)));
+    const bool nearI = fabs(sI - dI) <= 1e-14 * dI, nearD = fabs(sD - dD) <= 1e-14 * dD;
+    const bool nearN = fabs(sN - dN) <= 1e-14 * dN;
+    if (nearI || nearD || nearN) {  // rare: one branch for the three exact re-takes
+      const double2 o01x = SP(om01);
+      if (nearI) sI = __dsqrt_rn(__dmul_rn(__dmul_rn(e0, e0), o01x.x));
+      if (nearD) sD = __dsqrt_rn(__dmul_rn(__dmul_rn(e1, e1), o01x.y));
+      if (nearN)
+        sN = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(e2, e2), o23.x),
+                                            __dmul_rn(__dmul_rn(e3, e3), o23.y)),
+                                  __dmul_rn(__dmul_rn(e4, e4), o4.x)));
+    }
     const bool smI = sI <= dI, smD = sD <= dD, smN = sN <= dN;
     cost += (smI ? sI * sI : dI * (2.0 * sI - dI)) + (smD ? sD * sD : dD * (2.0 * sD - dD)) +
             (smN ? sN * sN : dN * (2.0 * sN - dN));
