@@ -839,22 +839,34 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
       // issued (volatile, so not hoisted together) only when that channel is
       // accumulated — fewer load destinations live at once, traded for
       // latency that the extra resident warps cover.
-      auto grad_at = [&](int plane) {
+      // One plane of look-ahead: the next channel's four corners are in
+      // flight while the current channel accumulates.
+      struct Corners {
+        double2 c00, c01, c10, c11;
+      };
+      auto load_plane = [&](int plane) {
         const double2* p0 = g00p + plane * dnp;
         const double2* p1 = g10p + plane * dnp;
-        return bil4(ldg2_ordered(p0), ldg2_ordered(p0 + 1), ldg2_ordered(p1), ldg2_ordered(p1 + 1),
-                    w00, w01, w10, w11);
+        return Corners{ldg2_ordered(p0), ldg2_ordered(p0 + 1), ldg2_ordered(p1),
+                       ldg2_ordered(p1 + 1)};
       };
-      accumulate_channel(Q, beta, grad_at(0), MP0, MP1, nullptr, pu, nullptr, wI, e0);
-      accumulate_channel(Q, beta, grad_at(1), MP0, MP1, ud, pu, nullptr, wD, e1);
+      auto interp = [&](const Corners& c) { return bil4(c.c00, c.c01, c.c10, c.c11, w00, w01, w10, w11); };
+      Corners cur = load_plane(0);
+      Corners nxt = load_plane(1);
+      accumulate_channel(Q, beta, interp(cur), MP0, MP1, nullptr, pu, nullptr, wI, e0);
+      cur = nxt;
+      if (normal_on) nxt = load_plane(2);
+      accumulate_channel(Q, beta, interp(cur), MP0, MP1, ud, pu, nullptr, wD, e1);
       if (normal_on) {
         double xn[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
+          cur = nxt;
+          if (k < 2) nxt = load_plane(3 + k);
           const Row4 r = setup_row(&S.MiC[4 * k]);
           const double mr[3] = {r.a.x, r.a.y, r.b.x};
           cross3(mr, no, xn);
-          accumulate_channel(Q, beta, grad_at(2 + k), MP0, MP1, nullptr, pu, xn,
+          accumulate_channel(Q, beta, interp(cur), MP0, MP1, nullptr, pu, xn,
                              wN * (k == 0 ? o23.x : (k == 1 ? o23.y : o4.x)),
                              k == 0 ? e2 : (k == 1 ? e3 : e4));
         }

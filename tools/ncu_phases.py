@@ -56,7 +56,7 @@ def phases(src_lines):
     """line -> phase, from the section comments of the pixel loop."""
     marks = [("---- source cue values and unprojection", "unproject + warp"),
              ("---- project into the destination", "project (+ table atan2)"),
-             ("---- bilinear footprint and validity", "dst gather + occlusion"),
+             ("---- bilinear footprint", "dst gather + occlusion"),
              ("const bool normal_on", "normals"),
              ("---- per-cue Huber", "huber + cost"),
              ("const double wI = smI", "weights"),
