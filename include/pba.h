@@ -206,6 +206,16 @@ size_t pba_solve_work_bytes(int32_t dim);
 int pba_solve_dense(const double* H, const double* b, int32_t dim, double lam,
                     const int32_t* tile_env, void* work, double* delta, int32_t* status,
                     void* stream);
+/* Graph-capturable form: lambda read from device memory (lam_dev, one
+ * double; NULL -> lam) when the kernels run, and with PBA_SOLVE_REUSE_PLAN
+ * the tile tables a previous call with the same dim / tile_env put in
+ * `work` are reused instead of copied from the host again — so the call
+ * issues only kernel launches and a memset, and a captured LM step replays
+ * with a new lambda. */
+#define PBA_SOLVE_REUSE_PLAN 1
+int pba_solve_dense_ex(const double* H, const double* b, int32_t dim, double lam,
+                       const double* lam_dev, const int32_t* tile_env, void* work, int32_t flags,
+                       double* delta, int32_t* status, void* stream);
 
 /* ---- the same system by block-Jacobi PCG (App. C c3: "LM with block-Jacobi
  * PCG"); replaces np.linalg.solve at solver.py:510-512 by an iterative solve.
@@ -224,6 +234,11 @@ size_t pba_pcg_work_bytes(int32_t n_free);
 int pba_solve_pcg(const double* H, const double* b, int32_t n_free, double lam,
                   const int32_t* row_ptr, const int32_t* cols, int32_t max_iter, double tol,
                   void* work, double* delta, int32_t* status, double* info, void* stream);
+/* The same with lambda read from device memory (lam_dev; NULL -> lam). */
+int pba_solve_pcg_ex(const double* H, const double* b, int32_t n_free, double lam,
+                     const double* lam_dev, const int32_t* row_ptr, const int32_t* cols,
+                     int32_t max_iter, double tol, void* work, double* delta, int32_t* status,
+                     double* info, void* stream);
 
 /* ---- pose update: _LevelProblem.apply_step (solver.py:451-460) --------
  * poses_out[k] = poses_in[k] * exp(delta[slot_k]) for every non-gauge pose

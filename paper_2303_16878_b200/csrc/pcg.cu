@@ -201,11 +201,13 @@ __device__ void grid_sum2(const double* partials, int grid, int s0, int s1, doub
 }
 
 __global__ void __launch_bounds__(kPcgThreads)
-    pcg_kernel(const double* __restrict__ H, const double* __restrict__ b, int n_free, double lam,
+    pcg_kernel(const double* __restrict__ H, const double* __restrict__ b, int n_free,
+               double lam_arg, const double* __restrict__ lam_dev,
                const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ cols,
                int max_iter, double tol, PcgWork w, double* __restrict__ delta,
                int32_t* __restrict__ status, double* __restrict__ info) {
   cg::grid_group grid = cg::this_grid();
+  const double lam = lam_dev ? *lam_dev : lam_arg;  // device lambda: graph-replayable step
   __shared__ double red[2][kPcgWarps];
   __shared__ double mv[6 * kPcgRows];  // mat-vec results of the pass
   __shared__ double rb[6 * kPcgRows];  // residual of the pass (block-Jacobi needs whole blocks)
@@ -411,10 +413,10 @@ extern "C" size_t pba_pcg_work_bytes(int32_t n_free) {
          5 * align_up(dim * sizeof(double), 256) + align_up(4 * max_grid * sizeof(double), 256);
 }
 
-extern "C" int pba_solve_pcg(const double* H, const double* b, int32_t n_free, double lam,
-                             const int32_t* row_ptr, const int32_t* cols, int32_t max_iter,
-                             double tol, void* work, double* delta, int32_t* status,
-                             double* info, void* stream) {
+extern "C" int pba_solve_pcg_ex(const double* H, const double* b, int32_t n_free, double lam,
+                                const double* lam_dev, const int32_t* row_ptr,
+                                const int32_t* cols, int32_t max_iter, double tol, void* work,
+                                double* delta, int32_t* status, double* info, void* stream) {
   PBA_ARG_CHECK(n_free > 0, "n_free must be positive");
   PBA_ARG_CHECK(max_iter >= 1 && tol >= 0.0, "bad iteration limit or tolerance");
   PBA_ARG_CHECK(H && b && row_ptr && cols && work && delta && status && info, "NULL buffer");
@@ -432,11 +434,20 @@ extern "C" int pba_solve_pcg(const double* H, const double* b, int32_t n_free, d
   PBA_ARG_CHECK(grid <= 148 * 16, "cooperative grid larger than the work buffer allows");
   PcgWork w = carve(work, n_free, grid);
   PBA_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int32_t), st));
-  void* args[] = {(void*)&H,   (void*)&b,        (void*)&n_free, (void*)&lam,
-                  (void*)&row_ptr, (void*)&cols, (void*)&max_iter, (void*)&tol,
-                  (void*)&w,   (void*)&delta,    (void*)&status, (void*)&info};
+  void* args[] = {(void*)&H,       (void*)&b,    (void*)&n_free,   (void*)&lam,
+                  (void*)&lam_dev, (void*)&row_ptr, (void*)&cols, (void*)&max_iter,
+                  (void*)&tol,     (void*)&w,    (void*)&delta,    (void*)&status,
+                  (void*)&info};
   PBA_CUDA_TRY(cudaLaunchCooperativeKernel((void*)pcg_kernel, dim3(grid), dim3(kPcgThreads), args,
                                            0, st));
   PBA_LAUNCH_CHECK();
   return PBA_OK;
+}
+
+extern "C" int pba_solve_pcg(const double* H, const double* b, int32_t n_free, double lam,
+                             const int32_t* row_ptr, const int32_t* cols, int32_t max_iter,
+                             double tol, void* work, double* delta, int32_t* status,
+                             double* info, void* stream) {
+  return pba_solve_pcg_ex(H, b, n_free, lam, nullptr, row_ptr, cols, max_iter, tol, work, delta,
+                          status, info, stream);
 }

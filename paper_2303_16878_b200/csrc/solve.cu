@@ -71,10 +71,12 @@ SolveWork carve(void* work, int dim) {
   return w;
 }
 
-__global__ void damp_copy_kernel(const double* __restrict__ H, int dim, double lam,
+__global__ void damp_copy_kernel(const double* __restrict__ H, int dim, double lam_arg,
+                                 const double* __restrict__ lam_dev,
                                  const int32_t* __restrict__ env, double* __restrict__ A) {
   const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (long)dim * dim) return;
+  const double lam = lam_dev ? *lam_dev : lam_arg;  // device lambda: graph-replayable step
   const int i = (int)(t / dim), j = (int)(t - (long)i * dim);
   if (j > i || j / NB < env[i / NB]) return;
   const double h = H[t];
@@ -512,10 +514,12 @@ __global__ void __launch_bounds__(256) syrk_kernel(double* __restrict__ A, int d
 
 // Ap (D x D, lower) = P (H + lam diag H) P^T on the structural tiles listed in
 // tiles (pairs of new tile indices, row >= col); padding rows are identity.
-__global__ void damp_copy_perm_kernel(const double* __restrict__ H, int dim, double lam, int D,
+__global__ void damp_copy_perm_kernel(const double* __restrict__ H, int dim, double lam_arg,
+                                      const double* __restrict__ lam_dev, int D,
                                       const int32_t* __restrict__ tiles,
                                       const int32_t* __restrict__ new_to_old,
                                       double* __restrict__ Ap) {
+  const double lam = lam_dev ? *lam_dev : lam_arg;
   const int ti = tiles[2 * blockIdx.x], tj = tiles[2 * blockIdx.x + 1];
   const int oi = new_to_old[ti], oj = new_to_old[tj];
   for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
@@ -717,8 +721,35 @@ using namespace pba;
 // tile.  Sequential steps: 2 * max segment length + (P - 1) * w instead of T.
 // Each tile update is the same arithmetic as the sequential path, in the
 // order of the new elimination sequence.
-int solve_dissected(const double* H, const double* b, int dim, double lam,
-                    const std::vector<int32_t>& env, const std::vector<int32_t>& last,
+// Dynamic shared-memory limits of the tile kernels, set once per device (so
+// a captured solve issues no attribute calls).
+int set_solver_smem_attributes() {
+  static bool done[64] = {false};
+  int dev = 0;
+  PBA_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev >= 0 && dev < 64 && done[dev]) return PBA_OK;
+  const int tile_smem = 2 * NB * LD * sizeof(double);
+  const int reg_smem = tile_smem + (NB / PW - 1) * PW * (PW + 1) * (int)sizeof(double);
+  PBA_CUDA_TRY(cudaFuncSetAttribute(syrk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    tile_smem));
+  PBA_CUDA_TRY(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    tile_smem));
+  PBA_CUDA_TRY(cudaFuncSetAttribute(potrf_inv_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));
+  PBA_CUDA_TRY(cudaFuncSetAttribute(potrf_reg_kernel<true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, reg_smem));
+  PBA_CUDA_TRY(cudaFuncSetAttribute(potrf_reg_kernel<false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, reg_smem));
+  PBA_CUDA_TRY(cudaFuncSetAttribute(panel_list_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));
+  PBA_CUDA_TRY(cudaFuncSetAttribute(syrk_list_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));
+  if (dev >= 0 && dev < 64) done[dev] = true;
+  return PBA_OK;
+}
+
+int solve_dissected(const double* H, const double* b, int dim, double lam, const double* lam_dev,
+                    bool reuse, const std::vector<int32_t>& env, const std::vector<int32_t>& last,
                     const SolveWork& w, double* delta, int32_t* status, cudaStream_t st) {
   const int T = (int)env.size(), D = T * NB;
   int band = 0;
@@ -828,14 +859,16 @@ int solve_dissected(const double* H, const double* b, int dim, double lam,
   int32_t* d_lists = w.lists;
   int32_t* d_env = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(w.nz) +
                                               align_up((size_t)T * T * sizeof(int32_t), 256));
-  PBA_CUDA_TRY(cudaMemcpyAsync(d_lists, staging.data(), off_nz * sizeof(int32_t),
-                               cudaMemcpyHostToDevice, st));
-  PBA_CUDA_TRY(cudaMemcpyAsync(w.nz, staging.data() + off_nz, (size_t)T * T * sizeof(int32_t),
-                               cudaMemcpyHostToDevice, st));
-  PBA_CUDA_TRY(cudaMemcpyAsync(d_env, staging.data() + off_nz + (size_t)T * T,
-                               2 * T * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  if (!reuse) {  // the tables depend only on (dim, tile_env): a reused plan is already there
+    PBA_CUDA_TRY(cudaMemcpyAsync(d_lists, staging.data(), off_nz * sizeof(int32_t),
+                                 cudaMemcpyHostToDevice, st));
+    PBA_CUDA_TRY(cudaMemcpyAsync(w.nz, staging.data() + off_nz, (size_t)T * T * sizeof(int32_t),
+                                 cudaMemcpyHostToDevice, st));
+    PBA_CUDA_TRY(cudaMemcpyAsync(d_env, staging.data() + off_nz + (size_t)T * T,
+                                 2 * T * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  }
   const int32_t* d_n2o = d_lists;
-  damp_copy_perm_kernel<<<(unsigned)(tiles.size() / 2), 256, 0, st>>>(H, dim, lam, D,
+  damp_copy_perm_kernel<<<(unsigned)(tiles.size() / 2), 256, 0, st>>>(H, dim, lam, lam_dev, D,
                                                                     d_lists + off_tiles, d_n2o,
                                                                     w.A);
   PBA_LAUNCH_CHECK();
@@ -843,14 +876,7 @@ int solve_dissected(const double* H, const double* b, int dim, double lam,
   PBA_LAUNCH_CHECK();
   const int tile_smem = 2 * NB * LD * sizeof(double);
   const int reg_smem = tile_smem + (NB / PW - 1) * PW * (PW + 1) * (int)sizeof(double);
-  PBA_CUDA_TRY(cudaFuncSetAttribute(potrf_reg_kernel<true>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, reg_smem));
-  PBA_CUDA_TRY(cudaFuncSetAttribute(potrf_reg_kernel<false>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, reg_smem));
-  PBA_CUDA_TRY(cudaFuncSetAttribute(panel_list_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));
-  PBA_CUDA_TRY(cudaFuncSetAttribute(syrk_list_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));
+  if (int rc = set_solver_smem_attributes()) return rc;
   for (const Launch& L : launches) {
     if (potrf_rb())
       potrf_reg_kernel<true><<<L.nk, 256, reg_smem, st>>>(w.A, D, 0, d_lists + off_k + L.k0,
@@ -897,9 +923,10 @@ extern "C" size_t pba_solve_work_bytes(int32_t dim) {
          align_up(T * T * sizeof(int32_t), 256) + align_up(2 * T * sizeof(int32_t), 256);
 }
 
-extern "C" int pba_solve_dense(const double* H, const double* b, int32_t dim, double lam,
-                               const int32_t* tile_env, void* work, double* delta,
-                               int32_t* status, void* stream) {
+extern "C" int pba_solve_dense_ex(const double* H, const double* b, int32_t dim, double lam,
+                                  const double* lam_dev, const int32_t* tile_env, void* work,
+                                  int32_t flags, double* delta, int32_t* status, void* stream) {
+  const bool reuse = (flags & PBA_SOLVE_REUSE_PLAN) != 0;
   PBA_ARG_CHECK(dim > 0, "dim must be positive");
   PBA_ARG_CHECK(H && b && work && delta && status, "NULL buffer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -931,7 +958,7 @@ extern "C" int pba_solve_dense(const double* H, const double* b, int32_t dim, do
   }
   if (dissect && potrf_variant == 1) {
     PBA_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int32_t), st));
-    const int rc = solve_dissected(H, b, dim, lam, env, last, w, delta, status, st);
+    const int rc = solve_dissected(H, b, dim, lam, lam_dev, reuse, env, last, w, delta, status, st);
     if (rc != 1) return rc;  // 1: structure not suited, the sequential path follows
   }
   int32_t* d_env = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(w.nz) +
@@ -939,28 +966,22 @@ extern "C" int pba_solve_dense(const double* H, const double* b, int32_t dim, do
   int32_t* d_last = d_env + T;
   // the tables are tiny; copy them with the stream so the call stays asynchronous
   static thread_local std::vector<int32_t> staging;
-  staging.assign(env.begin(), env.end());
-  staging.insert(staging.end(), last.begin(), last.end());
-  PBA_CUDA_TRY(cudaMemcpyAsync(d_env, staging.data(), 2 * T * sizeof(int32_t),
-                               cudaMemcpyHostToDevice, st));
+  if (!reuse) {
+    staging.assign(env.begin(), env.end());
+    staging.insert(staging.end(), last.begin(), last.end());
+    PBA_CUDA_TRY(cudaMemcpyAsync(d_env, staging.data(), 2 * T * sizeof(int32_t),
+                                 cudaMemcpyHostToDevice, st));
+  }
   PBA_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int32_t), st));
   const long n2 = (long)dim * dim;
-  damp_copy_kernel<<<(unsigned)((n2 + 255) / 256), 256, 0, st>>>(H, dim, lam, d_env, w.A);
+  damp_copy_kernel<<<(unsigned)((n2 + 255) / 256), 256, 0, st>>>(H, dim, lam, lam_dev, d_env,
+                                                                   w.A);
   PBA_LAUNCH_CHECK();
   tile_flags_kernel<<<dim3(T, T), 256, 0, st>>>(w.A, dim, T, d_env, w.nz);
   PBA_LAUNCH_CHECK();
   const int tile_smem = 2 * NB * LD * sizeof(double);
-  PBA_CUDA_TRY(cudaFuncSetAttribute(syrk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    tile_smem));
-  PBA_CUDA_TRY(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    tile_smem));
-  PBA_CUDA_TRY(cudaFuncSetAttribute(potrf_inv_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));
   const int reg_smem = tile_smem + (NB / PW - 1) * PW * (PW + 1) * (int)sizeof(double);
-  PBA_CUDA_TRY(cudaFuncSetAttribute(potrf_reg_kernel<true>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, reg_smem));
-  PBA_CUDA_TRY(cudaFuncSetAttribute(potrf_reg_kernel<false>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, reg_smem));
+  if (int rc = set_solver_smem_attributes()) return rc;
   for (int k = 0; k < T; ++k) {
     if (potrf_variant == 1 && potrf_rb())
       potrf_reg_kernel<true><<<1, 256, reg_smem, st>>>(w.A, dim, k, nullptr, w.Linv, status);
@@ -981,4 +1002,10 @@ extern "C" int pba_solve_dense(const double* H, const double* b, int32_t dim, do
                                       status);
   PBA_LAUNCH_CHECK();
   return PBA_OK;
+}
+
+extern "C" int pba_solve_dense(const double* H, const double* b, int32_t dim, double lam,
+                               const int32_t* tile_env, void* work, double* delta,
+                               int32_t* status, void* stream) {
+  return pba_solve_dense_ex(H, b, dim, lam, nullptr, tile_env, work, 0, delta, status, stream);
 }

@@ -308,6 +308,19 @@ class DeviceLevel:
             * math.ceil(c[2].pyramid.levels[level].intrinsics.height / stride) for c in mine)
         self._scal = torch.zeros(8, dtype=torch.float64, device=dev)
         self._scal_host = torch.zeros(8, dtype=torch.float64).pin_memory()
+        # LM damping read by the solve kernels from device memory, so one
+        # captured step (solve -> update -> linearise -> assemble -> readback)
+        # replays with a new lambda (CUDA graph per current buffer, try_step)
+        self._lam_dev = torch.zeros(1, dtype=torch.float64, device=dev)
+        self._lam_host = torch.zeros(1, dtype=torch.float64).pin_memory()
+        self._plan_ready = False
+        self._graphs = [None, None]
+        self._graph_events = [None, None]
+        self._eager_steps = [0, 0]
+        self._graph_failed = False
+        self._capture_lin_events = None
+        self._graph_nlaunch = [0, 0]        # library kernels in each captured step
+        self.graph_launches_replayed = 0    # library kernels launched through replays
         self.poses = [torch.zeros((self.n_poses, 12), dtype=torch.float64, device=dev)
                       for _ in range(2)]
         self.gens = [torch.zeros(self.n_poses, dtype=torch.int32, device=dev) for _ in range(2)]
@@ -369,19 +382,25 @@ class DeviceLevel:
         """Per-pair records of this shard at `poses_t` (device (N,12) fp64)."""
         if self.n_pairs == 0:
             return self.records[:0]
-        ev = self.kernel_events
-        if ev is not None:
+        stream = torch.cuda.current_stream(self.device)
+        cap = getattr(self, "_capture_lin_events", None)  # graph-owned events while capturing
+        ev = self.kernel_events if cap is None else None
+        if cap is not None:
+            cap[0].record(stream)
+        elif ev is not None:
             e0 = torch.cuda.Event(enable_timing=True)
-            e0.record(torch.cuda.current_stream(self.device))
+            e0.record(stream)
         N.check(self.lib.pba_linearize(
             self.frames_t.data_ptr(), self.pairs_t.data_ptr(), self.n_pairs,
             self.chunks_t.data_ptr(), self.n_chunks, self.offsets_t.data_ptr(), self.chunk_pixels,
             poses_t.data_ptr(), self.ext_t.data_ptr(), ctypes.byref(self.ccfg),
             int(bool(want_jacobians)), self.partials.data_ptr(), self.records.data_ptr(),
-            _stream_ptr(self.device)), "pba_linearize")
-        if ev is not None:
+            stream.cuda_stream), "pba_linearize")
+        if cap is not None:
+            cap[1].record(stream)
+        elif ev is not None:
             e1 = torch.cuda.Event(enable_timing=True)
-            e1.record(torch.cuda.current_stream(self.device))
+            e1.record(stream)
             ev.append((e0, e1))
         return self.records[: self.n_pairs]
 
@@ -397,26 +416,33 @@ class DeviceLevel:
         N.check(self.lib.pba_sum_totals(records.data_ptr(), records.shape[0], out.data_ptr(),
                                         _stream_ptr(self.device)), "pba_sum_totals")
 
-    def solve(self, which: int, lam: float, status_ptr: int) -> None:
-        ev = self.solve_events
+    def solve(self, which: int, lam, status_ptr: int) -> None:
+        """Damped solve of buffer `which`.  lam=None: lambda is read from
+        self._lam_dev on the device (the captured-step form)."""
+        ev = self.solve_events if getattr(self, "_capture_lin_events", None) is None else None
         if ev is not None:
             e0 = torch.cuda.Event(enable_timing=True)
             e0.record(torch.cuda.current_stream(self.device))
+        lam_v = 0.0 if lam is None else float(lam)
+        lam_p = self._lam_dev.data_ptr() if lam is None else None
         if self.pcg:
             rp, cols = self.pcg_rows
-            N.check(self.lib.pba_solve_pcg(self.H[which].data_ptr(), self.b[which].data_ptr(),
-                                           self.n_free, float(lam), rp.data_ptr(), cols.data_ptr(),
-                                           int(getattr(self.cfg, "pcg_max_iterations", 2000)),
-                                           float(getattr(self.cfg, "pcg_tolerance", 1e-12)),
-                                           self.pcg_work.data_ptr(), self.delta.data_ptr(),
-                                           status_ptr, self.pcg_info.data_ptr(),
-                                           _stream_ptr(self.device)), "pba_solve_pcg")
+            N.check(self.lib.pba_solve_pcg_ex(self.H[which].data_ptr(), self.b[which].data_ptr(),
+                                              self.n_free, lam_v, lam_p, rp.data_ptr(),
+                                              cols.data_ptr(),
+                                              int(getattr(self.cfg, "pcg_max_iterations", 2000)),
+                                              float(getattr(self.cfg, "pcg_tolerance", 1e-12)),
+                                              self.pcg_work.data_ptr(), self.delta.data_ptr(),
+                                              status_ptr, self.pcg_info.data_ptr(),
+                                              _stream_ptr(self.device)), "pba_solve_pcg_ex")
         else:
-            N.check(self.lib.pba_solve_dense(self.H[which].data_ptr(), self.b[which].data_ptr(),
-                                             self.dim, float(lam), self.tile_env.ctypes.data,
-                                             self.work.data_ptr(),
-                                             self.delta.data_ptr(), status_ptr,
-                                             _stream_ptr(self.device)), "pba_solve_dense")
+            flags = N.PBA_SOLVE_REUSE_PLAN if self._plan_ready else 0
+            N.check(self.lib.pba_solve_dense_ex(self.H[which].data_ptr(), self.b[which].data_ptr(),
+                                                self.dim, lam_v, lam_p, self.tile_env.ctypes.data,
+                                                self.work.data_ptr(), flags,
+                                                self.delta.data_ptr(), status_ptr,
+                                                _stream_ptr(self.device)), "pba_solve_dense_ex")
+            self._plan_ready = True  # the tile tables are now in self.work
         if ev is not None:
             e1 = torch.cuda.Event(enable_timing=True)
             e1.record(torch.cuda.current_stream(self.device))
@@ -461,15 +487,91 @@ class DeviceLevel:
     def try_step(self, lam: float):
         """solve -> update -> linearise + assemble the candidate, one readback.
 
+        The second and later steps from the same current buffer replay a
+        CUDA graph of this whole sequence (lambda in device memory), so a
+        small problem's step costs one graph launch instead of ~20 kernel
+        launches and their host calls (PBA_GRAPH=0 disables it).
+
         Returns (solve_ok, step_ok, new_cost, new_count)."""
         cur, cand = self.cur, 1 - self.cur
+        if self._graph_enabled():
+            g = self._graphs[cur]
+            if g is None and self._plan_ready:
+                g = self._capture_step(cur)
+            if g is not None:
+                self._lam_host[0] = lam
+                g.replay()
+                self.graph_launches_replayed += self._graph_nlaunch[cur]
+                torch.cuda.current_stream(self.device).synchronize()
+                ev = self._graph_events[cur]
+                if ev is not None and self.kernel_events is not None:
+                    self.kernel_events.append(ev[0].elapsed_time(ev[1]))
+                if ev is not None and self.solve_events is not None and self.has_solver:
+                    self.solve_events.append(ev[2].elapsed_time(ev[3]))
+                vals = self._scal_host.numpy().copy()
+                ints = self._scal_host.view(torch.int32).numpy().copy()
+                return ints[4] == 0, ints[6] == 0, float(vals[0]), int(round(vals[1]))
+        self._eager_steps[cur] += 1
+        self._step_body(cur, cand, lam)
+        vals, ints = self._read_scalars()
+        return ints[4] == 0, ints[6] == 0, float(vals[0]), int(round(vals[1]))
+
+    def _step_body(self, cur: int, cand: int, lam) -> None:
         self.solve(cur, lam, self._status_solve_ptr)
         self.apply_step(cur, cand, self._status_step_ptr)
         recs = self.linearize(self.poses[cand])
         self.assemble(recs, cand)
         self._scal[0:2].copy_(self.totals[cand])
-        vals, ints = self._read_scalars()
-        return ints[4] == 0, ints[6] == 0, float(vals[0]), int(round(vals[1]))
+
+    # ---- CUDA-graph step ------------------------------------------------------
+    def prepare_graphs(self) -> None:
+        """Capture the step graphs of both buffers now (after one eager step),
+        so no capture happens inside a timed loop."""
+        if self._graph_enabled() and self._plan_ready:
+            for c in (0, 1):
+                if self._graphs[c] is None:
+                    self._capture_step(c)
+
+    def _graph_enabled(self) -> bool:
+        import os
+
+        return (self.has_solver and not self._graph_failed
+                and os.environ.get("PBA_GRAPH", "1") != "0")
+
+    def _capture_step(self, cur: int):
+        """Capture one try_step from buffer `cur` (lambda from pinned host
+        memory -> device, solve, update, linearise, assemble, scalars -> pinned
+        host memory).  Events around the linearisation and the solve are
+        captured too, so the bench can still time the kernels per replay."""
+        cand = 1 - cur
+        stream = torch.cuda.Stream(self.device)
+        stream.wait_stream(torch.cuda.current_stream(self.device))
+        g = torch.cuda.CUDAGraph()
+        events = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(4)]
+        n0 = int(self.lib.pba_kernel_launches())
+        try:
+            with torch.cuda.graph(g, stream=stream):
+                self._capture_lin_events = (events[0], events[1])
+                self._lam_dev.copy_(self._lam_host, non_blocking=True)
+                events[2].record()
+                self.solve(cur, None, self._status_solve_ptr)
+                events[3].record()
+                self.apply_step(cur, cand, self._status_step_ptr)
+                recs = self.linearize(self.poses[cand])
+                self.assemble(recs, cand)
+                self._scal[0:2].copy_(self.totals[cand])
+                self._scal_host.copy_(self._scal, non_blocking=True)
+        except Exception:  # capture unsupported here (e.g. the cooperative PCG launch)
+            self._graph_failed = True
+            self._capture_lin_events = None
+            torch.cuda.synchronize(self.device)
+            return None
+        self._capture_lin_events = None
+        torch.cuda.current_stream(self.device).wait_stream(stream)
+        self._graph_nlaunch[cur] = int(self.lib.pba_kernel_launches()) - n0
+        self._graphs[cur] = g
+        self._graph_events[cur] = events
+        return g
 
     def accept(self) -> None:
         self.cur = 1 - self.cur

@@ -24,6 +24,7 @@ PBA_RASTER_U16_INTENSITY = 1
 PBA_RASTER_U16_DEPTH = 2
 PBA_PINHOLE = 0
 PBA_SPHERICAL = 1
+PBA_SOLVE_REUSE_PLAN = 1
 RECORD_DOUBLES = 92
 NORMALS_RECHECK_DOUBLES = 10
 PARTIAL_DOUBLES = 32
@@ -35,7 +36,8 @@ EXPORTED = (
     "pba_kernel_launches",
     "pba_build_texels_scratch_bytes", "pba_build_texels", "pba_plan_chunks", "pba_linearize",
     "pba_plan_assembly", "pba_assemble", "pba_sum_totals", "pba_solve_work_bytes",
-    "pba_solve_dense", "pba_pcg_work_bytes", "pba_solve_pcg", "pba_apply_step",
+    "pba_solve_dense", "pba_solve_dense_ex", "pba_pcg_work_bytes", "pba_solve_pcg",
+    "pba_solve_pcg_ex", "pba_apply_step",
     "pba_overlap_counts", "pba_normals_scratch_bytes",
     "pba_estimate_normals", "pba_downscale_cues", "pba_decode_raster", "pba_atan2_batch",
     "pba_diag_section_cycles",
@@ -99,7 +101,11 @@ _SIGNATURES = {
     "pba_sum_totals": (ctypes.c_int, [_vp, _i32, _vp, _vp]),
     "pba_solve_work_bytes": (_sz, [_i32]),
     "pba_solve_dense": (ctypes.c_int, [_vp, _vp, _i32, _dbl, _vp, _vp, _vp, _vp, _vp]),
+    "pba_solve_dense_ex": (ctypes.c_int, [_vp, _vp, _i32, _dbl, _vp, _vp, _vp, _i32, _vp, _vp,
+                                          _vp]),
     "pba_pcg_work_bytes": (_sz, [_i32]),
+    "pba_solve_pcg_ex": (ctypes.c_int, [_vp, _vp, _i32, _dbl, _vp, _vp, _vp, _i32, _dbl, _vp,
+                                        _vp, _vp, _vp, _vp]),
     "pba_solve_pcg": (ctypes.c_int, [_vp, _vp, _i32, _dbl, _vp, _vp, _i32, _dbl, _vp, _vp, _vp,
                                      _vp, _vp]),
     "pba_apply_step": (ctypes.c_int, [_vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp]),
