@@ -279,10 +279,24 @@ def compute_roofline(counts, lin_ms):
         return None
     valid = statistics.mean(counts)
     achieved = valid * FLOPS_PER_VALID_PAIR / (lin_ms * 1e-3) / 1e12
-    return {"bound": "fp64", "unit": "TFLOP/s", "achieved": achieved,
-            "peak": FP64_PEAK_TFLOPS, "peak_kind": "measured DFMA (tools/micro/dmma.cu)",
-            "frac": achieved / FP64_PEAK_TFLOPS, "valid_pairs_per_launch": valid,
-            "flops_per_valid_pair": FLOPS_PER_VALID_PAIR}
+    out = {"bound": "fp64", "unit": "TFLOP/s", "achieved": achieved,
+           "kind": "algorithmic: F_alg (the reference formulation's flops per valid pixel-pair) "
+                   "x valid pixel-pairs / K1 time; the q-basis kernel executes fewer flops, so "
+                   "this is not an executed rate",
+           "peak": FP64_PEAK_TFLOPS, "peak_kind": "measured DFMA (tools/micro/dmma.cu)",
+           "frac": achieved / FP64_PEAK_TFLOPS, "valid_pairs_per_launch": valid,
+           "flops_per_valid_pair": FLOPS_PER_VALID_PAIR}
+    # the executed fp64 utilisation of the same kernel, from the committed ncu capture
+    p = ROOT / "profiles" / "linearize_traffic.json"
+    try:
+        d = json.loads(p.read_text())
+        if d.get("fp64_pipe_active_pct") is not None:
+            out["ncu_fp64_pipe_active_pct"] = d["fp64_pipe_active_pct"]
+            out["ncu_issue_active_pct"] = d.get("issue_active_pct")
+            out["ncu_source"] = d.get("source")
+    except Exception:
+        pass
+    return out
 
 
 def ncu_traffic(name):
