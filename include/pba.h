@@ -188,6 +188,22 @@ int pba_assemble(const double* records, int32_t n_pairs, int32_t n_free, const i
                  const int32_t* diag_items, int32_t n_off, const int32_t* off_ptr,
                  const int32_t* off_rc, const int32_t* off_items, double* H, double* b,
                  double* totals, void* stream);
+/* The same sums into the block-sparse normal matrix (north_star: "into the
+ * block-sparse H/b"; what DeviceLevel uses): Hb (device, n_blocks x 36) holds
+ * the 6x6 blocks in the order of the block-row CSR of the damped system's
+ * non-zero blocks (row_ptr / cols: the diagonal and both orientations of
+ * every off-diagonal block, columns ascending), block e at Hb[36 e + 6 k + l].
+ * diag_blk[s] (n_free) and off_blk[2 o], off_blk[2 o + 1] (2 n_off) are the
+ * CSR positions of slot s's diagonal block and of the (row, col) / (col, row)
+ * blocks of off-diagonal target o (off_rc order of pba_plan_assembly).
+ * Every block is written (no clearing pass); per entry the sums run in the
+ * same edge order as pba_assemble, so Hb equals the dense H's blocks bit for
+ * bit (solver.py:428-449). */
+int pba_assemble_bsr(const double* records, int32_t n_pairs, int32_t n_free,
+                     const int32_t* diag_ptr, const int32_t* diag_items, int32_t n_off,
+                     const int32_t* off_ptr, const int32_t* off_items, const int32_t* diag_blk,
+                     const int32_t* off_blk, double* Hb, double* b, double* totals,
+                     void* stream);
 /* Cost/count only (cost-only path and the LM acceptance test). */
 int pba_sum_totals(const double* records, int32_t n_pairs, double* totals, void* stream);
 
@@ -216,6 +232,13 @@ int pba_solve_dense(const double* H, const double* b, int32_t dim, double lam,
 int pba_solve_dense_ex(const double* H, const double* b, int32_t dim, double lam,
                        const double* lam_dev, const int32_t* tile_env, void* work, int32_t flags,
                        double* delta, int32_t* status, void* stream);
+/* The same factorisation reading the block-sparse Hb of pba_assemble_bsr
+ * (row_ptr / cols its block-row CSR): the damped envelope tiles are built
+ * straight from the blocks, so no dense H exists. */
+int pba_solve_dense_bsr(const double* Hb, const int32_t* row_ptr, const int32_t* cols,
+                        const double* b, int32_t dim, double lam, const double* lam_dev,
+                        const int32_t* tile_env, void* work, int32_t flags, double* delta,
+                        int32_t* status, void* stream);
 
 /* ---- the same system by block-Jacobi PCG (App. C c3: "LM with block-Jacobi
  * PCG"); replaces np.linalg.solve at solver.py:510-512 by an iterative solve.
@@ -239,6 +262,12 @@ int pba_solve_pcg_ex(const double* H, const double* b, int32_t n_free, double la
                      const double* lam_dev, const int32_t* row_ptr, const int32_t* cols,
                      int32_t max_iter, double tol, void* work, double* delta, int32_t* status,
                      double* info, void* stream);
+/* PCG on the block-sparse Hb (its CSR is the mat-vec's row_ptr / cols;
+ * diag_blk[s] = CSR position of the diagonal block of block row s). */
+int pba_solve_pcg_bsr(const double* Hb, const double* b, int32_t n_free, double lam,
+                      const double* lam_dev, const int32_t* row_ptr, const int32_t* cols,
+                      const int32_t* diag_blk, int32_t max_iter, double tol, void* work,
+                      double* delta, int32_t* status, double* info, void* stream);
 
 /* ---- pose update: _LevelProblem.apply_step (solver.py:451-460) --------
  * poses_out[k] = poses_in[k] * exp(delta[slot_k]) for every non-gauge pose

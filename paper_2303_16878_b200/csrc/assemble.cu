@@ -77,6 +77,60 @@ __global__ void assemble_kernel(const double* __restrict__ rec, int n_free,
   H[PBA_DCHECK_INDEX((6 * c + l) * dim + 6 * r + k, dim * dim)] = acc;
 }
 
+// The same sums into the block-sparse (BSR) normal matrix: block-row CSR of
+// 6x6 blocks (the diagonal and both orientations of every off-diagonal
+// block, full symmetric storage), Hb[blk * 36 + 6 k + l].  diag_blk[s] /
+// off_blk[2 o], off_blk[2 o + 1] are the CSR positions of the diagonal block
+// of slot s and of the (r, c) / (c, r) blocks of off-diagonal target o.
+// Entry by entry the sums run in the same edge order as assemble_kernel,
+// so Hb holds exactly the dense H's non-zero blocks.
+__global__ void assemble_bsr_kernel(const double* __restrict__ rec, int n_free,
+                                    const int32_t* __restrict__ diag_ptr,
+                                    const int32_t* __restrict__ diag_items, int n_off,
+                                    const int32_t* __restrict__ off_ptr,
+                                    const int32_t* __restrict__ off_items,
+                                    const int32_t* __restrict__ diag_blk,
+                                    const int32_t* __restrict__ off_blk, double* __restrict__ Hb,
+                                    double* __restrict__ b) {
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long n_diag = 42L * n_free;
+  if (t < n_diag) {
+    const int s = (int)(t / 42), e = (int)(t - 42L * s);
+    const int i0 = diag_ptr[s], i1 = diag_ptr[s + 1];
+    double acc = 0.0;
+    if (e < 36) {
+      const int k = e / 6, l = e - 6 * (e / 6);
+      for (int it = i0; it < i1; ++it) {
+        const int item = diag_items[it];
+        const double* r = rec + (long)(item >> 1) * kRec;
+        acc += upper_get(r + ((item & 1) ? PBA_REC_HJJ : PBA_REC_HII), k, l);
+      }
+      Hb[(long)diag_blk[s] * 36 + 6 * k + l] = acc;
+    } else {
+      const int k = e - 36;
+      for (int it = i0; it < i1; ++it) {
+        const int item = diag_items[it];
+        const double* r = rec + (long)(item >> 1) * kRec;
+        acc += r[((item & 1) ? PBA_REC_BJ : PBA_REC_BI) + k];
+      }
+      b[6L * s + k] = acc;
+    }
+    return;
+  }
+  const long u = t - n_diag;
+  if (u >= 36L * n_off) return;
+  const int o = (int)(u / 36), e = (int)(u - 36L * o);
+  const int k = e / 6, l = e - 6 * (e / 6);
+  double acc = 0.0;
+  for (int it = off_ptr[o]; it < off_ptr[o + 1]; ++it) {
+    const int item = off_items[it];
+    const double* hij = rec + (long)(item >> 1) * kRec + PBA_REC_HIJ;
+    acc += (item & 1) ? hij[6 * l + k] : hij[6 * k + l];
+  }
+  Hb[(long)off_blk[2 * o] * 36 + 6 * k + l] = acc;      // block (r, c)
+  Hb[(long)off_blk[2 * o + 1] * 36 + 6 * l + k] = acc;  // block (c, r) = (r, c)^T
+}
+
 // cost and count summed over pairs: each thread a contiguous edge range in
 // order, then a fixed tree — deterministic for a given pair count.
 __global__ void totals_kernel(const double* __restrict__ rec, int n_pairs,
@@ -197,6 +251,29 @@ extern "C" int pba_sum_totals(const double* records, int32_t n_pairs, double* to
                               void* stream) {
   PBA_ARG_CHECK(totals != nullptr && n_pairs >= 0, "bad arguments");
   totals_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(records, n_pairs, totals);
+  PBA_LAUNCH_CHECK();
+  return PBA_OK;
+}
+
+extern "C" int pba_assemble_bsr(const double* records, int32_t n_pairs, int32_t n_free,
+                                const int32_t* diag_ptr, const int32_t* diag_items, int32_t n_off,
+                                const int32_t* off_ptr, const int32_t* off_items,
+                                const int32_t* diag_blk, const int32_t* off_blk, double* Hb,
+                                double* b, double* totals, void* stream) {
+  PBA_ARG_CHECK(n_free >= 0 && n_off >= 0 && n_pairs >= 0, "bad sizes");
+  PBA_ARG_CHECK(totals != nullptr, "NULL totals");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (n_free > 0) {
+    PBA_ARG_CHECK(Hb && b && diag_ptr && diag_blk && (n_off == 0 || (off_ptr && off_items &&
+                                                                     off_blk)),
+                  "NULL buffer");
+    const long threads = 42L * n_free + 36L * n_off;  // every block written: no memset
+    assemble_bsr_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
+        records, n_free, diag_ptr, diag_items, n_off, off_ptr, off_items, diag_blk, off_blk, Hb,
+        b);
+    PBA_LAUNCH_CHECK();
+  }
+  totals_kernel<<<1, 256, 0, st>>>(records, n_pairs, totals);
   PBA_LAUNCH_CHECK();
   return PBA_OK;
 }

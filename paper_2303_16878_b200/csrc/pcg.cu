@@ -140,7 +140,10 @@ __device__ bool spd_inverse6(const double* a, double* inv) {
 // Part of (H x)_row over every kSplit-th non-zero block of the row, starting
 // at block `sp`; the kSplit lanes of a row are adjacent and are combined by
 // a fixed butterfly in matvec_pass.
-__device__ __forceinline__ double row_part(const double* __restrict__ H, long dim,
+// H is either the dense matrix (bsr false: row-major dim x dim) or the
+// block-sparse one (bsr true: 6x6 blocks in the order of the block-row CSR
+// row_ptr / cols, Hb[e * 36 + 6 k + l], pba_assemble_bsr).
+__device__ __forceinline__ double row_part(const double* __restrict__ H, long dim, bool bsr,
                                            const int32_t* __restrict__ row_ptr,
                                            const int32_t* __restrict__ cols, int br, int k,
                                            int sp, const double* v) {
@@ -150,7 +153,7 @@ __device__ __forceinline__ double row_part(const double* __restrict__ H, long di
 #pragma unroll 2
   for (int e = row_ptr[br] + sp; e < e1; e += kSplit) {
     const int c = PBA_DCHECK_INDEX(__ldg(cols + e), dim / 6);
-    const double* hb = h + 6L * c;
+    const double* hb = bsr ? H + 36L * e + 6 * k : h + 6L * c;
     const double* vb = v + 6L * c;
 #pragma unroll
     for (int l = 0; l < 6; ++l) acc = fma(__ldg(hb + l), __ldcg(vb + l), acc);
@@ -160,19 +163,28 @@ __device__ __forceinline__ double row_part(const double* __restrict__ H, long di
 
 // mv[lr * 6 + k] = ((H + lam diag H) v)_row for the pass's block rows; all
 // threads call it (the butterfly is warp-wide), a __syncthreads follows.
-__device__ __forceinline__ void matvec_pass(const double* __restrict__ H, long dim, double lam,
+__device__ __forceinline__ double hdiag(const double* __restrict__ H, long dim,
+                                        const int32_t* __restrict__ diag_blk, int br, int i,
+                                        int j) {
+  return diag_blk ? __ldg(H + 36L * diag_blk[br] + 6 * i + j)
+                  : __ldg(H + (6L * br + i) * dim + 6L * br + j);
+}
+
+__device__ __forceinline__ void matvec_pass(const double* __restrict__ H, long dim,
+                                            const int32_t* __restrict__ diag_blk, double lam,
                                             const int32_t* __restrict__ row_ptr,
                                             const int32_t* __restrict__ cols, int base, int br1,
                                             const double* v, double* mv) {
   const int t = threadIdx.x;
   const int lr = t / (6 * kSplit), k = (t / kSplit) % 6, sp = t % kSplit;
   const int br = base + lr;
-  double acc = br < br1 ? row_part(H, dim, row_ptr, cols, br, k, sp, v) : 0.0;
+  double acc = br < br1 ? row_part(H, dim, diag_blk != nullptr, row_ptr, cols, br, k, sp, v)
+                        : 0.0;
 #pragma unroll
   for (int o = 1; o < kSplit; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if (sp == 0 && br < br1) {
     const long row = 6L * br + k;
-    mv[lr * 6 + k] = fma(lam * __ldg(H + row * dim + row), __ldcg(v + row), acc);
+    mv[lr * 6 + k] = fma(lam * hdiag(H, dim, diag_blk, br, k, k), __ldcg(v + row), acc);
   }
 }
 
@@ -204,6 +216,7 @@ __global__ void __launch_bounds__(kPcgThreads)
     pcg_kernel(const double* __restrict__ H, const double* __restrict__ b, int n_free,
                double lam_arg, const double* __restrict__ lam_dev,
                const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ cols,
+               const int32_t* __restrict__ diag_blk,
                int max_iter, double tol, PcgWork w, double* __restrict__ delta,
                int32_t* __restrict__ status, double* __restrict__ info) {
   cg::grid_group grid = cg::this_grid();
@@ -235,7 +248,7 @@ __global__ void __launch_bounds__(kPcgThreads)
       double a[36];
       for (int i = 0; i < 6; ++i)
         for (int j = 0; j < 6; ++j) {
-          const double h = H[(6L * br + i) * dim + 6L * br + j];
+          const double h = hdiag(H, dim, diag_blk, br, i, j);
           a[6 * i + j] = (i == j) ? h + lam * h : h;
         }
       if (!spd_inverse6(a, w.minv + 36L * br)) bad = 1;
@@ -291,7 +304,7 @@ __global__ void __launch_bounds__(kPcgThreads)
   for (int ps = 0; ps < kMaxPasses; ++ps) {
     if (ps < passes) {
       const int base = br0 + ps * kPcgRows;
-      matvec_pass(H, dim, lam, row_ptr, cols, base, br1, w.z, mv);
+      matvec_pass(H, dim, diag_blk, lam, row_ptr, cols, base, br1, w.z, mv);
       __syncthreads();
       if (vec && base + lr < br1) {
         qv[ps] = mv[threadIdx.x];
@@ -360,7 +373,7 @@ __global__ void __launch_bounds__(kPcgThreads)
     for (int ps = 0; ps < kMaxPasses; ++ps) {
       if (ps < passes) {
         const int base = br0 + ps * kPcgRows;
-        matvec_pass(H, dim, lam, row_ptr, cols, base, br1, w.z, mv);
+        matvec_pass(H, dim, diag_blk, lam, row_ptr, cols, base, br1, w.z, mv);
         __syncthreads();
         if (vec && base + lr < br1) {
           pv[ps] = fma(beta, pv[ps], zv[ps]);
@@ -413,10 +426,11 @@ extern "C" size_t pba_pcg_work_bytes(int32_t n_free) {
          5 * align_up(dim * sizeof(double), 256) + align_up(4 * max_grid * sizeof(double), 256);
 }
 
-extern "C" int pba_solve_pcg_ex(const double* H, const double* b, int32_t n_free, double lam,
-                                const double* lam_dev, const int32_t* row_ptr,
-                                const int32_t* cols, int32_t max_iter, double tol, void* work,
-                                double* delta, int32_t* status, double* info, void* stream) {
+namespace {
+int solve_pcg_impl(const double* H, const double* b, int32_t n_free, double lam,
+                   const double* lam_dev, const int32_t* row_ptr, const int32_t* cols,
+                   const int32_t* diag_blk, int32_t max_iter, double tol, void* work,
+                   double* delta, int32_t* status, double* info, void* stream) {
   PBA_ARG_CHECK(n_free > 0, "n_free must be positive");
   PBA_ARG_CHECK(max_iter >= 1 && tol >= 0.0, "bad iteration limit or tolerance");
   PBA_ARG_CHECK(H && b && row_ptr && cols && work && delta && status && info, "NULL buffer");
@@ -434,14 +448,33 @@ extern "C" int pba_solve_pcg_ex(const double* H, const double* b, int32_t n_free
   PBA_ARG_CHECK(grid <= 148 * 16, "cooperative grid larger than the work buffer allows");
   PcgWork w = carve(work, n_free, grid);
   PBA_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int32_t), st));
-  void* args[] = {(void*)&H,       (void*)&b,    (void*)&n_free,   (void*)&lam,
-                  (void*)&lam_dev, (void*)&row_ptr, (void*)&cols, (void*)&max_iter,
-                  (void*)&tol,     (void*)&w,    (void*)&delta,    (void*)&status,
-                  (void*)&info};
+  void* args[] = {(void*)&H,       (void*)&b,       (void*)&n_free, (void*)&lam,
+                  (void*)&lam_dev, (void*)&row_ptr, (void*)&cols,   (void*)&diag_blk,
+                  (void*)&max_iter, (void*)&tol,    (void*)&w,      (void*)&delta,
+                  (void*)&status,  (void*)&info};
   PBA_CUDA_TRY(cudaLaunchCooperativeKernel((void*)pcg_kernel, dim3(grid), dim3(kPcgThreads), args,
                                            0, st));
   PBA_LAUNCH_CHECK();
   return PBA_OK;
+}
+}  // namespace
+
+extern "C" int pba_solve_pcg_ex(const double* H, const double* b, int32_t n_free, double lam,
+                                const double* lam_dev, const int32_t* row_ptr,
+                                const int32_t* cols, int32_t max_iter, double tol, void* work,
+                                double* delta, int32_t* status, double* info, void* stream) {
+  return solve_pcg_impl(H, b, n_free, lam, lam_dev, row_ptr, cols, nullptr, max_iter, tol, work,
+                        delta, status, info, stream);
+}
+
+extern "C" int pba_solve_pcg_bsr(const double* Hb, const double* b, int32_t n_free, double lam,
+                                 const double* lam_dev, const int32_t* row_ptr,
+                                 const int32_t* cols, const int32_t* diag_blk, int32_t max_iter,
+                                 double tol, void* work, double* delta, int32_t* status,
+                                 double* info, void* stream) {
+  PBA_ARG_CHECK(diag_blk != nullptr, "NULL diag_blk");
+  return solve_pcg_impl(Hb, b, n_free, lam, lam_dev, row_ptr, cols, diag_blk, max_iter, tol,
+                        work, delta, status, info, stream);
 }
 
 extern "C" int pba_solve_pcg(const double* H, const double* b, int32_t n_free, double lam,

@@ -71,7 +71,29 @@ SolveWork carve(void* work, int dim) {
   return w;
 }
 
-__global__ void damp_copy_kernel(const double* __restrict__ H, int dim, double lam_arg,
+// H entry (r, c): dense row-major, or from the block-sparse matrix of
+// pba_assemble_bsr (6x6 blocks in block-row CSR order; a block absent from
+// the row's column list is zero).
+struct HSource {
+  const double* H;
+  const int32_t* row_ptr;  // nullptr: dense
+  const int32_t* cols;
+  int dim;
+  __device__ __forceinline__ double at(int r, int c) const {
+    if (!row_ptr) return H[(long)r * dim + c];
+    const int br = r / 6, bc = c / 6;
+    int lo = row_ptr[br], hi = row_ptr[br + 1] - 1;
+    while (lo <= hi) {  // columns ascending per block row
+      const int mid = (lo + hi) >> 1;
+      const int cm = cols[mid];
+      if (cm == bc) return H[36L * mid + 6 * (r - 6 * br) + (c - 6 * bc)];
+      if (cm < bc) lo = mid + 1; else hi = mid - 1;
+    }
+    return 0.0;
+  }
+};
+
+__global__ void damp_copy_kernel(HSource H, int dim, double lam_arg,
                                  const double* __restrict__ lam_dev,
                                  const int32_t* __restrict__ env, double* __restrict__ A) {
   const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -79,7 +101,7 @@ __global__ void damp_copy_kernel(const double* __restrict__ H, int dim, double l
   const double lam = lam_dev ? *lam_dev : lam_arg;  // device lambda: graph-replayable step
   const int i = (int)(t / dim), j = (int)(t - (long)i * dim);
   if (j > i || j / NB < env[i / NB]) return;
-  const double h = H[t];
+  const double h = H.at(i, j);
   A[t] = (i == j) ? h + lam * h : h;  // h + lam * np.diag(np.diag(h))
 }
 
@@ -514,7 +536,7 @@ __global__ void __launch_bounds__(256) syrk_kernel(double* __restrict__ A, int d
 
 // Ap (D x D, lower) = P (H + lam diag H) P^T on the structural tiles listed in
 // tiles (pairs of new tile indices, row >= col); padding rows are identity.
-__global__ void damp_copy_perm_kernel(const double* __restrict__ H, int dim, double lam_arg,
+__global__ void damp_copy_perm_kernel(HSource H, int dim, double lam_arg,
                                       const double* __restrict__ lam_dev, int D,
                                       const int32_t* __restrict__ tiles,
                                       const int32_t* __restrict__ new_to_old,
@@ -530,7 +552,7 @@ __global__ void damp_copy_perm_kernel(const double* __restrict__ H, int dim, dou
       v = (ti == tj && r == c) ? 1.0 : 0.0;
     } else {
       const int hi = max(gr, gc), lo = min(gr, gc);
-      const double h = H[(long)hi * dim + lo];
+      const double h = H.at(hi, lo);
       v = (gr == gc) ? h + lam * h : h;
     }
     Ap[(long)(ti * NB + r) * D + tj * NB + c] = v;
@@ -748,7 +770,7 @@ int set_solver_smem_attributes() {
   return PBA_OK;
 }
 
-int solve_dissected(const double* H, const double* b, int dim, double lam, const double* lam_dev,
+int solve_dissected(HSource H, const double* b, int dim, double lam, const double* lam_dev,
                     bool reuse, const std::vector<int32_t>& env, const std::vector<int32_t>& last,
                     const SolveWork& w, double* delta, int32_t* status, cudaStream_t st) {
   const int T = (int)env.size(), D = T * NB;
@@ -923,12 +945,13 @@ extern "C" size_t pba_solve_work_bytes(int32_t dim) {
          align_up(T * T * sizeof(int32_t), 256) + align_up(2 * T * sizeof(int32_t), 256);
 }
 
-extern "C" int pba_solve_dense_ex(const double* H, const double* b, int32_t dim, double lam,
-                                  const double* lam_dev, const int32_t* tile_env, void* work,
-                                  int32_t flags, double* delta, int32_t* status, void* stream) {
+namespace {
+int solve_dense_impl(HSource H, const double* b, int32_t dim, double lam, const double* lam_dev,
+                     const int32_t* tile_env, void* work, int32_t flags, double* delta,
+                     int32_t* status, void* stream) {
   const bool reuse = (flags & PBA_SOLVE_REUSE_PLAN) != 0;
   PBA_ARG_CHECK(dim > 0, "dim must be positive");
-  PBA_ARG_CHECK(H && b && work && delta && status, "NULL buffer");
+  PBA_ARG_CHECK(H.H && b && work && delta && status, "NULL buffer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   SolveWork w = carve(work, dim);
   const int T = (dim + NB - 1) / NB;
@@ -1002,6 +1025,24 @@ extern "C" int pba_solve_dense_ex(const double* H, const double* b, int32_t dim,
                                       status);
   PBA_LAUNCH_CHECK();
   return PBA_OK;
+}
+
+}  // namespace
+
+extern "C" int pba_solve_dense_ex(const double* H, const double* b, int32_t dim, double lam,
+                                  const double* lam_dev, const int32_t* tile_env, void* work,
+                                  int32_t flags, double* delta, int32_t* status, void* stream) {
+  return solve_dense_impl(HSource{H, nullptr, nullptr, dim}, b, dim, lam, lam_dev, tile_env,
+                          work, flags, delta, status, stream);
+}
+
+extern "C" int pba_solve_dense_bsr(const double* Hb, const int32_t* row_ptr, const int32_t* cols,
+                                   const double* b, int32_t dim, double lam,
+                                   const double* lam_dev, const int32_t* tile_env, void* work,
+                                   int32_t flags, double* delta, int32_t* status, void* stream) {
+  PBA_ARG_CHECK(row_ptr && cols && dim % 6 == 0, "block-sparse H needs its CSR and dim = 6 n");
+  return solve_dense_impl(HSource{Hb, row_ptr, cols, dim}, b, dim, lam, lam_dev, tile_env, work,
+                          flags, delta, status, stream);
 }
 
 extern "C" int pba_solve_dense(const double* H, const double* b, int32_t dim, double lam,

@@ -111,6 +111,23 @@ def order_chunks(chunk_tab, n_chunks, chunk_pixels, src_of_pair, dst_of_pair,
     return np.ascontiguousarray(tab[perm].reshape(-1), dtype=np.int32)
 
 
+def bsr_positions(row_ptr, cols, off_rc):
+    """CSR positions of every diagonal block (s, s) and of both orientations
+    (r, c) / (c, r) of every off-diagonal assembly target (off_rc pairs)."""
+    n = len(row_ptr) - 1
+
+    def pos(r, c):
+        lo, hi = int(row_ptr[r]), int(row_ptr[r + 1])
+        k = lo + int(np.searchsorted(cols[lo:hi], c))
+        assert k < hi and cols[k] == c
+        return k
+
+    diag = np.array([pos(s, s) for s in range(n)], dtype=np.int32)
+    rc = np.asarray(off_rc, dtype=np.int64).reshape(-1, 2)
+    off = np.array([[pos(r, c), pos(c, r)] for r, c in rc], dtype=np.int32).reshape(-1)
+    return diag, off
+
+
 def tile_envelope(slot_of_pose, pose_i, pose_j, dim, tile=64) -> np.ndarray:
     """First possibly non-zero 64-wide tile column of every tile row of the
     damped normal matrix: the envelope of its block sparsity (diagonal
@@ -359,7 +376,16 @@ class DeviceLevel:
         t = lambda a: torch.from_numpy(a).to(dev)
         self.plan = [t(diag_ptr), t(diag_items), t(off_ptr), t(off_rc), t(off_items)]
         d = max(1, self.dim)
-        self.H = [torch.zeros((d, d), dtype=torch.float64, device=dev) for _ in range(2)]
+        # block-sparse H (north_star: "into the block-sparse H/b"): the 6x6
+        # blocks of the block-row CSR of the damped system, diagonal + both
+        # orientations of every off-diagonal block (pba_assemble_bsr)
+        row_ptr, cols = block_rows(slot, self.pose_i, self.pose_j)
+        self.n_blocks = int(row_ptr[-1])
+        diag_blk, off_blk = bsr_positions(row_ptr, cols, off_rc[: 2 * self.n_off])
+        self.bsr = [t(row_ptr), t(cols), t(diag_blk), t(off_blk if len(off_blk) else
+                                                          np.zeros(2, np.int32))]
+        self.Hb = [torch.zeros((max(1, self.n_blocks), 36), dtype=torch.float64, device=dev)
+                   for _ in range(2)]
         self.b = [torch.zeros(d, dtype=torch.float64, device=dev) for _ in range(2)]
         self.totals = [torch.zeros(2, dtype=torch.float64, device=dev) for _ in range(2)]
         # getattr: a reference photoba SolverConfig (no B200 fields) is accepted as-is
@@ -370,8 +396,6 @@ class DeviceLevel:
         self.delta = torch.zeros(d, dtype=torch.float64, device=dev)
         self.tile_env = tile_envelope(slot, self.pose_i, self.pose_j, self.dim)
         if self.pcg:
-            row_ptr, cols = block_rows(slot, self.pose_i, self.pose_j)
-            self.pcg_rows = [t(row_ptr), t(cols)]
             self.pcg_work = torch.empty(max(8, int(lib.pba_pcg_work_bytes(self.n_free))),
                                         dtype=torch.uint8, device=dev)
             self.pcg_info = torch.zeros(3, dtype=torch.float64, device=dev)
@@ -406,11 +430,23 @@ class DeviceLevel:
 
     def assemble(self, records: torch.Tensor, which: int) -> None:
         dp, di, op, orc, oi = self.plan
-        N.check(self.lib.pba_assemble(
+        _, _, dblk, oblk = self.bsr
+        N.check(self.lib.pba_assemble_bsr(
             records.data_ptr(), self.n_pairs_total, self.n_free, dp.data_ptr(), di.data_ptr(),
-            self.n_off, op.data_ptr(), orc.data_ptr(), oi.data_ptr(), self.H[which].data_ptr(),
-            self.b[which].data_ptr(), self.totals[which].data_ptr(), _stream_ptr(self.device)),
-            "pba_assemble")
+            self.n_off, op.data_ptr(), oi.data_ptr(), dblk.data_ptr(), oblk.data_ptr(),
+            self.Hb[which].data_ptr(), self.b[which].data_ptr(), self.totals[which].data_ptr(),
+            _stream_ptr(self.device)), "pba_assemble_bsr")
+
+    def dense_H(self, which: int) -> torch.Tensor:
+        """The assembled normal matrix of buffer `which` as a dense (dim, dim)
+        tensor (tests and diagnostics; the solver never forms it)."""
+        rp, cols, _, _ = (x.cpu().numpy() for x in self.bsr)
+        rows = np.repeat(np.arange(self.n_free), np.diff(rp))
+        blocks = self.Hb[which][: self.n_blocks].reshape(-1, 6, 6)
+        H = torch.zeros((self.n_free, 6, self.n_free, 6), dtype=torch.float64, device=self.device)
+        H[torch.from_numpy(rows).to(self.device), :, torch.from_numpy(cols.astype(np.int64))
+          .to(self.device), :] = blocks
+        return H.reshape(self.dim, self.dim)
 
     def sum_totals(self, records: torch.Tensor, out: torch.Tensor) -> None:
         N.check(self.lib.pba_sum_totals(records.data_ptr(), records.shape[0], out.data_ptr(),
@@ -425,23 +461,24 @@ class DeviceLevel:
             e0.record(torch.cuda.current_stream(self.device))
         lam_v = 0.0 if lam is None else float(lam)
         lam_p = self._lam_dev.data_ptr() if lam is None else None
+        rp, cols, dblk, _ = self.bsr
         if self.pcg:
-            rp, cols = self.pcg_rows
-            N.check(self.lib.pba_solve_pcg_ex(self.H[which].data_ptr(), self.b[which].data_ptr(),
-                                              self.n_free, lam_v, lam_p, rp.data_ptr(),
-                                              cols.data_ptr(),
-                                              int(getattr(self.cfg, "pcg_max_iterations", 2000)),
-                                              float(getattr(self.cfg, "pcg_tolerance", 1e-12)),
-                                              self.pcg_work.data_ptr(), self.delta.data_ptr(),
-                                              status_ptr, self.pcg_info.data_ptr(),
-                                              _stream_ptr(self.device)), "pba_solve_pcg_ex")
+            N.check(self.lib.pba_solve_pcg_bsr(self.Hb[which].data_ptr(), self.b[which].data_ptr(),
+                                               self.n_free, lam_v, lam_p, rp.data_ptr(),
+                                               cols.data_ptr(), dblk.data_ptr(),
+                                               int(getattr(self.cfg, "pcg_max_iterations", 2000)),
+                                               float(getattr(self.cfg, "pcg_tolerance", 1e-12)),
+                                               self.pcg_work.data_ptr(), self.delta.data_ptr(),
+                                               status_ptr, self.pcg_info.data_ptr(),
+                                               _stream_ptr(self.device)), "pba_solve_pcg_bsr")
         else:
             flags = N.PBA_SOLVE_REUSE_PLAN if self._plan_ready else 0
-            N.check(self.lib.pba_solve_dense_ex(self.H[which].data_ptr(), self.b[which].data_ptr(),
-                                                self.dim, lam_v, lam_p, self.tile_env.ctypes.data,
-                                                self.work.data_ptr(), flags,
-                                                self.delta.data_ptr(), status_ptr,
-                                                _stream_ptr(self.device)), "pba_solve_dense_ex")
+            N.check(self.lib.pba_solve_dense_bsr(self.Hb[which].data_ptr(), rp.data_ptr(),
+                                                 cols.data_ptr(), self.b[which].data_ptr(),
+                                                 self.dim, lam_v, lam_p, self.tile_env.ctypes.data,
+                                                 self.work.data_ptr(), flags,
+                                                 self.delta.data_ptr(), status_ptr,
+                                                 _stream_ptr(self.device)), "pba_solve_dense_bsr")
             self._plan_ready = True  # the tile tables are now in self.work
         if ev is not None:
             e1 = torch.cuda.Event(enable_timing=True)

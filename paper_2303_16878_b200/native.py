@@ -35,9 +35,10 @@ EXPORTED = (
     "pba_build_checked",
     "pba_kernel_launches",
     "pba_build_texels_scratch_bytes", "pba_build_texels", "pba_plan_chunks", "pba_linearize",
-    "pba_plan_assembly", "pba_assemble", "pba_sum_totals", "pba_solve_work_bytes",
-    "pba_solve_dense", "pba_solve_dense_ex", "pba_pcg_work_bytes", "pba_solve_pcg",
-    "pba_solve_pcg_ex", "pba_apply_step",
+    "pba_plan_assembly", "pba_assemble", "pba_assemble_bsr", "pba_sum_totals",
+    "pba_solve_work_bytes", "pba_solve_dense", "pba_solve_dense_ex", "pba_solve_dense_bsr",
+    "pba_pcg_work_bytes", "pba_solve_pcg", "pba_solve_pcg_ex", "pba_solve_pcg_bsr",
+    "pba_apply_step",
     "pba_overlap_counts", "pba_normals_scratch_bytes",
     "pba_estimate_normals", "pba_downscale_cues", "pba_decode_raster", "pba_atan2_batch",
     "pba_diag_section_cycles",
@@ -98,12 +99,18 @@ _SIGNATURES = {
                                          ctypes.POINTER(_i32)]),
     "pba_assemble": (ctypes.c_int, [_vp, _i32, _i32, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp,
                                     _vp, _vp]),
+    "pba_assemble_bsr": (ctypes.c_int, [_vp, _i32, _i32, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp,
+                                        _vp, _vp, _vp]),
     "pba_sum_totals": (ctypes.c_int, [_vp, _i32, _vp, _vp]),
     "pba_solve_work_bytes": (_sz, [_i32]),
     "pba_solve_dense": (ctypes.c_int, [_vp, _vp, _i32, _dbl, _vp, _vp, _vp, _vp, _vp]),
     "pba_solve_dense_ex": (ctypes.c_int, [_vp, _vp, _i32, _dbl, _vp, _vp, _vp, _i32, _vp, _vp,
                                           _vp]),
+    "pba_solve_dense_bsr": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i32, _dbl, _vp, _vp, _vp, _i32,
+                                           _vp, _vp, _vp]),
     "pba_pcg_work_bytes": (_sz, [_i32]),
+    "pba_solve_pcg_bsr": (ctypes.c_int, [_vp, _vp, _i32, _dbl, _vp, _vp, _vp, _vp, _i32, _dbl,
+                                         _vp, _vp, _vp, _vp, _vp]),
     "pba_solve_pcg_ex": (ctypes.c_int, [_vp, _vp, _i32, _dbl, _vp, _vp, _vp, _i32, _dbl, _vp,
                                         _vp, _vp, _vp, _vp]),
     "pba_solve_pcg": (ctypes.c_int, [_vp, _vp, _i32, _dbl, _vp, _vp, _i32, _dbl, _vp, _vp, _vp,

@@ -57,7 +57,7 @@ def test_reductions_bit_identical_under_repetition():
             lv.set_poses(rows, gens)
             c0, n0 = lv.evaluate_current()
             ok_s, ok_u, c1, n1 = lv.try_step(1e-3)
-            out = (lv.records.cpu().numpy().copy(), lv.H[0].cpu().numpy().copy(),
+            out = (lv.records.cpu().numpy().copy(), lv.Hb[0].cpu().numpy().copy(),
                    lv.delta.cpu().numpy().copy(), lv.poses[1].cpu().numpy().copy(), c0, c1)
             assert ok_s and ok_u
             if first is None:

@@ -217,7 +217,7 @@ def test_assembled_normal_equations_match_oracle(gauge, capsys):
         lv = DeviceLevel([prob], level, P.SolverConfig(), _store())
         lv.set_poses(rows, gens)
         cost, count = lv.evaluate_current()
-        H = lv.H[lv.cur].cpu().numpy()
+        H = lv.dense_H(lv.cur).cpu().numpy()  # from the block-sparse Hb the solver reads
         b = lv.b[lv.cur].cpu().numpy()
         dev_recs = lv.records.cpu().numpy()
         lp = O.OracleLevel([prob], level, P.SolverConfig())
