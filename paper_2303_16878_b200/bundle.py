@@ -111,7 +111,8 @@ class BAProblem:
     gauge_index: int = 0
 
     def extrinsics_of(self, sensor_id: str) -> SensorExtrinsics:
-        return self.extrinsics.get(sensor_id, SensorExtrinsics.identity())
+        ext = self.extrinsics.get(sensor_id)
+        return ext if ext is not None else SensorExtrinsics.identity()
 
 
 @dataclass

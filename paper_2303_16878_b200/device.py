@@ -113,19 +113,25 @@ def order_chunks(chunk_tab, n_chunks, chunk_pixels, src_of_pair, dst_of_pair,
 
 def bsr_positions(row_ptr, cols, off_rc):
     """CSR positions of every diagonal block (s, s) and of both orientations
-    (r, c) / (c, r) of every off-diagonal assembly target (off_rc pairs)."""
+    (r, c) / (c, r) of every off-diagonal assembly target (off_rc pairs).
+    The CSR is sorted by (row, column), so one searchsorted on r * n + c."""
     n = len(row_ptr) - 1
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(np.asarray(row_ptr, np.int64)))
+    keys = rows * max(n, 1) + np.asarray(cols, np.int64)
 
     def pos(r, c):
-        lo, hi = int(row_ptr[r]), int(row_ptr[r + 1])
-        k = lo + int(np.searchsorted(cols[lo:hi], c))
-        assert k < hi and cols[k] == c
-        return k
+        want = r * max(n, 1) + c
+        k = np.searchsorted(keys, want)
+        if len(want) and not (np.all(k < len(keys)) and np.array_equal(keys[np.minimum(
+                k, len(keys) - 1)], want)):
+            raise ValueError("assembly target missing from the block CSR")
+        return k.astype(np.int32)
 
-    diag = np.array([pos(s, s) for s in range(n)], dtype=np.int32)
+    s = np.arange(n, dtype=np.int64)
+    diag = pos(s, s)
     rc = np.asarray(off_rc, dtype=np.int64).reshape(-1, 2)
-    off = np.array([[pos(r, c), pos(c, r)] for r, c in rc], dtype=np.int32).reshape(-1)
-    return diag, off
+    off = np.stack([pos(rc[:, 0], rc[:, 1]), pos(rc[:, 1], rc[:, 0])], axis=1).reshape(-1)
+    return diag, off.astype(np.int32)
 
 
 def tile_envelope(slot_of_pose, pose_i, pose_j, dim, tile=64) -> np.ndarray:
@@ -179,8 +185,27 @@ class FrameStore:
             out.append(h.to(self.device, non_blocking=False))
         return tuple(out)
 
-    def frame(self, cue):
-        """(texels, mask, ray table, Camera) of a cue image, uploading on first use."""
+    def prefetch(self, cues) -> None:
+        """Upload every not-yet-resident cue image of a level at once: one
+        texel slab and one mask slab per image size (one allocation each
+        instead of two per frame), then the per-frame texel build."""
+        todo, seen = {}, set()
+        for cue in cues:
+            if id(cue) in self._frames or id(cue) in seen:
+                continue
+            seen.add(id(cue))
+            intr = cue.intrinsics
+            todo.setdefault((int(intr.height), int(intr.width)), []).append(cue)
+        tb = int(self._lib.pba_texel_bytes())
+        for (h, w), group in todo.items():
+            tex = torch.empty((len(group), h * w * tb), dtype=torch.uint8, device=self.device)
+            msk = torch.empty((len(group), h * w), dtype=torch.uint8, device=self.device)
+            for k, cue in enumerate(group):
+                self.frame(cue, tex[k], msk[k])
+
+    def frame(self, cue, texels=None, mask=None):
+        """(texels, mask, ray table, Camera) of a cue image, uploading on first
+        use (into `texels` / `mask` when given, else fresh buffers)."""
         key = id(cue)
         hit = self._frames.get(key)
         if hit is not None:
@@ -191,9 +216,10 @@ class FrameStore:
         inten, depth, normals = self._channels(cue)
         if tuple(inten.shape) != (h, w):
             raise ValueError("intrinsics do not match image size")
-        texels = torch.empty(h * w * int(self._lib.pba_texel_bytes()), dtype=torch.uint8,
-                             device=self.device)
-        mask = torch.empty(h * w, dtype=torch.uint8, device=self.device)
+        if texels is None:
+            texels = torch.empty(h * w * int(self._lib.pba_texel_bytes()), dtype=torch.uint8,
+                                 device=self.device)
+            mask = torch.empty(h * w, dtype=torch.uint8, device=self.device)
         need = int(self._lib.pba_build_texels_scratch_bytes(ctypes.byref(cam)))
         if self._scratch is None or self._scratch.numel() < need:
             self._scratch = torch.empty(need, dtype=torch.uint8, device=self.device)
@@ -217,12 +243,15 @@ def level_contexts(problems, level, cfg):
     for problem in problems:
         nodes = problem.graph.nodes
         index_of = {n.id: k for k, n in enumerate(nodes)}
+        ext_of = {}
         for edge in problem.graph.edges:
             ni, nj = nodes[index_of[edge.i]], nodes[index_of[edge.j]]
             if ni.sensor_id != nj.sensor_id:
                 from .bundle import FusionConfigError
                 raise FusionConfigError("edges must connect frames of one sensor")
-            ext = problem.extrinsics_of(ni.sensor_id)
+            ext = ext_of.get(ni.sensor_id)
+            if ext is None:
+                ext = ext_of[ni.sensor_id] = problem.extrinsics_of(ni.sensor_id)
             tol = cfg.occlusion_depth_tolerance / ni.pyramid.scales[level]
             out.append((index_of[edge.i], index_of[edge.j], ni, nj, ext, tol))
     return out
@@ -275,6 +304,7 @@ class DeviceLevel:
         mine = ctxs[lo:hi]
         self.n_pairs = len(mine)
         # frame / extrinsics tables for this shard
+        store.prefetch([node.pyramid.levels[level] for c in mine for node in (c[2], c[3])])
         frames, frame_slot, ext_rows, ext_slot = [], {}, [], {}
         pairs = (N.Pair * max(1, self.n_pairs))()
         src_cams = (N.Camera * max(1, self.n_pairs))()
@@ -533,7 +563,7 @@ class DeviceLevel:
         cur, cand = self.cur, 1 - self.cur
         if self._graph_enabled():
             g = self._graphs[cur]
-            if g is None and self._plan_ready:
+            if g is None and self._plan_ready and self._graph_pays(cur):
                 g = self._capture_step(cur)
             if g is not None:
                 self._lam_host[0] = lam
@@ -561,6 +591,14 @@ class DeviceLevel:
         self._scal[0:2].copy_(self.totals[cand])
 
     # ---- CUDA-graph step ------------------------------------------------------
+    def _graph_pays(self, cur: int) -> bool:
+        """Capture lazily only where a replay saves a visible share of the
+        step: a problem small enough that host launch work matters
+        (<= 64 M source pixels per linearisation) that has already run two
+        eager steps from this buffer (so an LM level that stops after a few
+        iterations never pays for a capture).  prepare_graphs() forces it."""
+        return self.pixels_shard <= (1 << 26) and self._eager_steps[cur] >= 2
+
     def prepare_graphs(self) -> None:
         """Capture the step graphs of both buffers now (after one eager step),
         so no capture happens inside a timed loop."""
