@@ -305,26 +305,40 @@ class DeviceLevel:
         self.n_pairs = len(mine)
         # frame / extrinsics tables for this shard
         store.prefetch([node.pyramid.levels[level] for c in mine for node in (c[2], c[3])])
-        frames, frame_slot, ext_rows, ext_slot = [], {}, [], {}
-        pairs = (N.Pair * max(1, self.n_pairs))()
-        src_cams = (N.Camera * max(1, self.n_pairs))()
+        frames, frame_slot, ext_rows, ext_slot, ext_of = [], {}, [], {}, {}
+        idx = np.zeros((max(1, self.n_pairs), 5), dtype=np.int32)  # pose_i, pose_j, src, dst, ext
+        tols = np.zeros(max(1, self.n_pairs))
         for k, (pi, pj, ni, nj, ext, tol) in enumerate(mine):
             slots = []
             for node in (ni, nj):
                 cue = node.pyramid.levels[level]
-                if id(cue) not in frame_slot:
+                s_ = frame_slot.get(id(cue))
+                if s_ is None:
                     tex, mask, ray, cam = store.frame(cue)
-                    frame_slot[id(cue)] = len(frames)
+                    s_ = frame_slot[id(cue)] = len(frames)
                     frames.append(N.Frame(tex.data_ptr(), mask.data_ptr(), ray.data_ptr(), cam))
-                slots.append(frame_slot[id(cue)])
-            off = ext.offset
-            ekey = (np.asarray(off.rotation, float).tobytes(), np.asarray(off.translation, float).tobytes())
-            if ekey not in ext_slot:
-                ext_slot[ekey] = len(ext_rows)
-                ext_rows.append(np.concatenate([np.asarray(off.rotation, float).reshape(9),
-                                                np.asarray(off.translation, float).reshape(3)]))
-            pairs[k] = N.Pair(pi, pj, slots[0], slots[1], ext_slot[ekey], 0, float(tol))
-            src_cams[k] = frames[slots[0]].cam
+                slots.append(s_)
+            e_ = ext_of.get(id(ext))
+            if e_ is None:
+                off = ext.offset
+                ekey = (np.asarray(off.rotation, float).tobytes(),
+                        np.asarray(off.translation, float).tobytes())
+                if ekey not in ext_slot:
+                    ext_slot[ekey] = len(ext_rows)
+                    ext_rows.append(np.concatenate([np.asarray(off.rotation, float).reshape(9),
+                                                    np.asarray(off.translation, float).reshape(3)]))
+                e_ = ext_of[id(ext)] = ext_slot[ekey]
+            idx[k] = (pi, pj, slots[0], slots[1], e_)
+            tols[k] = tol
+        # the pba_pair / pba_camera tables built in one go (32 B / 64 B records)
+        pair_rec = np.zeros(max(1, self.n_pairs), dtype=[("i", "<i4", 6), ("tol", "<f8")])
+        pair_rec["i"][:, :5] = idx
+        pair_rec["tol"] = tols
+        pairs = (N.Pair * max(1, self.n_pairs)).from_buffer_copy(pair_rec.tobytes())
+        cam_bytes = np.frombuffer(b"".join(bytes(f.cam) for f in frames) or bytes(64),
+                                  dtype=np.uint8).reshape(-1, ctypes.sizeof(N.Camera))
+        src_cams = (N.Camera * max(1, self.n_pairs)).from_buffer_copy(
+            cam_bytes[idx[:, 2]].tobytes())
         n_chunks = ctypes.c_int64(0)
         N.check(self.lib.pba_plan_chunks(pairs, self.n_pairs, src_cams, stride, self.chunk_pixels,
                                          None, None, ctypes.byref(n_chunks)), "pba_plan_chunks")
@@ -334,11 +348,10 @@ class DeviceLevel:
         N.check(self.lib.pba_plan_chunks(pairs, self.n_pairs, src_cams, stride, self.chunk_pixels,
                                          chunk_tab.ctypes.data, offsets.ctypes.data,
                                          ctypes.byref(n_chunks)), "pba_plan_chunks")
+        frame_pinhole = np.array([int(f.cam.model == N.PBA_PINHOLE) for f in frames] or [0])
         chunk_tab = order_chunks(chunk_tab, self.n_chunks, self.chunk_pixels,
-                                 [pairs[k].src for k in range(self.n_pairs)],
-                                 [pairs[k].dst for k in range(self.n_pairs)],
-                                 [int(src_cams[k].model == N.PBA_PINHOLE)
-                                  for k in range(self.n_pairs)])
+                                 idx[: self.n_pairs, 2], idx[: self.n_pairs, 3],
+                                 frame_pinhole[idx[: self.n_pairs, 2]])
         dev = self.device
         self.frames_t = _struct_tensor((N.Frame * max(1, len(frames)))(*frames), dev)
         self.pairs_t = _struct_tensor(pairs, dev)
