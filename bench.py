@@ -628,6 +628,9 @@ def run_ours(args):
         "compute": compute_roofline(counts[args.warmup:args.warmup + args.steps], lin_avg_ms)
         if world == 1 else None,
         "e2e": e2e,
+        # the reference's `count` (valid blocks) per second too
+        "valid_blocks_per_s": (statistics.mean(counts[args.warmup:args.warmup + args.steps])
+                               / (ms_per_step / 1e3)) if counts else None,
         "gpu_launches": int(round(launches)),
         "clocks": clocks.summary(),
     }
