@@ -150,9 +150,13 @@ int pba_plan_chunks(pba_pair* pairs, int32_t n_pairs, const pba_camera* src_cams
                     int32_t pixel_stride, int32_t chunk_pixels, int32_t* chunk_table,
                     int32_t* pair_chunk_offsets, int64_t* n_chunks_out);
 
+/* Bytes of the `partials` scratch of pba_linearize: the chunk partials
+ * (n_chunks x PBA_PARTIAL_DOUBLES doubles, rounded up to 256 B) followed by
+ * one pair setup (the pair's geometry, formed once per pair) per pair. */
+size_t pba_linearize_scratch_bytes(int32_t n_pairs, int64_t n_chunks);
 /* frames, pairs, chunk_table, pair_chunk_offsets, poses (n_poses x 12),
- * extrinsics (n_ext x 12), partials (n_chunks x PBA_PARTIAL_DOUBLES) and records
- * (n_pairs x 92) are device pointers; cfg is a host pointer.
+ * extrinsics (n_ext x 12), partials (pba_linearize_scratch_bytes bytes) and
+ * records (n_pairs x 92) are device pointers; cfg is a host pointer.
  * The chunk table's rows may be permuted freely before upload (it is the
  * CTA launch order; each chunk's partials go to slot
  * pair_chunk_offsets[pair] + first / chunk_pixels, so records do not

@@ -431,6 +431,44 @@ __device__ __forceinline__ void accumulate_cheap(double* Q, double* beta, double
 }
 
 
+// Everything a CTA of pair P needs that does not depend on the pixel: the
+// pair's geometry (build_setup) plus the paired / grouped copies the lean
+// loop reads with 16-byte shared loads.
+__device__ void fill_setup(PairSetup& S, const pba_frame* frames, const pba_pair& P,
+                           const double* poses, const double* exts, const pba_config& cfg) {
+  build_setup(S, frames, P, poses, exts, cfg.pixel_stride);
+  S.cfg = cfg;
+  S.sqw0 = sqrt(cfg.omega[0]);
+  S.sqw1 = sqrt(cfg.omega[1]);
+  const pba_camera& dc = S.dst_cam;
+  S.fx_cx[0] = dc.fx, S.fx_cx[1] = dc.cx, S.fy_cy[0] = dc.fy, S.fy_cy[1] = dc.cy;
+  S.fx_fy[0] = dc.fx, S.fx_fy[1] = dc.fy;
+  S.range[0] = dc.depth_min, S.range[1] = dc.depth_max;
+  S.wh[0] = (double)dc.width, S.wh[1] = (double)dc.height;
+  S.sqw0_dI[0] = S.sqw0, S.sqw0_dI[1] = cfg.huber_delta[0];
+  S.sqw1_dD[0] = S.sqw1, S.sqw1_dD[1] = cfg.huber_delta[1];
+  S.om01[0] = cfg.omega[0], S.om01[1] = cfg.omega[1];
+  S.om23[0] = cfg.omega[2], S.om23[1] = cfg.omega[3];
+  S.om4_dN[0] = cfg.omega[4], S.om4_dN[1] = cfg.huber_delta[2];
+  S.dwh[0] = dc.width, S.dwh[1] = dc.height;
+  S.np_sd[0] = S.src_np, S.np_sd[1] = S.dst_np;
+  S.src_geo[0] = S.stride, S.src_geo[1] = S.src_cam.width, S.src_geo[2] = S.src_np;
+  S.src_geo[3] = S.grid_w;
+  S.src_mh[0] = S.src_cam.model, S.src_mh[1] = S.src_cam.height;
+  S.src_ptrs[0] = S.src_tex, S.src_ptrs[1] = S.src_ray;
+}
+
+// One thread per pair: the setup every CTA of the pair copies (so no CTA
+// spends its start on one thread's serial matrix products).
+__global__ void pair_setup_kernel(const pba_frame* __restrict__ frames,
+                                  const pba_pair* __restrict__ pairs, int n_pairs,
+                                  const double* __restrict__ poses,
+                                  const double* __restrict__ exts, pba_config cfg,
+                                  PairSetup* __restrict__ setups) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n_pairs) fill_setup(setups[p], frames, pairs[p], poses, exts, cfg);
+}
+
 // kProbe 13 (diagnostics only): per-thread clock64 section timing, summed
 // into g_sect_cycles / g_sect_count (read by pba_diag_section_cycles).
 __device__ unsigned long long g_sect_cycles[8];
@@ -441,11 +479,9 @@ __device__ unsigned long long g_sect_count[8];
 // 7-sum stand-in for the 27-sum accumulation.
 template <bool kJac, int kT, int kMinBlocks, int kProbe = 0, bool kLean = false>
 __global__ void __launch_bounds__(kT, kMinBlocks)
-    linearize_kernel(const pba_frame* __restrict__ frames, const pba_pair* __restrict__ pairs,
-                     const int32_t* __restrict__ chunk_table,
+    linearize_kernel(const PairSetup* __restrict__ setups, const int32_t* __restrict__ chunk_table,
                      const int32_t* __restrict__ pair_chunk_offsets, int chunk_pixels,
-                     const double* __restrict__ poses, const double* __restrict__ exts,
-                     pba_config cfg, double* __restrict__ partials) {
+                     double* __restrict__ partials) {
   __shared__ PairSetup S;
   constexpr int kWarps = kT / 32;
   __shared__ double red[kWarps][kPart];
@@ -453,27 +489,11 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
   const long chunk = blockIdx.x;
   const int pair = chunk_table[2 * chunk];
   const int first = chunk_table[2 * chunk + 1];
-  if (threadIdx.x == 0) {
-    build_setup(S, frames, pairs[pair], poses, exts, cfg.pixel_stride);
-    S.cfg = cfg;
-    S.sqw0 = sqrt(cfg.omega[0]);
-    S.sqw1 = sqrt(cfg.omega[1]);
-    const pba_camera& dc = S.dst_cam;
-    S.fx_cx[0] = dc.fx, S.fx_cx[1] = dc.cx, S.fy_cy[0] = dc.fy, S.fy_cy[1] = dc.cy;
-    S.fx_fy[0] = dc.fx, S.fx_fy[1] = dc.fy;
-    S.range[0] = dc.depth_min, S.range[1] = dc.depth_max;
-    S.wh[0] = (double)dc.width, S.wh[1] = (double)dc.height;
-    S.sqw0_dI[0] = S.sqw0, S.sqw0_dI[1] = cfg.huber_delta[0];
-    S.sqw1_dD[0] = S.sqw1, S.sqw1_dD[1] = cfg.huber_delta[1];
-    S.om01[0] = cfg.omega[0], S.om01[1] = cfg.omega[1];
-    S.om23[0] = cfg.omega[2], S.om23[1] = cfg.omega[3];
-    S.om4_dN[0] = cfg.omega[4], S.om4_dN[1] = cfg.huber_delta[2];
-    S.dwh[0] = dc.width, S.dwh[1] = dc.height;
-    S.np_sd[0] = S.src_np, S.np_sd[1] = S.dst_np;
-    S.src_geo[0] = S.stride, S.src_geo[1] = S.src_cam.width, S.src_geo[2] = S.src_np;
-    S.src_geo[3] = S.grid_w;
-    S.src_mh[0] = S.src_cam.model, S.src_mh[1] = S.src_cam.height;
-    S.src_ptrs[0] = S.src_tex, S.src_ptrs[1] = S.src_ray;
+  {  // the pair's setup, formed once per pair by pair_setup_kernel: a coalesced copy
+    static_assert(sizeof(PairSetup) % 16 == 0, "PairSetup is copied in 16-byte words");
+    const int4* src = reinterpret_cast<const int4*>(setups + pair);
+    int4* dst = reinterpret_cast<int4*>(&S);
+    for (int i = threadIdx.x; i < (int)(sizeof(PairSetup) / 16); i += kT) dst[i] = __ldg(src + i);
   }
   __syncthreads();
 
@@ -487,12 +507,7 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
   int count = 0;
 
   const int last = min(first + chunk_pixels, S.n_px);
-  const int sW = S.src_cam.width, sH = S.src_cam.height;
-  const int dW = S.dst_cam.width, dH = S.dst_cam.height;
-  const bool src_sph = S.src_cam.model == PBA_SPHERICAL;
-  const bool dst_sph = S.dst_cam.model == PBA_SPHERICAL;
-  const double dWd = (double)dW, dHd = (double)dH;
-  const double sqw0 = sqrt(cfg.omega[0]), sqw1 = sqrt(cfg.omega[1]);
+  const int sW = S.src_cam.width;
 
   const int gw = S.grid_w;
   const int stride = S.stride;
@@ -1094,6 +1109,17 @@ extern "C" int pba_plan_chunks(pba_pair* pairs, int32_t n_pairs, const pba_camer
   return PBA_OK;
 }
 
+namespace {
+size_t partials_bytes(int64_t n_chunks) {
+  return ((size_t)n_chunks * kPart * sizeof(double) + 255) / 256 * 256;
+}
+}  // namespace
+
+extern "C" size_t pba_linearize_scratch_bytes(int32_t n_pairs, int64_t n_chunks) {
+  if (n_pairs < 0 || n_chunks < 0) return 0;
+  return partials_bytes(n_chunks) + (size_t)n_pairs * sizeof(PairSetup);
+}
+
 extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int32_t n_pairs,
                              const int32_t* chunk_table, int64_t n_chunks,
                              const int32_t* pair_chunk_offsets, int32_t chunk_pixels,
@@ -1110,6 +1136,13 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
                 "NULL buffer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (int rc = ensure_atan_table()) return rc;
+  // scratch = [chunk partials | per-pair setups] (pba_linearize_scratch_bytes)
+  PairSetup* setups = reinterpret_cast<PairSetup*>(reinterpret_cast<char*>(partials) +
+                                                   partials_bytes(n_chunks));
+  pair_setup_kernel<<<(unsigned)((n_pairs + 127) / 128), 128, 0, st>>>(frames, pairs, n_pairs,
+                                                                      poses, extrinsics, *cfg,
+                                                                      setups);
+  PBA_LAUNCH_CHECK();
   if (n_chunks > 0) {
     // CTA-size / occupancy variant (PBA_LIN_VARIANT overrides):
     //   6 (default): lean, 128 thr, 168 regs (12 warps/SM), no spills
@@ -1126,7 +1159,7 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
     }
     const unsigned grid = (unsigned)n_chunks;
 #define PBA_LAUNCH_LIN(J, T, M) \
-  linearize_kernel<J, T, M><<<grid, T, 0, st>>>(frames, pairs, chunk_table, pair_chunk_offsets, chunk_pixels, poses, extrinsics, *cfg, partials)
+  linearize_kernel<J, T, M><<<grid, T, 0, st>>>(setups, chunk_table, pair_chunk_offsets, chunk_pixels, partials)
     if (want_jacobians) {
       switch (variant) {
         case 1: PBA_LAUNCH_LIN(true, 256, 1); break;
@@ -1134,29 +1167,20 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
         case 5: PBA_LAUNCH_LIN(true, 512, 1); break;
         case 2: PBA_LAUNCH_LIN(true, 256, 2); break;
         case 20:
-          linearize_kernel<true, 128, 3, 10><<<grid, 128, 0, st>>>(frames, pairs, chunk_table, pair_chunk_offsets,
-                                                                 chunk_pixels, poses, extrinsics,
-                                                                 *cfg, partials);
+          linearize_kernel<true, 128, 3, 10><<<grid, 128, 0, st>>>(setups, chunk_table, pair_chunk_offsets, chunk_pixels, partials);
           break;
         case 21:
-          linearize_kernel<true, 128, 3, 11><<<grid, 128, 0, st>>>(frames, pairs, chunk_table, pair_chunk_offsets,
-                                                                 chunk_pixels, poses, extrinsics,
-                                                                 *cfg, partials);
+          linearize_kernel<true, 128, 3, 11><<<grid, 128, 0, st>>>(setups, chunk_table, pair_chunk_offsets, chunk_pixels, partials);
           break;
         case 24:
-          linearize_kernel<true, 128, 3, 13><<<grid, 128, 0, st>>>(frames, pairs, chunk_table, pair_chunk_offsets,
-                                                                 chunk_pixels, poses, extrinsics,
-                                                                 *cfg, partials);
+          linearize_kernel<true, 128, 3, 13><<<grid, 128, 0, st>>>(setups, chunk_table, pair_chunk_offsets, chunk_pixels, partials);
           break;
         case 9:  // diagnostics: destination gather replaced by a fixed texel
-          linearize_kernel<true, 128, 3, 1><<<grid, 128, 0, st>>>(frames, pairs, chunk_table, pair_chunk_offsets,
-                                                                chunk_pixels, poses, extrinsics,
-                                                                *cfg, partials);
+          linearize_kernel<true, 128, 3, 1><<<grid, 128, 0, st>>>(setups, chunk_table, pair_chunk_offsets, chunk_pixels, partials);
           break;
         case 4: PBA_LAUNCH_LIN(true, 128, 3); break;  // round-1 kernel (comparison)
         default:  // 6: lean (DESIGN.md §3 K1)
-          linearize_kernel<true, 128, 3, 0, true><<<grid, 128, 0, st>>>(frames, pairs, chunk_table, pair_chunk_offsets,
-                                                                      chunk_pixels, poses, extrinsics, *cfg, partials);
+          linearize_kernel<true, 128, 3, 0, true><<<grid, 128, 0, st>>>(setups, chunk_table, pair_chunk_offsets, chunk_pixels, partials);
           break;
       }
     } else {

@@ -359,8 +359,10 @@ class DeviceLevel:
         self.offsets_t = torch.from_numpy(offsets).to(dev)
         ext_arr = np.array(ext_rows, dtype=np.float64).reshape(-1, 12)
         self.ext_t = torch.from_numpy(ext_arr if len(ext_arr) else np.zeros((1, 12))).to(dev)
-        self.partials = torch.empty((max(1, self.n_chunks), N.PARTIAL_DOUBLES), dtype=torch.float64,
-                                    device=dev)
+        # chunk partials + one setup per pair (pba_linearize_scratch_bytes)
+        self.partials = torch.empty(
+            max(16, int(self.lib.pba_linearize_scratch_bytes(self.n_pairs, self.n_chunks))),
+            dtype=torch.uint8, device=dev)
         self.records = torch.zeros((max(1, self.n_pairs), N.RECORD_DOUBLES), dtype=torch.float64,
                                    device=dev)
         self.pixels_shard = sum(
