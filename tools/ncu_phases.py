@@ -95,8 +95,10 @@ def main():
             name = ph.get(ln, "other")
             # inlined helpers defined above the kernel: charge to their phase
             text = src[ln - 1]
-            if "ld.volatile.shared" in text:
+            if "ld.volatile.shared" in text or "__cvta_generic_to_shared" in text:
                 name = "setup reads (volatile LDS)"
+            elif "ld.global.nc.v2.f64" in text:
+                name = "gradient gathers + accumulation"
             elif ln < len(src) and ("bil4" in text or "r.x = fma(w11" in text or "r.y = fma(w11" in text):
                 name = "gradient gathers + accumulation"
             elif "return (1.0 - wy)" in text:
