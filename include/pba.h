@@ -141,8 +141,12 @@ int pba_build_texels(const pba_camera* cam, const double* intensity, const doubl
 /* ---- linearisation: _LevelProblem.evaluate per-pair part --------------
  * (solver.py:416-426 -> _edge_term :356-390 -> PairContext.evaluate :222-303)
  *
- * Work is split into chunks of `chunk_pixels` source pixels (of the
- * strided source grid).  pba_plan_chunks fills pairs[].n_chunks (host) and
+ * Work is split into chunks of consecutive source pixels (of the strided
+ * source grid, row-major): `chunk_pixels` of them, or — when at least 8
+ * rows fit in chunk_pixels and the grid width is a multiple of 16 — the
+ * multiple of 8 whole rows nearest chunk_pixels (K1 walks those in 16 x 8
+ * tiles; the per-pair size is re-derived on the device by the same rule).
+ * pba_plan_chunks fills pairs[].n_chunks (host) and
  * writes the chunk table (host, 2 int32 per chunk: pair index, first pixel)
  * and the per-pair chunk offsets (host, n_pairs+1 int32).  Returns the chunk
  * count via *n_chunks_out.  Pass chunk_table == NULL to only count. */
@@ -159,7 +163,7 @@ size_t pba_linearize_scratch_bytes(int32_t n_pairs, int64_t n_chunks);
  * records (n_pairs x 92) are device pointers; cfg is a host pointer.
  * The chunk table's rows may be permuted freely before upload (it is the
  * CTA launch order; each chunk's partials go to slot
- * pair_chunk_offsets[pair] + first / chunk_pixels, so records do not
+ * pair_chunk_offsets[pair] + first / (the pair's chunk size), so records do not
  * change); the Python host tiles it by (source, destination) frame blocks
  * for L2 locality (device.order_chunks).
  * want_jacobians = 0 is the cost-only path of total_error

@@ -26,11 +26,13 @@
 // residuals, Huber weights, Jacobians and the sums — stay in fp64 (SURVEY.md
 // App. B; fp32 H partials measurably broke the 1e-6 LM-cost parity).
 //
-// Work decomposition: one CTA per chunk of `chunk_pixels` consecutive source
-// pixels of one pair (row-major over the strided source grid).  A thread
-// walks pixels tid, tid+128, ... (128-thread CTAs, 3 per SM at 168
-// registers) so a warp reads 32 consecutive source texels and samples a
-// compact destination footprint.  Texels are the plane layout of
+// Work decomposition: one CTA per chunk of consecutive source pixels of one
+// pair (row-major over the strided source grid; whole 8-row bands where the
+// grid allows, pair_chunk_pixels).  128-thread CTAs, 3 per SM at 168
+// registers.  A band is walked in 16 x 8 tiles (a warp: 16 columns x 2 rows),
+// so the CTA's warps read 16-pixel source row segments and sample one
+// compact, shared destination footprint; other chunks are walked row-major
+// (thread tid takes pixels tid, tid + 128, ...).  Texels are the plane layout of
 // pba_common.cuh (16-byte pairs, plane-major).  Per-thread sums are
 // reduced by a fixed warp-shuffle tree and a fixed cross-warp order into one
 // 32-double partial per chunk; a finalisation kernel sums the chunk partials
@@ -140,6 +142,19 @@ __global__ void atan2_batch_kernel(const double* y, const double* x, int64_t n, 
 constexpr int kThreads = 256;  // default CTA size
 constexpr int kQ = 21;    // upper triangle of Q (6x6)
 constexpr int kPart = 32; // chunk partial: Q[21], beta[6], cost, count, pad
+constexpr int kTileCols = 16, kTileRows = 8;  // K1's tiled walk (128 threads)
+
+// Source pixels per chunk of a pair whose strided grid is gw wide.  Grids
+// at least 8 rows of which fit in the launch's chunk_pixels, with a width
+// that is a multiple of 16, get chunks of whole 8-row bands (the multiple of
+// 8 rows nearest chunk_pixels), which K1 walks in 16 x 8 tiles; others use
+// chunk_pixels.  Host (pba_plan_chunks) and device use the same rule.
+__host__ __device__ inline int pair_chunk_pixels(int gw, int chunk_pixels) {
+  if (gw <= 0 || gw % kTileCols != 0 || kTileRows * gw > chunk_pixels) return chunk_pixels;
+  const int bands = (chunk_pixels + kTileRows * gw / 2) / (kTileRows * gw);
+  return bands * kTileRows * gw;
+}
+
 
 struct PairSetup {
   double Ri[9], Rj[9], Ro[9];
@@ -430,6 +445,52 @@ __device__ __forceinline__ void accumulate_cheap(double* Q, double* beta, double
   beta[0] = fma(ww, ec, beta[0]);
 }
 
+// The chunk's per-thread sums -> one 32-double partial, in a fixed order.
+template <int kWarps, bool kJac>
+__device__ __forceinline__ void store_chunk_partial(const double* Q, const double* beta,
+                                                    double cost, int count,
+                                                    double (*red)[kPart], int pair, int first,
+                                                    int chunk_px,
+                                                    const int32_t* __restrict__ pair_chunk_offsets,
+                                                    double* __restrict__ partials) {
+  // ---- fixed-order reduction: warp reduce-scatter, then warps in order ----
+  // The 32 partial values (Q 21, beta 6, cost, count, 3 zero pads) are
+  // halved over lanes five times: at offset o a lane keeps the half of its
+  // values selected by its lane bit o and adds the partner's copy of that
+  // half, so after 16+8+4+2+1 = 31 shuffles lane L holds the warp sum of
+  // value L (a butterfly per value would take 29 x 5 = 145).
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double v[kPart];
+#pragma unroll
+  for (int k = 0; k < kQ; ++k) v[k] = kJac ? Q[k] : 0.0;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) v[kQ + k] = kJac ? beta[k] : 0.0;
+  v[27] = cost;
+  v[28] = (double)count;
+  v[29] = v[30] = v[31] = 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const bool upper = (lane & o) != 0;
+#pragma unroll
+    for (int k = 0; k < o; ++k) {
+      const double send = upper ? v[k] : v[k + o];
+      const double keep = upper ? v[k + o] : v[k];
+      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  red[warp][lane] = v[0];
+  __syncthreads();
+  if (threadIdx.x < kPart) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) s += red[w][threadIdx.x];
+    // slot of this chunk in its pair's range (the launch order of the chunk
+    // table is free; the per-pair sums always run in chunk order)
+    const long slot = PBA_DCHECK_INDEX(pair_chunk_offsets[pair] + first / chunk_px,
+                                       pair_chunk_offsets[pair + 1]);
+    partials[slot * kPart + threadIdx.x] = s;
+  }
+}
 
 // Everything a CTA of pair P needs that does not depend on the pixel: the
 // pair's geometry (build_setup) plus the paired / grouped copies the lean
@@ -477,7 +538,8 @@ __device__ unsigned long long g_sect_count[8];
 // kProbe (diagnostics only, K1 ablations): 0 normal; 1 every
 // sample reads one fixed destination texel; 10 no gradient gathers; 11 a
 // 7-sum stand-in for the 27-sum accumulation.
-template <bool kJac, int kT, int kMinBlocks, int kProbe = 0, bool kLean = false>
+template <bool kJac, int kT, int kMinBlocks, int kProbe = 0, bool kLean = false,
+          bool kTile = kLean>
 __global__ void __launch_bounds__(kT, kMinBlocks)
     linearize_kernel(const PairSetup* __restrict__ setups, const int32_t* __restrict__ chunk_table,
                      const int32_t* __restrict__ pair_chunk_offsets, int chunk_pixels,
@@ -506,13 +568,37 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
   double cost = 0.0;
   int count = 0;
 
-  const int last = min(first + chunk_pixels, S.n_px);
+  const int chunk_px = pair_chunk_pixels(S.grid_w, chunk_pixels);
+  const int last = min(first + chunk_px, S.n_px);
   const int sW = S.src_cam.width;
 
   const int gw = S.grid_w;
   const int stride = S.stride;
   int gr = (first + (int)threadIdx.x) / gw;       // strided-grid row / column of
   int gcol = first + (int)threadIdx.x - gr * gw;  // this thread's current pixel
+  // kTile: a chunk of whole 8-row bands (pair_chunk_pixels) is walked in
+  // 16-column x 8-row tiles — warp w covers rows 2w, 2w + 1 of the band —
+  // so the CTA's four warps sample overlapping destination rows at the same
+  // time and each destination row is fetched from L2 about once per band
+  // instead of twice (row-major walk: once as the lower corner row of source
+  // row r, again as the upper one of row r + 1, a full row later).  Other
+  // chunks keep the row-major walk.  Same pixel set, same partial slot.
+  __shared__ int walk[2];  // column step, rows per wrap
+  if constexpr (kTile) {
+    static_assert(kT == kTileCols * kTileRows, "the tiled walk assumes 128-thread CTAs");
+    const int n = last - first;
+    const bool tiled = first % gw == 0 && n % gw == 0 && (n / gw) % kTileRows == 0 &&
+                       gw % kTileCols == 0;
+    if (tiled) {
+      gr = first / gw + (int)threadIdx.x / kTileCols;
+      gcol = (int)threadIdx.x % kTileCols;
+    }
+    if (threadIdx.x == 0) {
+      walk[0] = tiled ? kTileCols : kT;
+      walk[1] = tiled ? kTileRows : 1;
+    }
+    __syncthreads();
+  }
   // The source texel of the next pixel is always in flight one iteration
   // ahead: its (I, D) and (nz, mask) pairs, 2 x 16 B.  Masks come from the
   // texel planes themselves (not the separate mask plane), so a pixel costs
@@ -567,7 +653,16 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
 
     ngr = gr;
     ngcol = gcol;
-    advance_pixel(ngr, ngcol, sg.w, kT);
+    if constexpr (kTile) {
+      const int2 wk = setup_pair(walk);
+      ngcol += wk.x;
+      while (ngcol >= sg.w) {
+        ngcol -= sg.w;
+        ngr += wk.y;
+      }
+    } else {
+      advance_pixel(ngr, ngcol, sg.w, kT);
+    }
     if (!kNoPrefetch && idx + kT < last) {
       const double2* t = s_tex + PBA_DCHECK_INDEX(ngr * sg.x * sg.y + ngcol * sg.x, sg.z);
       nx0 = __ldg(t);
@@ -948,43 +1043,11 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     }
   }
 
-  // ---- fixed-order reduction: warp reduce-scatter, then warps in order ----
-  // The 32 partial values (Q 21, beta 6, cost, count, 3 zero pads) are
-  // halved over lanes five times: at offset o a lane keeps the half of its
-  // values selected by its lane bit o and adds the partner's copy of that
-  // half, so after 16+8+4+2+1 = 31 shuffles lane L holds the warp sum of
-  // value L (a butterfly per value would take 29 x 5 = 145).
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double v[kPart];
-#pragma unroll
-  for (int k = 0; k < kQ; ++k) v[k] = kJac ? Q[k] : 0.0;
-#pragma unroll
-  for (int k = 0; k < 6; ++k) v[kQ + k] = kJac ? beta[k] : 0.0;
-  v[27] = cost;
-  v[28] = (double)count;
-  v[29] = v[30] = v[31] = 0.0;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const bool upper = (lane & o) != 0;
-#pragma unroll
-    for (int k = 0; k < o; ++k) {
-      const double send = upper ? v[k] : v[k + o];
-      const double keep = upper ? v[k + o] : v[k];
-      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-    }
-  }
-  red[warp][lane] = v[0];
-  __syncthreads();
-  if (threadIdx.x < kPart) {
-    double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) s += red[w][threadIdx.x];
-    // slot of this chunk in its pair's range (the launch order of the chunk
-    // table is free; the per-pair sums always run in chunk order)
-    const long slot = PBA_DCHECK_INDEX(pair_chunk_offsets[pair] + first / chunk_pixels,
-                                       pair_chunk_offsets[pair + 1]);
-    partials[slot * kPart + threadIdx.x] = s;
-  }
+  // (the chunk size re-derived from a fresh shared read: nothing stays live
+  // across the pixel loop for it)
+  store_chunk_partial<kWarps, kJac>(Q, beta, cost, count, red, pair, first,
+                                    pair_chunk_pixels(SetupRead<true>::get(S.grid_w), chunk_pixels),
+                                    pair_chunk_offsets, partials);
 }
 
 // One warp per pair: sum the pair's chunk partials in chunk order, then
@@ -1092,13 +1155,14 @@ extern "C" int pba_plan_chunks(pba_pair* pairs, int32_t n_pairs, const pba_camer
     const int64_t gh = (c.height + pixel_stride - 1) / pixel_stride;
     const int64_t npx = gw * gh;
     PBA_ARG_CHECK(npx < (int64_t)1 << 31, "source image too large");
-    const int64_t nc = npx == 0 ? 0 : (npx + chunk_pixels - 1) / chunk_pixels;
+    const int64_t cp = pair_chunk_pixels((int)gw, chunk_pixels);
+    const int64_t nc = npx == 0 ? 0 : (npx + cp - 1) / cp;
     pairs[p].n_chunks = (int32_t)nc;
     if (pair_chunk_offsets) pair_chunk_offsets[p] = (int32_t)total;
     if (chunk_table) {
       for (int64_t k = 0; k < nc; ++k) {
         chunk_table[2 * (total + k)] = p;
-        chunk_table[2 * (total + k) + 1] = (int32_t)(k * chunk_pixels);
+        chunk_table[2 * (total + k) + 1] = (int32_t)(k * cp);
       }
     }
     total += nc;
@@ -1145,7 +1209,8 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
   PBA_LAUNCH_CHECK();
   if (n_chunks > 0) {
     // CTA-size / occupancy variant (PBA_LIN_VARIANT overrides):
-    //   6 (default): lean, 128 thr, 168 regs (12 warps/SM), no spills
+    //   6 (default): lean, tiled walk, 128 thr, 168 regs (12 warps/SM)
+    //   7: lean, row-major walk
     //   1: 256 thr, <=255 regs (8 warps/SM)    2: 256 thr, 128 regs (16 warps/SM)
     //   3: 128 thr, 128 regs (16 warps/SM)     4: round-1 kernel, 128 thr, 168 regs
     //   5: 512 thr, 128 regs (16 warps/SM)
@@ -1160,6 +1225,8 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
     const unsigned grid = (unsigned)n_chunks;
 #define PBA_LAUNCH_LIN(J, T, M) \
   linearize_kernel<J, T, M><<<grid, T, 0, st>>>(setups, chunk_table, pair_chunk_offsets, chunk_pixels, partials)
+#define PBA_LAUNCH_COST(M) \
+  linearize_kernel<false, 128, M, 0, false, true><<<grid, 128, 0, st>>>(setups, chunk_table, pair_chunk_offsets, chunk_pixels, partials)
     if (want_jacobians) {
       switch (variant) {
         case 1: PBA_LAUNCH_LIN(true, 256, 1); break;
@@ -1179,8 +1246,11 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
           linearize_kernel<true, 128, 3, 1><<<grid, 128, 0, st>>>(setups, chunk_table, pair_chunk_offsets, chunk_pixels, partials);
           break;
         case 4: PBA_LAUNCH_LIN(true, 128, 3); break;  // round-1 kernel (comparison)
-        default:  // 6: lean (DESIGN.md §3 K1)
-          linearize_kernel<true, 128, 3, 0, true><<<grid, 128, 0, st>>>(setups, chunk_table, pair_chunk_offsets, chunk_pixels, partials);
+        case 7:  // lean, row-major walk (comparison)
+          linearize_kernel<true, 128, 3, 0, true, false><<<grid, 128, 0, st>>>(setups, chunk_table, pair_chunk_offsets, chunk_pixels, partials);
+          break;
+        default:  // 6: lean, tiled walk (DESIGN.md §3 K1)
+          linearize_kernel<true, 128, 3, 0, true, true><<<grid, 128, 0, st>>>(setups, chunk_table, pair_chunk_offsets, chunk_pixels, partials);
           break;
       }
     } else {
@@ -1194,13 +1264,17 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
         cvariant = env ? atoi(env) : 5;
       }
       switch (cvariant) {
-        case 3: PBA_LAUNCH_LIN(false, 128, 3); break;
-        case 4: PBA_LAUNCH_LIN(false, 128, 4); break;
-        case 6: PBA_LAUNCH_LIN(false, 128, 6); break;
-        default: PBA_LAUNCH_LIN(false, 128, 5); break;
+        case 3: PBA_LAUNCH_COST(3); break;
+        case 4: PBA_LAUNCH_COST(4); break;
+        case 6: PBA_LAUNCH_COST(6); break;
+        case 7:  // row-major walk (comparison)
+          linearize_kernel<false, 128, 5><<<grid, 128, 0, st>>>(setups, chunk_table, pair_chunk_offsets, chunk_pixels, partials);
+          break;
+        default: PBA_LAUNCH_COST(5); break;
       }
     }
 #undef PBA_LAUNCH_LIN
+#undef PBA_LAUNCH_COST
     PBA_LAUNCH_CHECK();
   }
   finalize_pairs_kernel<<<(unsigned)((n_pairs + 3) / 4), 128, 0, st>>>(

@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 
 import numpy as np
 import torch
@@ -50,7 +51,8 @@ def chunk_pixels_for(total_pixels: int) -> int:
     most 8192 (the measured optimum on c4: 64 pixels per thread of the
     128-thread CTA, DESIGN.md §3 K1)."""
     units = total_pixels // (PIXELS_PER_CHUNK_UNIT * SM_COUNT * 4)
-    units = max(1, min(MAX_CHUNK_UNITS, int(units)))
+    cap = int(os.environ.get("PBA_CHUNK_UNITS", MAX_CHUNK_UNITS))  # (experiments)
+    units = max(1, min(cap, int(units)))
     return PIXELS_PER_CHUNK_UNIT * units
 
 
@@ -87,14 +89,15 @@ def order_chunks(chunk_tab, n_chunks, chunk_pixels, src_of_pair, dst_of_pair,
       "dst": pairs sharing a destination frame interleaved chunk by chunk;
       "src": the same for the source frame;  "pair": edge order.
     """
-    import os
 
     order = os.environ.get("PBA_CHUNK_ORDER", "blk")
     if order == "pair" or n_chunks == 0:
         return chunk_tab
     tab = chunk_tab[: 2 * n_chunks].reshape(-1, 2)
     pair = tab[:, 0].astype(np.int64)
-    pos = tab[:, 1].astype(np.int64) // chunk_pixels
+    # chunk position inside its pair (the plan lists each pair's chunks in
+    # order, pairs ascending; chunk sizes differ between pairs)
+    pos = np.arange(len(pair), dtype=np.int64) - np.searchsorted(pair, pair, side="left")
     src = np.asarray(src_of_pair, np.int64)[pair]
     dst = np.asarray(dst_of_pair, np.int64)[pair]
     if order == "blk":
@@ -623,8 +626,7 @@ class DeviceLevel:
                     self._capture_step(c)
 
     def _graph_enabled(self) -> bool:
-        import os
-
+    
         return (self.has_solver and not self._graph_failed
                 and os.environ.get("PBA_GRAPH", "1") != "0")
 
