@@ -108,8 +108,14 @@ typedef struct pba_config {
   double huber_delta[3]; /* intensity, depth, normal */
   double omega[5];       /* [I, D, nx, ny, nz] = omega_diagonal() (solver.py:90-91) */
   int32_t pixel_stride;  /* source pixel stride (solver.py:200-207) */
-  int32_t _pad;
+  int32_t flags;         /* launch hints (PBA_CFG_*); 0 is always valid */
 } pba_config;
+/* pba_config.flags: some pair samples a pinhole destination image.  Selects
+ * the K1 instantiation that prefetches the next tile's destination footprint
+ * into L1 for those pairs (measured: faster on pinhole destinations, slower
+ * on the spherical scans).  A launch-shape hint only: results are identical
+ * with or without it. */
+#define PBA_CFG_PINHOLE_DST 1
 
 /* ---- layout queries --------------------------------------------------- */
 size_t pba_texel_bytes(void);

@@ -539,7 +539,7 @@ __device__ unsigned long long g_sect_count[8];
 // sample reads one fixed destination texel; 10 no gradient gathers; 11 a
 // 7-sum stand-in for the 27-sum accumulation.
 template <bool kJac, int kT, int kMinBlocks, int kProbe = 0, bool kLean = false,
-          bool kTile = kLean>
+          bool kTile = kLean, int kPf = 0>
 __global__ void __launch_bounds__(kT, kMinBlocks)
     linearize_kernel(const PairSetup* __restrict__ setups, const int32_t* __restrict__ chunk_table,
                      const int32_t* __restrict__ pair_chunk_offsets, int chunk_pixels,
@@ -790,6 +790,24 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     const double2 a00 = __ldg(t00), a01 = __ldg(t00 + 1), a10 = __ldg(t10), a11 = __ldg(t10 + 1);
     const double2 m00 = __ldg(t00 + kPairNzM * dnp), m01 = __ldg(t00 + kPairNzM * dnp + 1);
     const double2 m10 = __ldg(t10 + kPairNzM * dnp), m11 = __ldg(t10 + kPairNzM * dnp + 1);
+    if constexpr (kPf > 0) {
+      // Pinhole destinations (PBA_CFG_PINHOLE_DST launches): L1 prefetch of
+      // the footprint this thread's next pixel (one tile, 16 source columns,
+      // to the right) most likely samples, all eight texel planes.  c3/100:
+      // 15.84 -> 15.44 ms; on the spherical scans the same prefetch was
+      // slower (27.40 -> 28.35 ms c4/200), so it is skipped for them, and
+      // launches without pinhole destinations use the kPf = 0 kernel (the
+      // prefetch costs registers).
+      if (x0 + kTileCols + 1 < dwh.x && !dsph) {
+        constexpr int order[8] = {0, kPairNzM, kPairGI, kPairGI + 1, kPairNxy, 5, 6, 7};
+#pragma unroll
+        for (int k = 0; k < kPf; ++k) {
+          const double2* p = t00 + kTileCols + order[k] * dnp;
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(p + dwh.x));
+        }
+      }
+    }
     double MP0[3], MP1[3], ud[3];
     double rho2 = 0.0;
     if constexpr (kEarlyMP && kJac) {
@@ -1250,7 +1268,10 @@ extern "C" int pba_linearize(const pba_frame* frames, const pba_pair* pairs, int
           linearize_kernel<true, 128, 3, 0, true, false><<<grid, 128, 0, st>>>(setups, chunk_table, pair_chunk_offsets, chunk_pixels, partials);
           break;
         default:  // 6: lean, tiled walk (DESIGN.md §3 K1)
-          linearize_kernel<true, 128, 3, 0, true, true><<<grid, 128, 0, st>>>(setups, chunk_table, pair_chunk_offsets, chunk_pixels, partials);
+          if (cfg->flags & PBA_CFG_PINHOLE_DST)
+            linearize_kernel<true, 128, 3, 0, true, true, 8><<<grid, 128, 0, st>>>(setups, chunk_table, pair_chunk_offsets, chunk_pixels, partials);
+          else
+            linearize_kernel<true, 128, 3, 0, true, true><<<grid, 128, 0, st>>>(setups, chunk_table, pair_chunk_offsets, chunk_pixels, partials);
           break;
       }
     } else {

@@ -342,6 +342,8 @@ class DeviceLevel:
                                   dtype=np.uint8).reshape(-1, ctypes.sizeof(N.Camera))
         src_cams = (N.Camera * max(1, self.n_pairs)).from_buffer_copy(
             cam_bytes[idx[:, 2]].tobytes())
+        if self.n_pairs and any(frames[d].cam.model == N.PBA_PINHOLE for d in set(idx[:, 3])):
+            self.ccfg.flags |= N.PBA_CFG_PINHOLE_DST
         n_chunks = ctypes.c_int64(0)
         N.check(self.lib.pba_plan_chunks(pairs, self.n_pairs, src_cams, stride, self.chunk_pixels,
                                          None, None, ctypes.byref(n_chunks)), "pba_plan_chunks")

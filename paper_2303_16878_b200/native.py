@@ -25,6 +25,7 @@ PBA_RASTER_U16_DEPTH = 2
 PBA_PINHOLE = 0
 PBA_SPHERICAL = 1
 PBA_SOLVE_REUSE_PLAN = 1
+PBA_CFG_PINHOLE_DST = 1  # pba_config.flags: pinhole destinations present (K1 prefetch)
 RECORD_DOUBLES = 92
 NORMALS_RECHECK_DOUBLES = 10
 PARTIAL_DOUBLES = 32
@@ -65,7 +66,7 @@ class Pair(ctypes.Structure):
 
 class Config(ctypes.Structure):
     _fields_ = [("huber_delta", ctypes.c_double * 3), ("omega", ctypes.c_double * 5),
-                ("pixel_stride", ctypes.c_int32), ("_pad", ctypes.c_int32)]
+                ("pixel_stride", ctypes.c_int32), ("flags", ctypes.c_int32)]
 
 
 class NormalConfigC(ctypes.Structure):

@@ -7,6 +7,6 @@ run() { # tag variant
 }
 V=(${VARIANTS:-6 7})
 for i in 1 2; do for v in "${V[@]}"; do run v${v}_$i $v; done; done
-if [ -n "${PARITY:-1}" ]; then
+if [ -n "${PARITY-1}" ]; then
   PBA_LIN_VARIANT=${V[-1]} timeout 1200 python -m pytest -x -q tests/test_gpu_parity.py tests/test_gpu_configs.py -k "not c2_full and not c3" 2>&1 | tail -5
 fi
