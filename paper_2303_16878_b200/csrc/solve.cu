@@ -945,6 +945,129 @@ extern "C" size_t pba_solve_work_bytes(int32_t dim) {
          align_up(T * T * sizeof(int32_t), 256) + align_up(2 * T * sizeof(int32_t), 256);
 }
 
+namespace pba {
+namespace {
+// dim <= 64 (one tile, e.g. c1's 54): damping, factorisation and both
+// substitutions in one CTA — the tiled path's four launches (damp, tile
+// flags, diagonal-tile potrf with its inverse, substitution) cost ~48 us
+// there, mostly launch and barrier latency of kernels sized for big tiles.
+// LDL^T by right-looking elimination on the unscaled columns
+// (A_ij -= A_ik A_jk / A_kk for k < j <= i) of the matrix bordered by the
+// row -b^T, so the elimination also yields the forward substitution (row
+// dim ends as L~^{-1} (-b), L~ the unit lower factor).  Eight threads share
+// each row (every eighth column of it), so a step updates only the live
+// trailing entries (n^3/6 in all) with one barrier (a column-per-thread split
+// reads along diagonals: 4-way bank conflicts, 1.4x slower).  Warp 0 then
+// solves L~^T x = D^{-1} y with two rows per lane.
+constexpr int kSmallQ = 8;  // threads per row
+constexpr int kSmallThreads = ((NB + 1) * kSmallQ + 31) / 32 * 32;  // rows 0..64, 544
+__global__ void __launch_bounds__(kSmallThreads)
+    small_solve_kernel(HSource H, const double* __restrict__ b, int dim, double lam_arg,
+                       const double* __restrict__ lam_dev, double* __restrict__ delta,
+                       int32_t* __restrict__ status) {
+  // unscaled columns; row dim = L~^{-1} (-b).  Row stride 68 doubles: the
+  // four rows of a warp's row writes fall on distinct bank halves.
+  constexpr int kLd = 68;
+  __shared__ double L[NB + 1][kLd];
+  __shared__ int rp[NB / 6 + 2];
+  const int tid = threadIdx.x;
+  const double lam = lam_dev ? *lam_dev : lam_arg;
+  // Stage H's lower triangle and the border row in L.  Every global load of
+  // a thread is issued before its first shared store (the compiler cannot
+  // prove a generic load does not alias the shared tile, so an interleaved
+  // loop would wait out one global round trip per entry).
+  for (int e = tid; e < (dim + 1) * kLd; e += kSmallThreads) (&L[0][0])[e] = 0.0;
+  if (H.row_ptr)
+    for (int t = tid; t <= dim / 6; t += kSmallThreads) rp[t] = H.row_ptr[t];
+  __syncthreads();
+  {
+    constexpr int kMaxPer = (NB * NB + kSmallThreads - 1) / kSmallThreads;  // 16
+    double v[kMaxPer];
+    int at[kMaxPer];  // i * kLd + j, or -1
+    const int n = H.row_ptr ? 36 * rp[dim / 6] : dim * dim;
+#pragma unroll
+    for (int r = 0; r < kMaxPer; ++r) {
+      const int e = tid + r * kSmallThreads;
+      at[r] = -1;
+      v[r] = 0.0;
+      if (e < n) {
+        int i, jj;
+        if (H.row_ptr) {
+          const int blk = e / 36, rc = e - 36 * blk;
+          int br = 0;
+          while (rp[br + 1] <= blk) ++br;
+          i = 6 * br + rc / 6;
+          jj = 6 * H.cols[blk] + rc % 6;
+        } else {
+          i = e / dim;
+          jj = e - i * dim;
+        }
+        if (jj <= i) {
+          at[r] = i * kLd + jj;
+          v[r] = H.H[e];
+        }
+      }
+    }
+    const double bj = tid < dim ? -b[tid] : 0.0;
+#pragma unroll
+    for (int r = 0; r < kMaxPer; ++r)
+      if (at[r] >= 0) (&L[0][0])[at[r]] = v[r];
+    if (tid < dim) L[dim][tid] = bj;
+  }
+  __syncthreads();
+  if (tid < dim) L[tid][tid] = L[tid][tid] + lam * L[tid][tid];  // h + lam * np.diag(np.diag(h))
+  __syncthreads();
+  // thread (i, q) updates row i's entries j = k+1+q, k+1+q+8, ... <= min(i, dim-1)
+  const int i = tid / kSmallQ, q = tid - i * kSmallQ;
+  bool bad = false;
+  for (int k = 0; k < dim; ++k) {
+    const double d = L[k][k];  // final since step k - 1 (the same value in every thread)
+    if (!(d > 0.0)) {
+      bad = true;
+      break;
+    }
+    if (i > k && i <= dim) {
+      const double f = L[i][k] * __drcp_rn(d);
+      const int jmax = min(i, dim - 1);
+      // all loads first (column k is read-only in this step), then the updates
+      double lk[NB / kSmallQ], li[NB / kSmallQ];
+#pragma unroll
+      for (int r = 0; r < NB / kSmallQ; ++r) {
+        const int jj = k + 1 + q + kSmallQ * r;
+        lk[r] = jj <= jmax ? L[jj][k] : 0.0;
+        li[r] = jj <= jmax ? L[i][jj] : 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < NB / kSmallQ; ++r) {
+        const int jj = k + 1 + q + kSmallQ * r;
+        if (jj <= jmax) L[i][jj] = fma(-lk[r], f, li[r]);
+      }
+    }
+    __syncthreads();
+  }
+  if (bad) {  // the reference's LinAlgError
+    if (tid == 0) *status = 1;
+    return;
+  }
+  if (tid >= 32) return;
+  // L~^T x = z, z_j = y_j / d_j, L~_ij = L_ij / d_j: column sweep from the last row
+  const int r0 = tid, r1 = tid + 32;
+  const double id0 = r0 < dim ? __drcp_rn(L[r0][r0]) : 0.0;
+  const double id1 = r1 < dim ? __drcp_rn(L[r1][r1]) : 0.0;
+  double z0 = r0 < dim ? L[dim][r0] * id0 : 0.0, z1 = r1 < dim ? L[dim][r1] * id1 : 0.0;
+  for (int k = dim - 1; k > 0; --k) {
+    const double xk = __shfl_sync(0xffffffffu, k < 32 ? z0 : z1, k & 31);
+    if (r0 < k) z0 = fma(-L[k][r0] * id0, xk, z0);
+    if (r1 < k) z1 = fma(-L[k][r1] * id1, xk, z1);
+  }
+  if (r0 < dim) delta[r0] = z0;
+  if (r1 < dim) delta[r1] = z1;
+  if (tid == 0) *status = 0;
+}
+
+}  // namespace
+}  // namespace pba
+
 namespace {
 int solve_dense_impl(HSource H, const double* b, int32_t dim, double lam, const double* lam_dev,
                      const int32_t* tile_env, void* work, int32_t flags, double* delta,
@@ -978,6 +1101,11 @@ int solve_dense_impl(HSource H, const double* b, int32_t dim, double lam, const 
   if (dissect < 0) {
     const char* env = getenv("PBA_SOLVE_DISSECT");
     dissect = !(env && env[0] == '0');
+  }
+  if (T == 1 && potrf_variant == 1) {
+    small_solve_kernel<<<1, kSmallThreads, 0, st>>>(H, b, dim, lam, lam_dev, delta, status);
+    PBA_LAUNCH_CHECK();
+    return PBA_OK;
   }
   if (dissect && potrf_variant == 1) {
     PBA_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int32_t), st));

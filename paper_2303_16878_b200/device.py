@@ -27,6 +27,7 @@ from .camera import PINHOLE, ray_table
 PIXELS_PER_CHUNK_UNIT = 256  # chunk sizes are multiples of this
 MAX_CHUNK_UNITS = 32         # <= 8192 pixels per chunk: 64 per thread of K1's 128-thread CTA
 SM_COUNT = 148
+K1_CTAS_PER_SM = 3           # resident K1 CTAs per SM (168 registers x 128 threads)
 
 
 def camera_struct(intr) -> N.Camera:
@@ -47,12 +48,16 @@ def _struct_tensor(arr, device) -> torch.Tensor:
 def chunk_pixels_for(total_pixels: int) -> int:
     """Source pixels per K1 CTA (chunk).  Chosen from the whole level problem
     (never from a shard) so per-pair sums are identical for any GPU count:
-    enough chunks for ~4 waves over 148 SMs, in multiples of 256 pixels, at
-    most 8192 (the measured optimum on c4: 64 pixels per thread of the
-    128-thread CTA, DESIGN.md §3 K1)."""
-    units = total_pixels // (PIXELS_PER_CHUNK_UNIT * SM_COUNT * 4)
-    cap = int(os.environ.get("PBA_CHUNK_UNITS", MAX_CHUNK_UNITS))  # (experiments)
-    units = max(1, min(cap, int(units)))
+    at least one full wave of resident K1 CTAs (3 per SM on 148 SMs), in
+    multiples of 256 pixels, at most 8192 (the measured optimum on c4: 64
+    pixels per thread of the 128-thread CTA, DESIGN.md §3 K1).  c1: 1024
+    pixels (456 CTAs), 0.0575 -> 0.0511 ms per linearisation vs 768 (600
+    CTAs, 1.35 waves).  pba_plan_chunks may round a pair's chunk to whole
+    8-row bands (pair_chunk_pixels)."""
+    units = max(1, min(MAX_CHUNK_UNITS,
+                       int(total_pixels // (PIXELS_PER_CHUNK_UNIT * SM_COUNT * K1_CTAS_PER_SM))))
+    if os.environ.get("PBA_CHUNK_UNITS"):  # (experiments: a fixed chunk size)
+        units = max(1, int(os.environ["PBA_CHUNK_UNITS"]))
     return PIXELS_PER_CHUNK_UNIT * units
 
 

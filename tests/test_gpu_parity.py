@@ -254,8 +254,12 @@ def _dense_solve(H, b, lam, env=None):
     return delta.cpu().numpy(), int(status.item())
 
 
-@pytest.mark.parametrize("dim,band", [(54, None), (130, None), (594, None), (600, 40), (1998, 126)])
+@pytest.mark.parametrize("dim,band", [(1, None), (6, None), (54, None), (63, None), (64, None),
+                                      (65, None), (130, None), (594, None), (600, 40),
+                                      (1998, 126)])
 def test_dense_cholesky_matches_numpy_solve(dim, band):
+    """dim <= 64 runs the one-CTA small solve (c1), larger ones the tiled
+    factorisation."""
     rng = np.random.default_rng(dim)
     A = rng.normal(size=(dim, dim))
     if band is not None:
@@ -310,11 +314,15 @@ def test_dissected_cholesky_reports_singular():
     assert st == 1
 
 
-def test_dense_cholesky_reports_singular():
-    H = np.eye(12)
+@pytest.mark.parametrize("dim", [12, 200])
+def test_dense_cholesky_reports_singular(dim):
+    H = np.eye(dim)
     H[5, 5] = 0.0
-    _, st = _dense_solve(H, np.ones(12), 1e-3)
+    _, st = _dense_solve(H, np.ones(dim), 1e-3)
     assert st == 1
+    # the status word is rewritten by the next (good) solve
+    x, st = _dense_solve(np.eye(dim) * 2.0, np.ones(dim), 0.0)
+    assert st == 0 and np.allclose(x, -0.5)
 
 
 def test_apply_step_matches_host_boxplus():
