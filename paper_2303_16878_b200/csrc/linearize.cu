@@ -1082,8 +1082,17 @@ __global__ void finalize_pairs_kernel(const double* __restrict__ partials,
   const int p = blockIdx.x * 4 + w;
   if (p >= n_pairs) return;
   const int c0 = offsets[p], c1 = offsets[p + 1];
+  // chunk order, eight loads in flight at a time (same sums, same order)
   double s = 0.0;
-  for (int c = c0; c < c1; ++c) s += partials[(long)c * kPart + lane];
+  int c = c0;
+  for (; c + 8 <= c1; c += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = partials[(long)(c + u) * kPart + lane];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += v[u];
+  }
+  for (; c < c1; ++c) s += partials[(long)c * kPart + lane];
   sQ[w][lane] = s;
   if (lane == 0) {
     const pba_pair P = pairs[p];
