@@ -47,15 +47,18 @@ def _struct_tensor(arr, device) -> torch.Tensor:
 
 def chunk_pixels_for(total_pixels: int) -> int:
     """Source pixels per K1 CTA (chunk).  Chosen from the whole level problem
-    (never from a shard) so per-pair sums are identical for any GPU count:
-    at least one full wave of resident K1 CTAs (3 per SM on 148 SMs), in
-    multiples of 256 pixels, at most 8192 (the measured optimum on c4: 64
-    pixels per thread of the 128-thread CTA, DESIGN.md §3 K1).  c1: 1024
-    pixels (456 CTAs), 0.0575 -> 0.0511 ms per linearisation vs 768 (600
-    CTAs, 1.35 waves).  pba_plan_chunks may round a pair's chunk to whole
-    8-row bands (pair_chunk_pixels)."""
-    units = max(1, min(MAX_CHUNK_UNITS,
-                       int(total_pixels // (PIXELS_PER_CHUNK_UNIT * SM_COUNT * K1_CTAS_PER_SM))))
+    (never from a shard) so per-pair sums are identical for any GPU count.
+    In multiples of 256 pixels: ~32 waves of resident K1 CTAs (3 per SM on
+    148 SMs) so the last wave's tail stays small, between 1,024 and 8,192
+    pixels (8,192 = 64 pixels per thread of the 128-thread CTA, the measured
+    optimum on c4; c2, 47 M pixels: 3,328 -> 3.23 ms per linearisation vs
+    8,192 -> 3.31 / 3.45 ms row-major / tiled); a problem too small for one
+    wave at 1,024 gets one wave (DESIGN.md §3 K1).  pba_plan_chunks may round
+    a pair's chunk to whole 8-row bands (pair_chunk_pixels)."""
+    wave = PIXELS_PER_CHUNK_UNIT * SM_COUNT * K1_CTAS_PER_SM
+    units = max(4, min(MAX_CHUNK_UNITS, total_pixels // (wave * 32)))
+    if total_pixels < wave * units:  # not even one wave: one wave of smaller chunks
+        units = max(1, total_pixels // wave)
     if os.environ.get("PBA_CHUNK_UNITS"):  # (experiments: a fixed chunk size)
         units = max(1, int(os.environ["PBA_CHUNK_UNITS"]))
     return PIXELS_PER_CHUNK_UNIT * units
