@@ -18,3 +18,6 @@ out = bench.e2e_api("c4", None, dev, None, None)
 pr.disable()
 print("seconds", out["seconds"], "first", out["seconds_first_call"])
 pstats.Stats(pr).sort_stats("cumulative").print_stats(45)
+st = pstats.Stats(pr)
+st.print_callers("method 'cpu'")
+st.print_callers("__init__\\)$")
