@@ -204,6 +204,45 @@ def test_host_planning_functions():
     assert b"stride" in lib.pba_last_error()
 
 
+def test_chunk_plan_whole_row_bands():
+    """pba_plan_chunks rounds a pair's chunk to whole 8-row bands when the
+    strided grid width is a multiple of 16 and 8 rows fit the requested size
+    (K1's 16 x 8 tiled walk, linearize.cu pair_chunk_pixels), else keeps it."""
+    lib = native.load()
+
+    def plan(w, h, chunk, stride=1):
+        cam = native.Camera(1, w, h, 0, 100.0, 100.0, w / 2, h / 2, 0.1, 50.0)
+        pairs = (native.Pair * 1)(native.Pair(0, 1, 0, 1, 0, 0, 0.05))
+        cams = (native.Camera * 1)(cam)
+        n = ctypes.c_int64(0)
+        assert lib.pba_plan_chunks(pairs, 1, cams, stride, chunk, None, None, ctypes.byref(n)) == 0
+        tab = np.zeros(2 * n.value, np.int32)
+        off = np.zeros(2, np.int32)
+        assert lib.pba_plan_chunks(pairs, 1, cams, stride, chunk, tab.ctypes.data,
+                                   off.ctypes.data, ctypes.byref(n)) == 0
+        assert off[-1] == n.value and (tab[0::2] == 0).all()
+        return tab[1::2]
+
+    assert list(plan(1024, 128, 8192)) == [8192 * k for k in range(16)]   # c4: 8 x 1024
+    assert list(plan(640, 480, 8192)) == [10240 * k for k in range(30)]   # c3: 16 x 640
+    assert list(plan(160, 120, 1024)) == [1024 * k for k in range(19)]    # c1: 8 rows > 1024
+    assert list(plan(1000, 64, 8192)) == [8192 * k for k in range(8)]     # width % 16 != 0
+    firsts = plan(48, 100, 4096)                                          # 11 bands of 8 rows
+    assert list(firsts) == [4224 * k for k in range(2)] and 48 * 100 - firsts[-1] == 576
+    assert list(plan(2048, 64, 3072, stride=2)) == [3072 * k for k in range(11)]  # 8 x 1024 > 3072
+
+
+def test_chunk_size_rule():
+    from paper_2303_16878_b200.device import chunk_pixels_for
+
+    # ~32 waves of 444 resident CTAs, 1,024..8,192 pixels; one wave for small problems
+    assert chunk_pixels_for(2_519_907_096) == 8192   # c4
+    assert chunk_pixels_for(47_316_992) == 3328      # c2
+    assert chunk_pixels_for(460_800) == 1024         # c1
+    assert chunk_pixels_for(200_000) == 256          # below one wave of 1,024-pixel chunks
+    assert chunk_pixels_for(10) == 256
+
+
 def test_shard_ranges_balanced_and_contiguous():
     from paper_2303_16878_b200.distributed import shard_ranges
 
@@ -238,6 +277,12 @@ def test_chunk_orders_are_permutations(monkeypatch):
     got = order_chunks(tab.copy(), 6, 100, src, dst, [1, 0, 1]).reshape(-1, 2)
     idx = [int(np.nonzero((tab.reshape(-1, 2) == r).all(1))[0][0]) for r in got]
     assert idx == [2, 3, 4, 0, 5, 1]  # pair 1 (spherical) first; pinhole pairs 0, 2 interleaved
+    # chunk positions are counted inside each pair (pairs may have different chunk sizes)
+    monkeypatch.setenv("PBA_CHUNK_ORDER", "dst")
+    tab2 = np.array([0, 0, 0, 8192, 1, 0, 1, 10240, 1, 20480, 2, 0], np.int32)
+    got = order_chunks(tab2.copy(), 6, 8192, src, dst).reshape(-1, 2)
+    idx = [int(np.nonzero((tab2.reshape(-1, 2) == r).all(1))[0][0]) for r in got]
+    assert idx == [0, 5, 1, 2, 3, 4]
     monkeypatch.setenv("PBA_CHUNK_ORDER", "bogus")
     with pytest.raises(ValueError):
         order_chunks(tab.copy(), 6, 100, src, dst)

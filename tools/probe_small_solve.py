@@ -51,16 +51,5 @@ def main():
 
 
 
-def section_times():
-    """(development) clock64 sections of the small solve from an instrumented build."""
-    import ctypes
-    lib = N.load()
-    out = (ctypes.c_longlong * 8)()
-    if hasattr(lib, "pba_hack_small_times"):
-        lib.pba_hack_small_times(out)
-        print("cycles: stage", out[0], "factor", out[1], "substitute", out[2], "54 barriers", out[3], "54 drcp", out[4])
-
-
 if __name__ == "__main__":
     main()
-    section_times()
