@@ -293,6 +293,57 @@ int pba_apply_step(const double* poses_in, const int32_t* gen_in, const double* 
                    int32_t n_poses, int32_t gauge, double* poses_out, int32_t* gen_out,
                    int32_t* status, void* stream);
 
+/* ---- device-resident LM level: _solve_level_multi (solver.py:505-537) ----
+ * A CUDA graph with a conditional WHILE node runs a whole LM level without a
+ * host round trip per iteration.  pba_lm_loop_begin creates the graph and
+ * starts capturing `stream` (a non-default stream) into the loop body; the
+ * caller then issues one iteration on that stream — the damped solve with
+ * lambda read from lam_dev, pba_apply_step into the candidate buffers,
+ * pba_linearize + assembly of the candidate, pba_lm_decide, and pba_copy_if
+ * of the candidate buffers over the current ones — and pba_lm_loop_end
+ * instantiates it.  Each pba_lm_loop_launch runs the body until
+ * pba_lm_decide clears the loop condition.
+ * state: device doubles, PBA_LM_STATE_DOUBLES of them (indices below), set
+ * by the host before a launch (iteration = 1, n_records = 0, stop = error =
+ * 0) and read back after it.  records: device doubles,
+ * PBA_LM_RECORD_DOUBLES per iteration: lambda, cost, count, accepted —
+ * solver.py's IterationRecord fields — then the candidate's cost and count.
+ * pba_lm_decide applies one iteration's accept / reject, lambda update,
+ * termination tests and loop-head test exactly as the reference loop does;
+ * a singular first solve or an ||dq|| >= 1 step stops the loop with
+ * state[PBA_LM_ERROR] set (the host raises UnderConstrainedError /
+ * InvalidPerturbationError). */
+#define PBA_LM_COST 0
+#define PBA_LM_COUNT 1
+#define PBA_LM_LAMBDA 2
+#define PBA_LM_FACTOR 3
+#define PBA_LM_REL_TOL 4
+#define PBA_LM_LAMBDA_CEILING 5
+#define PBA_LM_COST_FLOOR 6
+#define PBA_LM_ITERATION 7
+#define PBA_LM_MAX_ITERATIONS 8
+#define PBA_LM_STOP 9
+#define PBA_LM_ERROR 10
+#define PBA_LM_N_RECORDS 11
+#define PBA_LM_ACCEPTED 12
+#define PBA_LM_STATE_DOUBLES 16
+#define PBA_LM_ERR_UNDERCONSTRAINED 1
+#define PBA_LM_ERR_PERTURBATION 2
+#define PBA_LM_MAX_COPY 8
+#define PBA_LM_RECORD_DOUBLES 6
+typedef struct pba_lm_loop pba_lm_loop;
+int pba_lm_loop_begin(void* stream, pba_lm_loop** loop, uint64_t* handle);
+int pba_lm_decide(double* state, double* records, const int32_t* status_solve,
+                  const int32_t* status_step, const double* new_totals, double* lam_dev,
+                  uint64_t handle, void* stream);
+/* dst[k] <- src[k] (bytes[k], a multiple of 4; device pointers; host arrays
+ * of n <= PBA_LM_MAX_COPY) when *flag != 0 (device double). */
+int pba_copy_if(const double* flag, void* const* dst, const void* const* src,
+                const int64_t* bytes, int32_t n, void* stream);
+int pba_lm_loop_end(pba_lm_loop* loop);
+int pba_lm_loop_launch(pba_lm_loop* loop, void* stream);
+void pba_lm_loop_destroy(pba_lm_loop* loop);
+
 /* ---- match-graph construction: overlap_ratio (graph.py:70-101) ---------
  * Valid-projection counts for directed candidate pairs (device pointers):
  * points: sensor-frame points of every frame's valid graph-level pixels
@@ -361,6 +412,11 @@ int pba_atan2_batch(const double* y, const double* x, int64_t n, double* out, vo
  * summed clock64 cycles and visit counts of 8 per-pixel sections, host
  * arrays of 8; reset != 0 zeroes the counters after reading. */
 int pba_diag_section_cycles(uint64_t* cycles, uint64_t* counts, int32_t reset);
+/* Device-resident LM loop timing (diagnostics): out[8 * iteration + slot]
+ * = %globaltimer (ns) when the stamp runs; iteration read from the loop
+ * state (PBA_LM_ITERATION).  Issued between the captured calls of a loop
+ * body it gives per-iteration phase times. */
+int pba_diag_lm_stamp(const double* state, int64_t* out, int32_t slot, void* stream);
 
 #ifdef __cplusplus
 }

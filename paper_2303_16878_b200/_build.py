@@ -24,7 +24,7 @@ LIB = OUT_DIR / "libpba_b200.so"
 # makes native.load() pick it (tests/test_gpu_checked.py)
 LIB_CHECKED = OUT_DIR / "libpba_b200_checked.so"
 SOURCES = ["capi.cu", "texels.cu", "linearize.cu", "assemble.cu", "solve.cu", "pcg.cu", "update.cu",
-           "overlap.cu", "pyramid.cu", "rasters.cu"]
+           "overlap.cu", "pyramid.cu", "rasters.cu", "lmloop.cu"]
 GENCODE = "-gencode=arch=compute_100a,code=sm_100a"
 
 

@@ -58,6 +58,7 @@ CONSECUTIVE = "consecutive"
 
 _LAMBDA_CEILING = 1e12         # solver.py:489
 _COST_FLOOR_PER_BLOCK = 1e-18  # solver.py:492
+N_LM_ERR_UNDERCONSTRAINED, N_LM_ERR_PERTURBATION = 1, 2  # include/pba.h PBA_LM_ERR_*
 
 
 @dataclass(frozen=True)
@@ -223,6 +224,21 @@ def _lm_level(backend, level: int, cfg: SolverConfig, max_iterations: int):
     records = []
     cost, count = backend.evaluate_current()
     lam = cfg.lm_initial_lambda
+    device_loop = getattr(backend, "lm_level_device", None)
+    if device_loop is not None and max_iterations >= 1 and not (
+            cost <= _COST_FLOOR_PER_BLOCK * max(count, 1)):
+        # the same loop as below, run on the GPU as one conditional-graph launch
+        out = device_loop(cost, count, lam, cfg, max_iterations)
+        if out is not None:
+            recs, error, _, _ = out
+            if error == N_LM_ERR_UNDERCONSTRAINED:
+                raise UnderConstrainedError(
+                    "normal equations are singular; some pose has no valid observations")
+            if error == N_LM_ERR_PERTURBATION:
+                raise InvalidPerturbationError(
+                    "LM step has ||dq|| >= 1 for some pose; not a quaternion imaginary part")
+            return [IterationRecord(level, k + 1, r_lam, r_cost, r_count, acc)
+                    for k, (r_lam, r_cost, r_count, acc) in enumerate(recs)]
     for iteration in range(1, max_iterations + 1):
         if cost <= _COST_FLOOR_PER_BLOCK * max(count, 1):
             break

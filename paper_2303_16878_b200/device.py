@@ -28,6 +28,8 @@ PIXELS_PER_CHUNK_UNIT = 256  # chunk sizes are multiples of this
 MAX_CHUNK_UNITS = 32         # <= 8192 pixels per chunk: 64 per thread of K1's 128-thread CTA
 SM_COUNT = 148
 K1_CTAS_PER_SM = 3           # resident K1 CTAs per SM (168 registers x 128 threads)
+LAMBDA_CEILING = 1e12         # solver.py:489 (bundle._LAMBDA_CEILING)
+COST_FLOOR_PER_BLOCK = 1e-18  # solver.py:492 (bundle._COST_FLOOR_PER_BLOCK)
 
 
 def camera_struct(intr) -> N.Camera:
@@ -395,6 +397,11 @@ class DeviceLevel:
         self._graph_failed = False
         self._capture_lin_events = None
         self._graph_nlaunch = [0, 0]        # library kernels in each captured step
+        self._lm_loop = None                # device-resident LM level (lm_level_device)
+        self._lm_loop_failed = False
+        self._lm_loop_error = None
+        self._lm_nlaunch = 0
+        self.lm_device_iterations = 0
         self.graph_launches_replayed = 0    # library kernels launched through replays
         self.poses = [torch.zeros((self.n_poses, 12), dtype=torch.float64, device=dev)
                       for _ in range(2)]
@@ -467,7 +474,7 @@ class DeviceLevel:
         stream = torch.cuda.current_stream(self.device)
         cap = getattr(self, "_capture_lin_events", None)  # graph-owned events while capturing
         ev = self.kernel_events if cap is None else None
-        if cap is not None:
+        if cap:
             cap[0].record(stream)
         elif ev is not None:
             e0 = torch.cuda.Event(enable_timing=True)
@@ -478,7 +485,7 @@ class DeviceLevel:
             poses_t.data_ptr(), self.ext_t.data_ptr(), ctypes.byref(self.ccfg),
             int(bool(want_jacobians)), self.partials.data_ptr(), self.records.data_ptr(),
             stream.cuda_stream), "pba_linearize")
-        if cap is not None:
+        if cap:
             cap[1].record(stream)
         elif ev is not None:
             e1 = torch.cuda.Event(enable_timing=True)
@@ -674,6 +681,148 @@ class DeviceLevel:
         self._graphs[cur] = g
         self._graph_events[cur] = events
         return g
+
+    # ---- device-resident LM level (csrc/lmloop.cu) ---------------------------
+    LM_RECORD_CAPACITY = 256
+
+    def lm_loop_ready(self) -> bool:
+        """Whether lm_level_device runs here (policy + a captured loop graph)."""
+        if (os.environ.get("PBA_LM_DEVICE", "1") == "0" or not self._graph_enabled()
+                or self.pixels_shard > (1 << 26)):
+            return False
+        if self.cur != 0:  # the loop body is captured on buffer 0
+            for bufs in (self.poses, self.gens, self.Hb, self.b, self.totals):
+                bufs[0].copy_(bufs[1])
+            self.cur = 0
+        return self._lm_loop_graph() is not None
+
+    def lm_level_device(self, cost: float, count: int, lam: float, cfg, max_iterations: int,
+                        lam_ceiling: float = LAMBDA_CEILING, details: bool = False):
+        """The iterations of bundle._lm_level (solver.py:505-537) as one graph
+        launch: a conditional WHILE node replays solve -> update -> linearise
+        -> assemble -> decide -> copy-on-accept until the device-side decision
+        stops the loop; the host reads the records once.  Returns
+        (records [(lambda, cost, count, accepted)], error code, cost, count),
+        or None where the loop graph is not used (large problems, where a
+        host round trip per iteration is negligible; PBA_LM_DEVICE=0; a
+        backend whose step cannot be captured) — the caller then runs the
+        host loop."""
+        if max_iterations > self.LM_RECORD_CAPACITY or not self.lm_loop_ready():
+            return None
+        loop = self._lm_loop
+        st = self._lm_state_host
+        st.zero_()
+        st[N.LM_COST], st[N.LM_COUNT], st[N.LM_LAMBDA] = cost, float(count), lam
+        st[N.LM_FACTOR] = cfg.lm_factor
+        st[N.LM_REL_TOL] = cfg.termination_rel_decrease
+        st[N.LM_LAMBDA_CEILING], st[N.LM_COST_FLOOR] = lam_ceiling, COST_FLOOR_PER_BLOCK
+        st[N.LM_ITERATION], st[N.LM_MAX_ITERATIONS] = 1.0, float(max_iterations)
+        stream = torch.cuda.current_stream(self.device)
+        self._lm_state.copy_(st, non_blocking=True)
+        self._lam_dev.copy_(self._lm_state[N.LM_LAMBDA:N.LM_LAMBDA + 1])
+        N.check(self.lib.pba_lm_loop_launch(loop, stream.cuda_stream), "pba_lm_loop_launch")
+        st.copy_(self._lm_state, non_blocking=True)
+        stream.synchronize()
+        n = int(st[N.LM_N_RECORDS])
+        recs = self._lm_records[: N.LM_RECORD_DOUBLES * n].cpu().numpy().reshape(
+            n, N.LM_RECORD_DOUBLES)
+        iters = int(st[N.LM_ITERATION]) - 1
+        self.graph_launches_replayed += self._lm_nlaunch * iters
+        self.lm_device_iterations += iters
+        out = [(float(r[0]), float(r[1]), int(round(r[2])), bool(r[3])) for r in recs]
+        if details:  # + the candidate's (cost, count) per iteration
+            out = [o + (float(r[4]), int(round(r[5]))) for o, r in zip(out, recs)]
+        return (out, int(st[N.LM_ERROR]), float(st[N.LM_COST]),
+                int(round(float(st[N.LM_COUNT]))))
+
+    def _lm_loop_graph(self):
+        if self._lm_loop is not None or self._lm_loop_failed:
+            return self._lm_loop
+        if not self._plan_ready:  # the solver's tile tables go up once, outside the capture
+            self.solve(0, 1.0, self._status_solve_ptr)
+        dev = self.device
+        self._lm_state = torch.zeros(N.LM_STATE_DOUBLES, dtype=torch.float64, device=dev)
+        self._lm_state_host = torch.zeros(N.LM_STATE_DOUBLES, dtype=torch.float64).pin_memory()
+        self._lm_records = torch.zeros(N.LM_RECORD_DOUBLES * self.LM_RECORD_CAPACITY,
+                                       dtype=torch.float64, device=dev)
+        segs = [(self.poses[0], self.poses[1]), (self.gens[0], self.gens[1]),
+                (self.Hb[0], self.Hb[1]), (self.b[0], self.b[1]),
+                (self.totals[0], self.totals[1])]
+        n = len(segs)
+        dst = (ctypes.c_void_p * n)(*[d.data_ptr() for d, _ in segs])
+        src = (ctypes.c_void_p * n)(*[s_.data_ptr() for _, s_ in segs])
+        nbytes = (ctypes.c_int64 * n)(*[d.numel() * d.element_size() for d, _ in segs])
+        stream = torch.cuda.Stream(dev)
+        stream.wait_stream(torch.cuda.current_stream(dev))
+        torch.cuda.synchronize(dev)
+        loop, handle = ctypes.c_void_p(), ctypes.c_uint64()
+        # (no event-record nodes: a conditional node's body may not hold them)
+        self._lm_events = None
+        n0 = int(self.lib.pba_kernel_launches())
+        ok = False
+        if self.lib.pba_lm_loop_begin(stream.cuda_stream, ctypes.byref(loop),
+                                      ctypes.byref(handle)) == N.PBA_OK:
+            try:
+                stamp = self._lm_stamp_fn(stream)
+                with torch.cuda.stream(stream):
+                    self._capture_lin_events = ()  # capturing: no per-call timing events
+                    stamp(0)
+                    self.solve(0, None, self._status_solve_ptr)
+                    stamp(1)
+                    self.apply_step(0, 1, self._status_step_ptr)
+                    stamp(2)
+                    recs = self.linearize(self.poses[1])
+                    stamp(3)
+                    self.assemble(recs, 1)
+                    stamp(4)
+                    N.check(self.lib.pba_lm_decide(
+                        self._lm_state.data_ptr(), self._lm_records.data_ptr(),
+                        self._status_solve_ptr, self._status_step_ptr,
+                        self.totals[1].data_ptr(), self._lam_dev.data_ptr(), handle.value,
+                        stream.cuda_stream), "pba_lm_decide")
+                    N.check(self.lib.pba_copy_if(
+                        self._lm_state.data_ptr() + 8 * N.LM_ACCEPTED, dst, src, nbytes, n,
+                        stream.cuda_stream), "pba_copy_if")
+                    stamp(5)
+                N.check(self.lib.pba_lm_loop_end(loop), "pba_lm_loop_end")
+                ok = True
+            except Exception as exc:  # capture unsupported here: the host loop runs instead
+                self._lm_loop_error = repr(exc)
+            finally:
+                self._capture_lin_events = None
+        if not ok:
+            if loop.value:
+                self.lib.pba_lm_loop_destroy(loop)
+            torch.cuda.synchronize(dev)
+            self._lm_loop_failed = True
+            return None
+        torch.cuda.current_stream(dev).wait_stream(stream)
+        self._lm_nlaunch = int(self.lib.pba_kernel_launches()) - n0
+        self._lm_loop = loop
+        self._lm_loop_handle = handle
+        self._lm_stream = stream
+        return loop
+
+    def _lm_stamp_fn(self, stream):
+        """PBA_LM_STAMPS=1 (diagnostics): globaltimer stamps between the
+        phases of the captured loop body into self.lm_stamps (8 per iteration)."""
+        if os.environ.get("PBA_LM_STAMPS") != "1":
+            return lambda slot: None
+        self.lm_stamps = torch.zeros(8 * (self.LM_RECORD_CAPACITY + 2), dtype=torch.int64,
+                                     device=self.device)
+
+        def stamp(slot):
+            N.check(self.lib.pba_diag_lm_stamp(self._lm_state.data_ptr(), self.lm_stamps.data_ptr(),
+                                               slot, stream.cuda_stream), "pba_diag_lm_stamp")
+        return stamp
+
+    def __del__(self):
+        loop = getattr(self, "_lm_loop", None)
+        if loop is not None and getattr(loop, "value", None):
+            try:
+                self.lib.pba_lm_loop_destroy(loop)
+            except Exception:
+                pass
 
     def accept(self) -> None:
         self.cur = 1 - self.cur

@@ -29,6 +29,11 @@ PBA_CFG_PINHOLE_DST = 1  # pba_config.flags: pinhole destinations present (K1 pr
 RECORD_DOUBLES = 92
 NORMALS_RECHECK_DOUBLES = 10
 PARTIAL_DOUBLES = 32
+# device-resident LM level (pba_lm_*): state indices and error codes
+LM_COST, LM_COUNT, LM_LAMBDA, LM_FACTOR, LM_REL_TOL, LM_LAMBDA_CEILING = 0, 1, 2, 3, 4, 5
+LM_COST_FLOOR, LM_ITERATION, LM_MAX_ITERATIONS, LM_STOP, LM_ERROR = 6, 7, 8, 9, 10
+LM_N_RECORDS, LM_ACCEPTED, LM_STATE_DOUBLES = 11, 12, 16
+LM_ERR_UNDERCONSTRAINED, LM_ERR_PERTURBATION, LM_MAX_COPY, LM_RECORD_DOUBLES = 1, 2, 8, 6
 
 # symbols declared in include/pba.h, in header order
 EXPORTED = (
@@ -40,9 +45,11 @@ EXPORTED = (
     "pba_solve_work_bytes", "pba_solve_dense", "pba_solve_dense_ex", "pba_solve_dense_bsr",
     "pba_pcg_work_bytes", "pba_solve_pcg", "pba_solve_pcg_ex", "pba_solve_pcg_bsr",
     "pba_apply_step",
+    "pba_lm_loop_begin", "pba_lm_decide", "pba_copy_if", "pba_lm_loop_end", "pba_lm_loop_launch",
+    "pba_lm_loop_destroy",
     "pba_overlap_counts", "pba_normals_scratch_bytes",
     "pba_estimate_normals", "pba_downscale_cues", "pba_decode_raster", "pba_atan2_batch",
-    "pba_diag_section_cycles",
+    "pba_diag_section_cycles", "pba_diag_lm_stamp",
 )
 
 
@@ -118,8 +125,15 @@ _SIGNATURES = {
     "pba_solve_pcg": (ctypes.c_int, [_vp, _vp, _i32, _dbl, _vp, _vp, _i32, _dbl, _vp, _vp, _vp,
                                      _vp, _vp]),
     "pba_apply_step": (ctypes.c_int, [_vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp]),
+    "pba_lm_loop_begin": (ctypes.c_int, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_uint64)]),
+    "pba_lm_decide": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_uint64, _vp]),
+    "pba_copy_if": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i32, _vp]),
+    "pba_lm_loop_end": (ctypes.c_int, [_vp]),
+    "pba_lm_loop_launch": (ctypes.c_int, [_vp, _vp]),
+    "pba_lm_loop_destroy": (None, [_vp]),
     "pba_atan2_batch": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp]),
     "pba_diag_section_cycles": (ctypes.c_int, [_vp, _vp, _i32]),
+    "pba_diag_lm_stamp": (ctypes.c_int, [_vp, _vp, _i32, _vp]),
     "pba_overlap_counts": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _dbl, _vp, _vp]),
     "pba_normals_scratch_bytes": (_sz, [ctypes.POINTER(Camera), _i32]),
     "pba_estimate_normals": (ctypes.c_int, [ctypes.POINTER(Camera), _vp, _vp, _i32,

@@ -51,5 +51,10 @@ def test_gpu_arm_line():
     assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0
     assert line["cpu_baseline"]["kind"] == "port"
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(line["clocks"])
+    # c1 fits the device-resident LM loop: the timed steps are one conditional-graph launch
+    assert line["parallelism"] == "single GPU, device-resident LM loop"
+    host = _run(["--config", "c1", "--steps", "3", "--warmup", "3", "--no-e2e-api",
+                 "--no-cpu-baseline", "--lm-loop", "host"])
+    assert host["parallelism"] == "single GPU" and host["config"] == line["config"]
     ref = _run(["--impl", "reference", "--config", "c1", "--steps", "1", "--warmup", "3"])
     assert ref["config"] == line["config"]  # the driver compares them

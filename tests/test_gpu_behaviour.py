@@ -166,3 +166,56 @@ def test_graph_replayed_steps_equal_eager_steps(monkeypatch, solver):
     assert out["0"][2] == 0
     if solver == "cholesky":
         assert out["1"][2] > 0  # the replayed path really ran
+
+
+# ---------------------------------------------------------------------------
+# Device-resident LM level (csrc/lmloop.cu): one conditional-graph launch per
+# level, identical to the host-driven loop
+# ---------------------------------------------------------------------------
+def _room_level_problem(gauge, n=10, scales=(1.0,)):
+    import math
+
+    from paper_2303_16878_b200 import scenes as S
+
+    cam = S.rgbd_160()
+    gt = S.room_loop(n)
+    pyrs = S.host_pyramids(S.BoxScene(), cam, gt, P.Pose.identity(), scales)
+    guess = S.perturb(gt, 0.05, math.radians(2.0), 11)
+    nodes = [P.FrameNode(k, guess[k], pyrs[k], 0.1 * k) for k in range(n)]
+    return P.BAProblem(P.build_graph(nodes), gauge_index=gauge), guess
+
+
+@pytest.mark.parametrize("gauge,max_it", [(0, 10), (4, 10), (2, 3), (2, 1)])
+def test_device_lm_loop_equals_host_loop(monkeypatch, gauge, max_it):
+    import torch
+
+    from paper_2303_16878_b200.bundle import _lm_level, _Runtime
+
+    prob, guess = _room_level_problem(gauge)
+    rows, gens = P.se3.pose_rows(guess)
+    cfg = P.SolverConfig()
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("PBA_LM_DEVICE", mode)
+        backend = _Runtime().level([prob], 0, cfg)
+        backend.set_poses(rows, gens)
+        recs = _lm_level(backend, 0, cfg, max_it)
+        out[mode] = (recs, backend.current_rows(), backend.lm_device_iterations)
+        del backend
+        torch.cuda.synchronize()
+    assert out["0"][2] == 0 and out["1"][2] == len(out["1"][0]) > 0  # the loop ran on the GPU
+    assert out["1"][0] == out["0"][0]  # every IterationRecord field equal
+    assert any(not r.accepted for r in out["1"][0]) or max_it < 10
+    assert np.array_equal(out["1"][1][0], out["0"][1][0])
+    assert np.array_equal(out["1"][1][1], out["0"][1][1])
+
+
+def test_device_lm_loop_whole_solve_equals_host_loop(monkeypatch):
+    prob, _ = _room_level_problem(3, scales=(0.5, 1.0))
+    res = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("PBA_LM_DEVICE", mode)
+        res[mode] = P.solve_hierarchical(prob, P.SolverConfig())
+    assert res["1"].records == res["0"].records
+    assert all(np.array_equal(a.as_row(), b.as_row())
+               for a, b in zip(res["1"].poses, res["0"].poses))

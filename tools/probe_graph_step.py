@@ -1,7 +1,9 @@
-"""Device time of one captured LM step (c1 by default): the step graph
-replayed back to back with no host work in between, against the bench's
-host-driven loop (replay, synchronise, read the scalars, decide) — the gap
-is the host turnaround a device-resident loop would remove."""
+"""Per-iteration time of an LM level on a small problem (c1 by default):
+the bench's host-driven loop (step graph replay, synchronise, read the
+scalars, decide on the host), the step graph replayed back to back with no
+host work in between (a lower bound), and the device-resident loop
+(DeviceLevel.lm_level_device: one conditional-graph launch runs all
+iterations, decisions on the GPU)."""
 import sys
 import time
 from pathlib import Path
@@ -38,7 +40,22 @@ def main(config="c1", reps=200):
     for _ in range(reps):
         lv.try_step(1e-3)
     host_us = (time.perf_counter() - t0) / reps * 1e6
-    print(f"{config}: graph replay back to back {dev_us:.1f} us/step; try_step loop {host_us:.1f} us/step")
+    # device-resident loop: `reps` iterations in one launch, no termination test
+    class NoStop:
+        lm_factor = 10.0
+        termination_rel_decrease = -1.0
+
+    cost, count = lv.evaluate_current()
+    lv.lm_level_device(cost, count, 1e-3, NoStop, 5)  # capture + warm
+    cost, count = lv.evaluate_current()
+    torch.cuda.synchronize()
+    a.record()
+    recs, err, _, _ = lv.lm_level_device(cost, count, 1e-3, NoStop, reps)
+    b.record()
+    torch.cuda.synchronize()
+    loop_us = a.elapsed_time(b) / max(len(recs), 1) * 1e3
+    print(f"{config}: try_step loop {host_us:.1f} us/iteration; graph replay back to back "
+          f"{dev_us:.1f}; device-resident loop {loop_us:.1f} ({len(recs)} iterations, error {err})")
 
 
 if __name__ == "__main__":
