@@ -643,7 +643,6 @@ class DeviceLevel:
                     self._capture_step(c)
 
     def _graph_enabled(self) -> bool:
-    
         return (self.has_solver and not self._graph_failed
                 and os.environ.get("PBA_GRAPH", "1") != "0")
 
