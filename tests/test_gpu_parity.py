@@ -711,6 +711,40 @@ def test_chunk_launch_order_does_not_change_records(monkeypatch):
         assert np.array_equal(out["pair"], out[order]), order
 
 
+@pytest.mark.parametrize("model", ["pinhole", "spherical"])
+def test_tiled_walk_and_partial_bands_match_oracle(monkeypatch, model):
+    """Chunks of whole 8-row bands walked in 16 x 8 tiles (linearize.cu
+    pair_chunk_pixels), here 16-row bands of a 100-row image so each pair
+    also ends in a partial 4-row band walked row-major: records within the
+    §8(c) bar of the oracle, and equal to the all-row-major chunking up to
+    summation order (counts exactly)."""
+    from paper_2303_16878_b200 import scenes as S
+
+    if model == "pinhole":
+        cam = P.Intrinsics(120.0, 120.0, 79.5, 49.5, 160, 100, P.PINHOLE, 0.1, 50.0)
+        prob, gt, guess = _room_problem(n=4, cam=cam)
+    else:
+        cam = S.hdl64(256, 100)
+        gt = S.corridor_trajectory(4, 0.5)
+        pyrs = S.host_pyramids(S.corridor_scene(20.0), cam, gt, P.Pose.identity(), (1.0,))
+        guess = S.perturb(gt, 0.05, math.radians(2.0), 11)
+        nodes = [P.FrameNode(k, guess[k], pyrs[k], 0.1 * k) for k in range(len(gt))]
+        prob = P.BAProblem(P.build_graph(nodes))
+    rows, _ = P.se3.pose_rows(guess)
+    width = cam.width
+    monkeypatch.setenv("PBA_CHUNK_UNITS", str(16 * width // 256))  # 16-row bands
+    lv = _level([prob], 0)
+    assert lv.chunk_pixels == 16 * width
+    tiled = lv.linearize(_rows(rows)).cpu().numpy()
+    ref = O.OracleLevel([prob], 0, P.SolverConfig()).records(rows)
+    F.compare_records(tiled, ref)
+    monkeypatch.setenv("PBA_CHUNK_UNITS", "1")  # 256-pixel chunks: row-major everywhere
+    flat = _level([prob], 0).linearize(_rows(rows)).cpu().numpy()
+    assert np.array_equal(tiled[:, 91], flat[:, 91])
+    np.testing.assert_allclose(tiled[:, :91], flat[:, :91], rtol=1e-11,
+                               atol=1e-11 * np.abs(flat[:, :91]).max())
+
+
 @pytest.mark.parametrize("config,frames", [("c3", 4), ("c5", 3)])
 def test_bench_shapes_records_and_trace_match_oracle(config, frames):
     """The other bench sensor shapes at full resolution against the oracle:
