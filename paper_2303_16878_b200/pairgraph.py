@@ -20,7 +20,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .camera import SensorExtrinsics, project, unproject
+from .camera import PINHOLE, SensorExtrinsics, project, ray_factors, unproject
 from .se3 import Pose, rotation_angle
 
 COVISIBILITY = "covisibility"
@@ -89,6 +89,60 @@ def _source_points(src, stride: int, cache: dict | None):
     if cache is not None:
         cache[key] = (n_valid, pts, src)
     return n_valid, pts, src
+
+
+def _prime_source_points(srcs, stride: int, cache: dict) -> None:
+    """_source_points of many frames at once, into `cache`, with the same
+    results: frames of one camera share the strided pixel grid and its rays
+    (elementwise (u - c)/f, cos and sin, so a ray is the same double whether
+    computed for the grid or for a frame's valid subset), each frame's points
+    are ray * depth exactly as unproject forms them (sensors.py:133-154), and
+    device-resident depth images come back in one transfer per camera
+    instead of two per frame."""
+    groups: dict = {}
+    for src in srcs:
+        if (id(src), stride) in cache:
+            continue
+        cam = src.intrinsics
+        key = (cam.model, cam.width, cam.height, cam.fx, cam.fy, cam.cx, cam.cy, cam.depth_min,
+               cam.depth_max, tuple(src.shape))
+        groups.setdefault(key, []).append(src)
+    for group in groups.values():
+        cam = group[0].intrinsics
+        h, w = group[0].shape
+        on_device = [s for s in group if getattr(s, "device_depth", None) is not None
+                     and getattr(s, "_host", None) is None]
+        depth_of = {}
+        if on_device:
+            import torch
+
+            raw = torch.stack([s.device_depth[::stride, ::stride] for s in on_device]).cpu().numpy()
+            for s, d in zip(on_device, raw):
+                d = np.asarray(d, dtype=float)
+                with np.errstate(invalid="ignore"):
+                    ok = (d >= cam.depth_min) & (d <= cam.depth_max) & (d > 0)  # depth_valid
+                depth_of[id(s)] = (ok, d)
+        for s in group:
+            if id(s) not in depth_of:
+                depth_of[id(s)] = (np.asarray(s.depth_valid)[::stride, ::stride],
+                                   np.asarray(s.depth)[::stride, ::stride])
+        cols, rows = np.meshgrid(np.arange(0, w, stride, dtype=float),
+                                 np.arange(0, h, stride, dtype=float))
+        a, e = ray_factors(cam, cols, rows)
+        if cam.model == PINHOLE:
+            rx, ry, rz = a, e, None
+        else:
+            ce = np.cos(e)
+            rx, ry, rz = ce * np.cos(a), ce * np.sin(a), np.sin(e)
+        for s in group:
+            valid, d = depth_of[id(s)]
+            n_valid = int(valid.sum())
+            pts = None
+            if n_valid:
+                dv = np.asarray(d, dtype=float)[valid]
+                pts = np.stack([rx[valid] * dv, ry[valid] * dv,
+                                dv if rz is None else rz[valid] * dv], axis=-1)
+            cache[(id(s), stride)] = (n_valid, pts, s)
 
 
 def overlap_ratio(node_i: FrameNode, node_j: FrameNode, level: int = 0, stride: int = 1,
@@ -275,8 +329,8 @@ def build_graph(nodes, criteria: MatchCriteria | None = None, sequential: bool =
                 f"(frame {b.id} at {b.timestamp} after {a.timestamp})")
     candidates = _prefilter(nodes, crit)
     cache: dict = {}
-    for nd in nodes:  # per-frame source points, shared by every pair of the frame
-        _source_points(nd.pyramid.levels[overlap_level], overlap_stride, cache)
+    # per-frame source points, shared by every pair of the frame
+    _prime_source_points([nd.pyramid.levels[overlap_level] for nd in nodes], overlap_stride, cache)
 
     def check(ab):
         a, b = ab

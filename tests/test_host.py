@@ -288,6 +288,25 @@ def test_chunk_orders_are_permutations(monkeypatch):
         order_chunks(tab.copy(), 6, 100, src, dst)
 
 
+def test_batched_source_points_equal_per_frame():
+    """pairgraph._prime_source_points (all frames of a camera at once) gives
+    the per-frame _source_points arrays bit for bit."""
+    from paper_2303_16878_b200 import pairgraph as G
+    from tests import fixtures as F
+
+    for name in ("pinhole_small", "spherical_small"):
+        srcs = [lv for p in F.pyramids(F.load(name)) for lv in p.levels]
+        for stride in (1, 2, 3):
+            one, many = {}, {}
+            for s in srcs:
+                G._source_points(s, stride, one)
+            G._prime_source_points(srcs, stride, many)
+            assert one.keys() == many.keys()
+            for k, (n, pts, _) in one.items():
+                assert many[k][0] == n
+                assert (pts is None and many[k][1] is None) or np.array_equal(pts, many[k][1])
+
+
 def test_bulk_graph_gates_and_transforms_match_scalar_path():
     """The bulk helpers of the device graph build (pairgraph._gated,
     _relative_rows) decide exactly like the per-pair reference path and give
