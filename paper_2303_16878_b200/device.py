@@ -306,10 +306,18 @@ class DeviceLevel:
         self.pose_j = np.array([c[1] for c in ctxs], dtype=np.int32)
         # chunk size from the whole level (shard-independent)
         stride = int(cfg.pixel_stride)
-        total_px = 0
-        for c in ctxs:
-            intr = c[2].pyramid.levels[level].intrinsics
-            total_px += math.ceil(intr.width / stride) * math.ceil(intr.height / stride)
+        px_of_node: dict = {}  # strided source-grid size per source node
+
+        def grid_px(node):
+            v = px_of_node.get(id(node))
+            if v is None:
+                intr = node.pyramid.levels[level].intrinsics
+                v = px_of_node[id(node)] = (math.ceil(intr.width / stride)
+                                            * math.ceil(intr.height / stride))
+            return v
+
+        pair_px = np.array([grid_px(c[2]) for c in ctxs], dtype=np.int64)
+        total_px = int(pair_px.sum())
         self.total_pixels = total_px
         self.chunk_pixels = chunk_pixels_for(total_px)
         lo, hi = (0, len(ctxs)) if pair_range is None else pair_range
@@ -318,19 +326,21 @@ class DeviceLevel:
         self.n_pairs = len(mine)
         # frame / extrinsics tables for this shard
         store.prefetch([node.pyramid.levels[level] for c in mine for node in (c[2], c[3])])
-        frames, frame_slot, ext_rows, ext_slot, ext_of = [], {}, [], {}, {}
-        idx = np.zeros((max(1, self.n_pairs), 5), dtype=np.int32)  # pose_i, pose_j, src, dst, ext
-        tols = np.zeros(max(1, self.n_pairs))
-        for k, (pi, pj, ni, nj, ext, tol) in enumerate(mine):
-            slots = []
-            for node in (ni, nj):
+        frames, frame_slot, node_slot, ext_rows, ext_slot, ext_of = [], {}, {}, [], {}, {}
+
+        def slot_of(node):  # frame table slot of a node's level image
+            s_ = node_slot.get(id(node))
+            if s_ is None:
                 cue = node.pyramid.levels[level]
                 s_ = frame_slot.get(id(cue))
                 if s_ is None:
                     tex, mask, ray, cam = store.frame(cue)
                     s_ = frame_slot[id(cue)] = len(frames)
                     frames.append(N.Frame(tex.data_ptr(), mask.data_ptr(), ray.data_ptr(), cam))
-                slots.append(s_)
+                node_slot[id(node)] = s_
+            return s_
+
+        def ext_of_pair(ext):
             e_ = ext_of.get(id(ext))
             if e_ is None:
                 off = ext.offset
@@ -341,8 +351,15 @@ class DeviceLevel:
                     ext_rows.append(np.concatenate([np.asarray(off.rotation, float).reshape(9),
                                                     np.asarray(off.translation, float).reshape(3)]))
                 e_ = ext_of[id(ext)] = ext_slot[ekey]
-            idx[k] = (pi, pj, slots[0], slots[1], e_)
-            tols[k] = tol
+            return e_
+
+        idx = np.zeros((max(1, self.n_pairs), 5), dtype=np.int32)  # pose_i, pose_j, src, dst, ext
+        tols = np.zeros(max(1, self.n_pairs))
+        if mine:
+            idx[: self.n_pairs] = np.array(
+                [(c[0], c[1], slot_of(c[2]), slot_of(c[3]), ext_of_pair(c[4])) for c in mine],
+                dtype=np.int32)
+            tols[: self.n_pairs] = [c[5] for c in mine]
         # the pba_pair / pba_camera tables built in one go (32 B / 64 B records)
         pair_rec = np.zeros(max(1, self.n_pairs), dtype=[("i", "<i4", 6), ("tol", "<f8")])
         pair_rec["i"][:, :5] = idx
@@ -380,9 +397,7 @@ class DeviceLevel:
             dtype=torch.uint8, device=dev)
         self.records = torch.zeros((max(1, self.n_pairs), N.RECORD_DOUBLES), dtype=torch.float64,
                                    device=dev)
-        self.pixels_shard = sum(
-            math.ceil(c[2].pyramid.levels[level].intrinsics.width / stride)
-            * math.ceil(c[2].pyramid.levels[level].intrinsics.height / stride) for c in mine)
+        self.pixels_shard = int(pair_px[lo:hi].sum())
         self._scal = torch.zeros(8, dtype=torch.float64, device=dev)
         self._scal_host = torch.zeros(8, dtype=torch.float64).pin_memory()
         # LM damping read by the solve kernels from device memory, so one

@@ -44,9 +44,18 @@ def main():
                           extrinsics=sext, device=dev)
         torch.cuda.synchronize()
         t2 = time.perf_counter()
+        if rep == 1 and "--profile" in sys.argv:
+            import cProfile
+            import pstats
+
+            pr = cProfile.Profile()
+            pr.enable()
         P.solve_hierarchical(P.BAProblem(g, {"sensor0": sext}))
         torch.cuda.synchronize()
         t3 = time.perf_counter()
+        if rep == 1 and "--profile" in sys.argv:
+            pr.disable()
+            pstats.Stats(pr).sort_stats("tottime").print_stats(25)
         print(f"rep {rep}: pyramids {t1 - t0:.3f} s, graph {t2 - t1:.3f} s, "
               f"solve {t3 - t2:.3f} s, total {t3 - t0:.3f} s")
 
