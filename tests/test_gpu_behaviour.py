@@ -219,3 +219,25 @@ def test_device_lm_loop_whole_solve_equals_host_loop(monkeypatch):
     assert res["1"].records == res["0"].records
     assert all(np.array_equal(a.as_row(), b.as_row())
                for a, b in zip(res["1"].poses, res["0"].poses))
+
+
+def test_device_lm_loop_with_pcg_matches_host_loop(monkeypatch):
+    """The PCG solve's cooperative launch may not be capturable into the loop
+    body; either way the level's records equal the host-driven loop's."""
+    import torch
+
+    from paper_2303_16878_b200.bundle import _lm_level, _Runtime
+
+    prob, guess = _room_level_problem(1)
+    rows, gens = P.se3.pose_rows(guess)
+    cfg = P.SolverConfig(linear_solver="pcg")
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("PBA_LM_DEVICE", mode)
+        backend = _Runtime().level([prob], 0, cfg)
+        backend.set_poses(rows, gens)
+        out[mode] = (_lm_level(backend, 0, cfg, 6), backend.current_rows()[0])
+        del backend
+        torch.cuda.synchronize()
+    assert out["1"][0] == out["0"][0]
+    assert np.array_equal(out["1"][1], out["0"][1])
