@@ -48,6 +48,12 @@ def main():
     t_den = timed(lambda: lib.pba_solve_dense(H.data_ptr(), b.data_ptr(), lv.dim, 1e-3, None,
                                               work.data_ptr(), d.data_ptr(), s.data_ptr(), st))
     print(f"dim {lv.dim}: bsr {t_bsr:.1f} us, dense {t_den:.1f} us per call (back-to-back)")
+    if hasattr(lib, "pba_hack_small_times"):  # an instrumented build (clock64 sections)
+        import ctypes
+
+        out = (ctypes.c_longlong * 8)()
+        lib.pba_hack_small_times(out)
+        print("cycles: stage", out[0], "factor", out[1], "substitute", out[2])
 
 
 
