@@ -700,10 +700,8 @@ def run_ours_device_loop(args, lv, lib, problems, level, meta, cfg, solver, stor
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(device.index or 0) as clocks:
-        e0.record(stream)
         recs, err, _, _ = lv.lm_level_device(cost, count, lam, _NoTermination, args.steps,
-                                             float("inf"), details=True)
-        e1.record(stream)
+                                             float("inf"), details=True, events=(e0, e1))
         torch.cuda.synchronize()
     elapsed_ms = e0.elapsed_time(e1)
     if err or len(recs) != args.steps:

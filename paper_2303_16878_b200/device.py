@@ -711,7 +711,8 @@ class DeviceLevel:
         return self._lm_loop_graph() is not None
 
     def lm_level_device(self, cost: float, count: int, lam: float, cfg, max_iterations: int,
-                        lam_ceiling: float = LAMBDA_CEILING, details: bool = False):
+                        lam_ceiling: float = LAMBDA_CEILING, details: bool = False,
+                        events=None):
         """The iterations of bundle._lm_level (solver.py:505-537) as one graph
         launch: a conditional WHILE node replays solve -> update -> linearise
         -> assemble -> decide -> copy-on-accept until the device-side decision
@@ -720,7 +721,8 @@ class DeviceLevel:
         or None where the loop graph is not used (large problems, where a
         host round trip per iteration is negligible; PBA_LM_DEVICE=0; a
         backend whose step cannot be captured) — the caller then runs the
-        host loop."""
+        host loop.  `events` (start, stop) are recorded on the stream around
+        the loop launch alone (the bench's timed region)."""
         if max_iterations > self.LM_RECORD_CAPACITY or not self.lm_loop_ready():
             return None
         loop = self._lm_loop
@@ -734,7 +736,11 @@ class DeviceLevel:
         stream = torch.cuda.current_stream(self.device)
         self._lm_state.copy_(st, non_blocking=True)
         self._lam_dev.copy_(self._lm_state[N.LM_LAMBDA:N.LM_LAMBDA + 1])
+        if events is not None:
+            events[0].record(stream)
         N.check(self.lib.pba_lm_loop_launch(loop, stream.cuda_stream), "pba_lm_loop_launch")
+        if events is not None:
+            events[1].record(stream)
         st.copy_(self._lm_state, non_blocking=True)
         stream.synchronize()
         n = int(st[N.LM_N_RECORDS])
