@@ -299,9 +299,9 @@ int pba_apply_step(const double* poses_in, const int32_t* gen_in, const double* 
  * starts capturing `stream` (a non-default stream) into the loop body; the
  * caller then issues one iteration on that stream — the damped solve with
  * lambda read from lam_dev, pba_apply_step into the candidate buffers,
- * pba_linearize + assembly of the candidate, pba_lm_decide, and pba_copy_if
- * of the candidate buffers over the current ones — and pba_lm_loop_end
- * instantiates it.  Each pba_lm_loop_launch runs the body until
+ * pba_linearize + assembly of the candidate, and pba_lm_decide (which also
+ * copies the candidate buffers over the current ones on acceptance) — and
+ * pba_lm_loop_end instantiates it.  Each pba_lm_loop_launch runs the body until
  * pba_lm_decide clears the loop condition.
  * state: device doubles, PBA_LM_STATE_DOUBLES of them (indices below), set
  * by the host before a launch (iteration = 1, n_records = 0, stop = error =
@@ -333,13 +333,14 @@ int pba_apply_step(const double* poses_in, const int32_t* gen_in, const double* 
 #define PBA_LM_RECORD_DOUBLES 6
 typedef struct pba_lm_loop pba_lm_loop;
 int pba_lm_loop_begin(void* stream, pba_lm_loop** loop, uint64_t* handle);
+/* One iteration's decision, then on acceptance dst[k] <- src[k] (the
+ * candidate poses / generations / H / b / totals over the current ones;
+ * bytes[k] a multiple of 4; device pointers in host arrays of
+ * n <= PBA_LM_MAX_COPY). */
 int pba_lm_decide(double* state, double* records, const int32_t* status_solve,
                   const int32_t* status_step, const double* new_totals, double* lam_dev,
-                  uint64_t handle, void* stream);
-/* dst[k] <- src[k] (bytes[k], a multiple of 4; device pointers; host arrays
- * of n <= PBA_LM_MAX_COPY) when *flag != 0 (device double). */
-int pba_copy_if(const double* flag, void* const* dst, const void* const* src,
-                const int64_t* bytes, int32_t n, void* stream);
+                  uint64_t handle, void* const* dst, const void* const* src,
+                  const int64_t* bytes, int32_t n, void* stream);
 int pba_lm_loop_end(pba_lm_loop* loop);
 int pba_lm_loop_launch(pba_lm_loop* loop, void* stream);
 void pba_lm_loop_destroy(pba_lm_loop* loop);

@@ -7,9 +7,9 @@
 //                       one iteration, one IterationRecord appended to a
 //                       device array, and the loop condition set for the
 //                       next iteration (cudaGraphSetConditional);
-//   copy_if_kernel    — on acceptance, the candidate buffers (poses,
-//                       generations, H, b, totals) copied over the current
-//                       ones, so the captured body always reads buffer 0.
+//                       On acceptance the same kernel copies the candidate
+//                       buffers (poses, generations, H, b, totals) over the
+//                       current ones, so the captured body reads buffer 0.
 // One graph launch then runs a whole level with no host round trip per
 // iteration; the host reads the records and the final state once.
 
@@ -28,12 +28,28 @@ struct pba_lm_loop {
 namespace pba {
 namespace {
 
-// state layout (doubles), see include/pba.h PBA_LM_*
-__global__ void lm_decide_kernel(double* __restrict__ s, double* __restrict__ records,
-                                 const int32_t* __restrict__ status_solve,
-                                 const int32_t* __restrict__ status_step,
-                                 const double* __restrict__ new_totals, double* __restrict__ lam_dev,
-                                 cudaGraphConditionalHandle handle) {
+struct CopySegs {
+  uint32_t* dst[PBA_LM_MAX_COPY];
+  const uint32_t* src[PBA_LM_MAX_COPY];
+  int64_t words[PBA_LM_MAX_COPY];
+  int n;
+};
+
+// One iteration's decision (thread 0; state layout in include/pba.h
+// PBA_LM_*), then — on acceptance — the candidate buffers copied over the
+// current ones by the whole CTA, so the loop body always reads buffer 0.
+__global__ void __launch_bounds__(256) lm_decide_kernel(double* __restrict__ s,
+                                                        double* __restrict__ records,
+                                                        const int32_t* __restrict__ status_solve,
+                                                        const int32_t* __restrict__ status_step,
+                                                        const double* __restrict__ new_totals,
+                                                        double* __restrict__ lam_dev,
+                                                        cudaGraphConditionalHandle handle,
+                                                        CopySegs segs) {
+  __shared__ int take;
+  if (threadIdx.x == 0) take = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
   double cost = s[PBA_LM_COST], count = s[PBA_LM_COUNT], lam = s[PBA_LM_LAMBDA];
   const double factor = s[PBA_LM_FACTOR], rel_tol = s[PBA_LM_REL_TOL];
   const double ceiling = s[PBA_LM_LAMBDA_CEILING], floor_pb = s[PBA_LM_COST_FLOOR];
@@ -86,21 +102,12 @@ __global__ void lm_decide_kernel(double* __restrict__ s, double* __restrict__ re
   s[PBA_LM_STOP] = stop ? 1.0 : 0.0;
   *lam_dev = lam;
   cudaGraphSetConditional(handle, stop ? 0u : 1u);
-}
-
-struct CopySegs {
-  uint32_t* dst[PBA_LM_MAX_COPY];
-  const uint32_t* src[PBA_LM_MAX_COPY];
-  int64_t words[PBA_LM_MAX_COPY];
-  int n;
-};
-
-__global__ void copy_if_kernel(const double* __restrict__ flag, CopySegs segs) {
-  if (*flag == 0.0) return;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  take = accepted ? 1 : 0;
+  }
+  __syncthreads();
+  if (!take) return;
   for (int k = 0; k < segs.n; ++k)
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < segs.words[k]; i += stride)
-      segs.dst[k][i] = segs.src[k][i];
+    for (int64_t i = threadIdx.x; i < segs.words[k]; i += blockDim.x) segs.dst[k][i] = segs.src[k][i];
 }
 
 __global__ void stamp_kernel(const double* __restrict__ state, int64_t* __restrict__ out, int slot) {
@@ -157,33 +164,24 @@ extern "C" int pba_lm_loop_begin(void* stream, pba_lm_loop** out, uint64_t* hand
 
 extern "C" int pba_lm_decide(double* state, double* records, const int32_t* status_solve,
                              const int32_t* status_step, const double* new_totals,
-                             double* lam_dev, uint64_t handle, void* stream) {
+                             double* lam_dev, uint64_t handle, void* const* dst,
+                             const void* const* src, const int64_t* bytes, int32_t n,
+                             void* stream) {
   PBA_ARG_CHECK(state && records && status_solve && status_step && new_totals && lam_dev,
                 "NULL buffer");
-  lm_decide_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(
-      state, records, status_solve, status_step, new_totals, lam_dev,
-      (cudaGraphConditionalHandle)handle);
-  PBA_LAUNCH_CHECK();
-  return PBA_OK;
-}
-
-extern "C" int pba_copy_if(const double* flag, void* const* dst, const void* const* src,
-                           const int64_t* bytes, int32_t n, void* stream) {
-  PBA_ARG_CHECK(flag && dst && src && bytes, "NULL argument");
-  PBA_ARG_CHECK(n >= 0 && n <= PBA_LM_MAX_COPY, "too many copy segments");
+  PBA_ARG_CHECK(n >= 0 && n <= PBA_LM_MAX_COPY && (n == 0 || (dst && src && bytes)),
+                "bad copy segments");
   CopySegs segs{};
-  int64_t most = 0;
   for (int k = 0; k < n; ++k) {
     PBA_ARG_CHECK(bytes[k] >= 0 && bytes[k] % 4 == 0, "copy sizes must be multiples of 4 bytes");
     segs.dst[k] = static_cast<uint32_t*>(dst[k]);
     segs.src[k] = static_cast<const uint32_t*>(src[k]);
     segs.words[k] = bytes[k] / 4;
-    most = segs.words[k] > most ? segs.words[k] : most;
   }
   segs.n = n;
-  const int blocks = (int)((most + 255) / 256 < 148 ? (most + 255) / 256 : 148);
-  copy_if_kernel<<<blocks > 0 ? blocks : 1, 256, 0, static_cast<cudaStream_t>(stream)>>>(flag,
-                                                                                         segs);
+  lm_decide_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      state, records, status_solve, status_step, new_totals, lam_dev,
+      (cudaGraphConditionalHandle)handle, segs);
   PBA_LAUNCH_CHECK();
   return PBA_OK;
 }

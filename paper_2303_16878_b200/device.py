@@ -715,7 +715,7 @@ class DeviceLevel:
                         events=None):
         """The iterations of bundle._lm_level (solver.py:505-537) as one graph
         launch: a conditional WHILE node replays solve -> update -> linearise
-        -> assemble -> decide -> copy-on-accept until the device-side decision
+        -> assemble -> decide (+ copy on accept) until the device-side decision
         stops the loop; the host reads the records once.  Returns
         (records [(lambda, cost, count, accepted)], error code, cost, count),
         or None where the loop graph is not used (large problems, where a
@@ -799,10 +799,7 @@ class DeviceLevel:
                         self._lm_state.data_ptr(), self._lm_records.data_ptr(),
                         self._status_solve_ptr, self._status_step_ptr,
                         self.totals[1].data_ptr(), self._lam_dev.data_ptr(), handle.value,
-                        stream.cuda_stream), "pba_lm_decide")
-                    N.check(self.lib.pba_copy_if(
-                        self._lm_state.data_ptr() + 8 * N.LM_ACCEPTED, dst, src, nbytes, n,
-                        stream.cuda_stream), "pba_copy_if")
+                        dst, src, nbytes, n, stream.cuda_stream), "pba_lm_decide")
                     stamp(5)
                 N.check(self.lib.pba_lm_loop_end(loop), "pba_lm_loop_end")
                 ok = True

@@ -45,7 +45,7 @@ EXPORTED = (
     "pba_solve_work_bytes", "pba_solve_dense", "pba_solve_dense_ex", "pba_solve_dense_bsr",
     "pba_pcg_work_bytes", "pba_solve_pcg", "pba_solve_pcg_ex", "pba_solve_pcg_bsr",
     "pba_apply_step",
-    "pba_lm_loop_begin", "pba_lm_decide", "pba_copy_if", "pba_lm_loop_end", "pba_lm_loop_launch",
+    "pba_lm_loop_begin", "pba_lm_decide", "pba_lm_loop_end", "pba_lm_loop_launch",
     "pba_lm_loop_destroy",
     "pba_overlap_counts", "pba_normals_scratch_bytes",
     "pba_estimate_normals", "pba_downscale_cues", "pba_decode_raster", "pba_atan2_batch",
@@ -126,8 +126,8 @@ _SIGNATURES = {
                                      _vp, _vp]),
     "pba_apply_step": (ctypes.c_int, [_vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp]),
     "pba_lm_loop_begin": (ctypes.c_int, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_uint64)]),
-    "pba_lm_decide": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_uint64, _vp]),
-    "pba_copy_if": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i32, _vp]),
+    "pba_lm_decide": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_uint64, _vp, _vp,
+                                     _vp, _i32, _vp]),
     "pba_lm_loop_end": (ctypes.c_int, [_vp]),
     "pba_lm_loop_launch": (ctypes.c_int, [_vp, _vp]),
     "pba_lm_loop_destroy": (None, [_vp]),
