@@ -143,6 +143,14 @@ size_t pba_build_texels_scratch_bytes(const pba_camera* cam);
 int pba_build_texels(const pba_camera* cam, const double* intensity, const double* depth,
                      const double* normals, void* texels, uint8_t* mask, void* scratch,
                      void* stream);
+/* The same for n_frames frames of one camera stored back to back: frame f's
+ * intensity / depth at + f*H*W, normals at + 3*f*H*W, texels at
+ * + f*H*W*pba_texel_bytes() bytes, mask at + f*H*W, scratch at
+ * + f*pba_build_texels_scratch_bytes(cam) bytes (three launches in all
+ * instead of three per frame; identical texels). */
+int pba_build_texels_batch(const pba_camera* cam, int32_t n_frames, const double* intensity,
+                           const double* depth, const double* normals, void* texels,
+                           uint8_t* mask, void* scratch, void* stream);
 
 /* ---- linearisation: _LevelProblem.evaluate per-pair part --------------
  * (solver.py:416-426 -> _edge_term :356-390 -> PairContext.evaluate :222-303)

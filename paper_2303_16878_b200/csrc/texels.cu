@@ -24,11 +24,35 @@ constexpr uint8_t kDV = PBA_MASK_DEPTH_VALID;
 constexpr uint8_t kNV = PBA_MASK_NORMAL_VALID;
 constexpr uint8_t kCoherent = 0x80;  // scratch bit: normal_valid & neighbour-coherent
 
+// Frame f = blockIdx.y of a batch: inputs at f * H * W (normals f * 3 H W),
+// scratch at f * scratch_stride bytes, texels at f * kTexelBytes * H * W.
+struct FrameScratch {
+  double* d;
+  double* n;
+  uint8_t* flags;
+};
+__device__ __forceinline__ FrameScratch frame_scratch(char* scratch, size_t stride, size_t px) {
+  char* s = scratch + blockIdx.y * stride;
+  FrameScratch f;
+  f.d = reinterpret_cast<double*>(s);
+  f.n = reinterpret_cast<double*>(s + ((px * sizeof(double) + 255) / 256) * 256);
+  f.flags = reinterpret_cast<uint8_t*>(s + ((px * sizeof(double) + 255) / 256) * 256 +
+                                       ((px * 3 * sizeof(double) + 255) / 256) * 256);
+  return f;
+}
+
 __global__ void clean_pass(int H, int W, double dmin, double dmax, const double* __restrict__ depth,
-                           const double* __restrict__ normals, double* __restrict__ d_out,
-                           double* __restrict__ n_out, uint8_t* __restrict__ flags) {
+                           const double* __restrict__ normals, char* __restrict__ scratch,
+                           size_t scratch_stride) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= H * W) return;
+  const size_t px = (size_t)H * W;
+  const FrameScratch fs = frame_scratch(scratch, scratch_stride, px);
+  double* __restrict__ d_out = fs.d;
+  double* __restrict__ n_out = fs.n;
+  uint8_t* __restrict__ flags = fs.flags;
+  depth += blockIdx.y * px;
+  normals += blockIdx.y * 3 * px;
   double d = depth[p];
   // cues.py:114-115: non-finite or out-of-range depth becomes 0 (invalid).
   if (!isfinite(d) || d < dmin || d > dmax) d = 0.0;
@@ -50,10 +74,12 @@ __device__ __forceinline__ double dot3_rn(const double* a, const double* b) {
   return __dadd_rn(__dadd_rn(__dmul_rn(a[0], b[0]), __dmul_rn(a[1], b[1])), __dmul_rn(a[2], b[2]));
 }
 
-__global__ void coherence_pass(int H, int W, const double* __restrict__ n,
-                               uint8_t* __restrict__ flags) {
+__global__ void coherence_pass(int H, int W, char* __restrict__ scratch, size_t scratch_stride) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= H * W) return;
+  const FrameScratch fs = frame_scratch(scratch, scratch_stride, (size_t)H * W);
+  const double* __restrict__ n = fs.n;
+  uint8_t* __restrict__ flags = fs.flags;
   const int r = p / W, c = p - r * W;
   uint8_t f = flags[p];
   bool coherent = false;
@@ -67,11 +93,18 @@ __global__ void coherence_pass(int H, int W, const double* __restrict__ n,
 }
 
 __global__ void gradient_pass(int H, int W, const double* __restrict__ inten,
-                              const double* __restrict__ d, const double* __restrict__ n,
-                              const uint8_t* __restrict__ flags, double2* __restrict__ out,
-                              uint8_t* __restrict__ mask_out) {
+                              char* __restrict__ scratch, size_t scratch_stride,
+                              double2* __restrict__ out, uint8_t* __restrict__ mask_out) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= H * W) return;
+  const size_t px = (size_t)H * W;
+  const FrameScratch fs = frame_scratch(scratch, scratch_stride, px);
+  const double* __restrict__ d = fs.d;
+  const double* __restrict__ n = fs.n;
+  const uint8_t* __restrict__ flags = fs.flags;
+  inten += blockIdx.y * px;
+  out += blockIdx.y * (px * (kTexelBytes / sizeof(double2)));
+  mask_out += blockIdx.y * px;
   const int r = p / W, c = p - r * W;
   const uint8_t f = flags[p];
   double g[10];
@@ -133,30 +166,35 @@ extern "C" size_t pba_build_texels_scratch_bytes(const pba_camera* cam) {
          align_up(px, 256);
 }
 
-extern "C" int pba_build_texels(const pba_camera* cam, const double* intensity,
-                                const double* depth, const double* normals, void* texels,
-                                uint8_t* mask, void* scratch, void* stream) {
+extern "C" int pba_build_texels_batch(const pba_camera* cam, int32_t n_frames,
+                                      const double* intensity, const double* depth,
+                                      const double* normals, void* texels, uint8_t* mask,
+                                      void* scratch, void* stream) {
   PBA_ARG_CHECK(cam != nullptr, "cam is NULL");
   PBA_ARG_CHECK(cam->width >= 2 && cam->height >= 2, "image must be at least 2x2");
+  PBA_ARG_CHECK(n_frames >= 0 && n_frames <= 65535, "n_frames must lie in [0, 65535]");
+  if (n_frames == 0) return PBA_OK;
   PBA_ARG_CHECK(intensity && depth && normals && texels && mask && scratch, "NULL buffer");
   const int H = cam->height, W = cam->width;
   const size_t px = (size_t)W * H;
+  const size_t stride = pba_build_texels_scratch_bytes(cam);
   char* s = static_cast<char*>(scratch);
-  double* d_clean = reinterpret_cast<double*>(s);
-  s += align_up(px * sizeof(double), 256);
-  double* n_clean = reinterpret_cast<double*>(s);
-  s += align_up(px * 3 * sizeof(double), 256);
-  uint8_t* flags = reinterpret_cast<uint8_t*>(s);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int threads = 256;
-  const int blocks = (int)((px + threads - 1) / threads);
-  clean_pass<<<blocks, threads, 0, st>>>(H, W, cam->depth_min, cam->depth_max, depth, normals,
-                                          d_clean, n_clean, flags);
+  const dim3 grid((unsigned)((px + threads - 1) / threads), (unsigned)n_frames);
+  clean_pass<<<grid, threads, 0, st>>>(H, W, cam->depth_min, cam->depth_max, depth, normals, s,
+                                        stride);
   PBA_LAUNCH_CHECK();
-  coherence_pass<<<blocks, threads, 0, st>>>(H, W, n_clean, flags);
+  coherence_pass<<<grid, threads, 0, st>>>(H, W, s, stride);
   PBA_LAUNCH_CHECK();
-  gradient_pass<<<blocks, threads, 0, st>>>(H, W, intensity, d_clean, n_clean, flags,
-                                             static_cast<double2*>(texels), mask);
+  gradient_pass<<<grid, threads, 0, st>>>(H, W, intensity, s, stride,
+                                           static_cast<double2*>(texels), mask);
   PBA_LAUNCH_CHECK();
   return PBA_OK;
+}
+
+extern "C" int pba_build_texels(const pba_camera* cam, const double* intensity,
+                                const double* depth, const double* normals, void* texels,
+                                uint8_t* mask, void* scratch, void* stream) {
+  return pba_build_texels_batch(cam, 1, intensity, depth, normals, texels, mask, scratch, stream);
 }

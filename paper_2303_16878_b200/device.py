@@ -213,8 +213,64 @@ class FrameStore:
         for (h, w), group in todo.items():
             tex = torch.empty((len(group), h * w * tb), dtype=torch.uint8, device=self.device)
             msk = torch.empty((len(group), h * w), dtype=torch.uint8, device=self.device)
-            for k, cue in enumerate(group):
-                self.frame(cue, tex[k], msk[k])
+            k = 0
+            while k < len(group):
+                n = self._batch_run(group, k, h * w)
+                if n > 1:  # consecutive frames of one device batch: one batched texel build
+                    self._frames_batch(group[k:k + n], tex[k:k + n], msk[k:k + n])
+                else:
+                    self.frame(group[k], tex[k], msk[k])
+                k += max(n, 1)
+
+    @staticmethod
+    def _batch_run(group, k, px) -> int:
+        """How many cues from group[k] on are consecutive frames of one
+        device-resident (n, H, W) batch (device pyramid levels are views
+        li[b] of such batches) with identical intrinsics."""
+        first = group[k]
+        if getattr(first, "device_intensity", None) is None:
+            return 1
+        chans = ("device_intensity", "device_depth", "device_normals")
+        sizes = (px * 8, px * 8, 3 * px * 8)
+
+        def ok(cue):
+            return all(getattr(cue, c, None) is not None and getattr(cue, c).dtype == torch.float64
+                       and getattr(cue, c).is_contiguous() for c in chans)
+
+        if not ok(first):
+            return 1
+        base = [getattr(first, c).data_ptr() for c in chans]
+        n = 1
+        while k + n < len(group):
+            cue = group[k + n]
+            if (cue.intrinsics != first.intrinsics or not ok(cue)
+                    or any(getattr(cue, c).data_ptr() != b + n * sz
+                           for c, b, sz in zip(chans, base, sizes))):
+                break
+            n += 1
+        return n
+
+    def _frames_batch(self, cues, texels, mask) -> None:
+        """FrameStore.frame for consecutive frames of one device batch through
+        pba_build_texels_batch (sub-batches bounded by the scratch size)."""
+        first = cues[0]
+        intr = first.intrinsics
+        cam = camera_struct(intr)
+        per = int(self._lib.pba_build_texels_scratch_bytes(ctypes.byref(cam)))
+        step = max(1, min(len(cues), (256 << 20) // max(per, 1)))
+        if self._scratch is None or self._scratch.numel() < per * step:
+            self._scratch = torch.empty(per * step, dtype=torch.uint8, device=self.device)
+        ray = self.ray(intr)
+        for a in range(0, len(cues), step):
+            b = min(len(cues), a + step)
+            c0 = cues[a]
+            N.check(self._lib.pba_build_texels_batch(
+                ctypes.byref(cam), b - a, c0.device_intensity.data_ptr(),
+                c0.device_depth.data_ptr(), c0.device_normals.data_ptr(), texels[a].data_ptr(),
+                mask[a].data_ptr(), self._scratch.data_ptr(), _stream_ptr(self.device)),
+                "pba_build_texels_batch")
+            for k in range(a, b):  # keep each cue referenced so its id() stays unique
+                self._frames[id(cues[k])] = (cues[k], texels[k], mask[k], ray, camera_struct(intr))
 
     def frame(self, cue, texels=None, mask=None):
         """(texels, mask, ray table, Camera) of a cue image, uploading on first

@@ -40,7 +40,7 @@ EXPORTED = (
     "pba_texel_bytes", "pba_ray_table_doubles", "pba_version", "pba_last_error",
     "pba_build_checked",
     "pba_kernel_launches",
-    "pba_build_texels_scratch_bytes", "pba_build_texels", "pba_plan_chunks", "pba_linearize_scratch_bytes", "pba_linearize",
+    "pba_build_texels_scratch_bytes", "pba_build_texels", "pba_build_texels_batch", "pba_plan_chunks", "pba_linearize_scratch_bytes", "pba_linearize",
     "pba_plan_assembly", "pba_assemble", "pba_assemble_bsr", "pba_sum_totals",
     "pba_solve_work_bytes", "pba_solve_dense", "pba_solve_dense_ex", "pba_solve_dense_bsr",
     "pba_pcg_work_bytes", "pba_solve_pcg", "pba_solve_pcg_ex", "pba_solve_pcg_bsr",
@@ -99,6 +99,8 @@ _SIGNATURES = {
     "pba_kernel_launches": (ctypes.c_uint64, []),
     "pba_build_texels_scratch_bytes": (_sz, [ctypes.POINTER(Camera)]),
     "pba_build_texels": (ctypes.c_int, [ctypes.POINTER(Camera), _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "pba_build_texels_batch": (ctypes.c_int, [ctypes.POINTER(Camera), _i32, _vp, _vp, _vp, _vp,
+                                              _vp, _vp, _vp]),
     "pba_plan_chunks": (ctypes.c_int, [_vp, _i32, _vp, _i32, _i32, _vp, _vp,
                                        ctypes.POINTER(_i64)]),
     "pba_linearize_scratch_bytes": (_sz, [_i32, _i64]),

@@ -103,6 +103,31 @@ def test_device_pyramid_batch_equals_single():
             assert torch.equal(x.device_normals, y.device_normals)
 
 
+def test_batched_texel_build_equals_per_frame():
+    """FrameStore.prefetch builds the texels of consecutive frames of one
+    device batch with one pba_build_texels_batch call; per-frame
+    pba_build_texels gives the same bytes (and host cue images still take
+    the per-frame path)."""
+    from paper_2303_16878_b200 import scenes as S
+    from paper_2303_16878_b200.device import FrameStore
+
+    cam = S.rgbd_160()
+    rows = S.sensor_rows(S.room_loop(5), P.Pose.identity()).cuda()
+    inten, depth, _ = S.render_batch(S.BoxScene(), cam, rows)
+    pyrs = P.build_pyramids_device(inten, depth, cam, (0.5, 1.0))
+    dev = torch.device("cuda", 0)
+    for level in (0, 1):
+        cues = [p.levels[level] for p in pyrs]
+        batched, single = FrameStore(dev), FrameStore(dev)
+        batched.prefetch(cues)
+        assert FrameStore._batch_run(cues, 0, cues[0].shape[0] * cues[0].shape[1]) == 5
+        for cue in cues:
+            tb, mb, rb, cb = batched.frame(cue)
+            ts, ms, rs, cs = single.frame(cue)
+            assert torch.equal(tb, ts) and torch.equal(mb, ms) and torch.equal(rb, rs)
+            assert bytes(cb) == bytes(cs)
+
+
 def _assert_normals_equal_host(depth_batch, cam, dev):
     """zero validity flips, normals within 1e-10, against the host
     restatement (bit-exact to the reference's estimate_normals)."""
