@@ -155,7 +155,6 @@ __host__ __device__ inline int pair_chunk_pixels(int gw, int chunk_pixels) {
   return bands * kTileRows * gw;
 }
 
-
 struct PairSetup {
   double Ri[9], Rj[9], Ro[9];
   double Mi[9];    // R_o^T R_j^T R_i                       (solver.py:265)
