@@ -241,3 +241,83 @@ def test_device_lm_loop_with_pcg_matches_host_loop(monkeypatch):
         torch.cuda.synchronize()
     assert out["1"][0] == out["0"][0]
     assert np.array_equal(out["1"][1], out["0"][1])
+
+
+def _decide_once(cost, count, lam, iteration, max_iterations, status_solve, status_step,
+                 new_cost, new_count, rel_tol=1e-4):
+    """One pba_lm_decide run as the whole body of a conditional loop graph."""
+    import ctypes
+
+    import torch
+
+    from paper_2303_16878_b200 import native as N
+
+    lib = N.load()
+    dev = torch.device("cuda", 0)
+    st = torch.zeros(N.LM_STATE_DOUBLES, dtype=torch.float64)
+    st[N.LM_COST], st[N.LM_COUNT], st[N.LM_LAMBDA] = cost, count, lam
+    st[N.LM_FACTOR], st[N.LM_REL_TOL] = 10.0, rel_tol
+    st[N.LM_LAMBDA_CEILING], st[N.LM_COST_FLOOR] = 1e12, 1e-18
+    st[N.LM_ITERATION], st[N.LM_MAX_ITERATIONS] = iteration, max_iterations
+    state = st.to(dev)
+    records = torch.zeros(N.LM_RECORD_DOUBLES * 8, dtype=torch.float64, device=dev)
+    s_solve = torch.tensor([status_solve], dtype=torch.int32, device=dev)
+    s_step = torch.tensor([status_step], dtype=torch.int32, device=dev)
+    totals = torch.tensor([new_cost, new_count], dtype=torch.float64, device=dev)
+    lam_dev = torch.zeros(1, dtype=torch.float64, device=dev)
+    src = torch.arange(1.0, 7.0, dtype=torch.float64, device=dev)
+    dst = torch.zeros(6, dtype=torch.float64, device=dev)
+    d_arr = (ctypes.c_void_p * 1)(dst.data_ptr())
+    s_arr = (ctypes.c_void_p * 1)(src.data_ptr())
+    n_arr = (ctypes.c_int64 * 1)(48)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.synchronize()
+    loop, handle = ctypes.c_void_p(), ctypes.c_uint64()
+    N.check(lib.pba_lm_loop_begin(stream.cuda_stream, ctypes.byref(loop), ctypes.byref(handle)),
+            "begin")
+    N.check(lib.pba_lm_decide(state.data_ptr(), records.data_ptr(), s_solve.data_ptr(),
+                              s_step.data_ptr(), totals.data_ptr(), lam_dev.data_ptr(),
+                              handle.value, d_arr, s_arr, n_arr, 1, stream.cuda_stream), "decide")
+    N.check(lib.pba_lm_loop_end(loop), "end")
+    N.check(lib.pba_lm_loop_launch(loop, stream.cuda_stream), "launch")
+    stream.synchronize()
+    lib.pba_lm_loop_destroy(loop)
+    out = state.cpu().numpy()
+    n = int(out[N.LM_N_RECORDS])
+    return out, records.cpu().numpy().reshape(-1, N.LM_RECORD_DOUBLES)[:n], float(lam_dev.item()), \
+        dst.cpu().numpy()
+
+
+def test_lm_decide_kernel_branches():
+    """lm_decide_kernel against bundle._lm_level's branches (solver.py:505-537):
+    singular first solve, singular later solve, ||dq|| >= 1, accept, reject,
+    relative-decrease stop, iteration cap; the candidate is copied only on
+    acceptance."""
+    from paper_2303_16878_b200 import native as N
+
+    # singular first solve -> UnderConstrainedError, no record
+    s, r, _, dst = _decide_once(10.0, 3, 1e-3, 1, 10, 1, 0, 0.0, 0)
+    assert s[N.LM_ERROR] == N.LM_ERR_UNDERCONSTRAINED and s[N.LM_STOP] == 1 and len(r) == 0
+    # singular later solve -> lambda x factor, record, continue (cap stops this one)
+    s, r, lam, dst = _decide_once(10.0, 3, 1e-3, 4, 4, 1, 0, 0.0, 0)
+    assert s[N.LM_ERROR] == 0 and lam == 1e-3 * 10.0
+    assert r.tolist() == [[1e-3 * 10.0, 10.0, 3.0, 0.0, 0.0, 0.0]] and not dst.any()
+    # ||dq|| >= 1 -> InvalidPerturbationError
+    s, r, _, _ = _decide_once(10.0, 3, 1e-3, 2, 10, 0, 1, 5.0, 3)
+    assert s[N.LM_ERROR] == N.LM_ERR_PERTURBATION and s[N.LM_STOP] == 1 and len(r) == 0
+    # accepted: cost / count move, lambda halves, candidate copied; cap stops
+    s, r, lam, dst = _decide_once(10.0, 3, 1e-3, 1, 1, 0, 0, 5.0, 4)
+    assert s[N.LM_ACCEPTED] == 1 and lam == max(1e-3 * 0.5, 1e-12)
+    assert r.tolist() == [[lam, 5.0, 4.0, 1.0, 5.0, 4.0]]
+    assert (s[N.LM_COST], s[N.LM_COUNT]) == (5.0, 4.0) and dst.tolist() == [1, 2, 3, 4, 5, 6]
+    # rejected (no decrease, or count 0): lambda x factor, nothing copied
+    for new_cost, new_count in ((20.0, 3), (5.0, 0)):
+        s, r, lam, dst = _decide_once(10.0, 3, 1e-3, 1, 1, 0, 0, new_cost, new_count)
+        assert s[N.LM_ACCEPTED] == 0 and lam == 1e-3 * 10.0 and not dst.any()
+        assert (s[N.LM_COST], s[N.LM_COUNT]) == (10.0, 3.0)
+    # relative decrease below the tolerance stops after accepting
+    s, r, _, _ = _decide_once(10.0, 3, 1e-3, 1, 10, 0, 0, 10.0 * (1 - 1e-6), 3)
+    assert s[N.LM_ACCEPTED] == 1 and s[N.LM_STOP] == 1 and s[N.LM_ITERATION] == 2
+    # lambda above the ceiling stops after rejecting
+    s, r, lam, _ = _decide_once(10.0, 3, 2e11, 1, 10, 0, 0, 20.0, 3)
+    assert lam == 2e12 and s[N.LM_STOP] == 1
