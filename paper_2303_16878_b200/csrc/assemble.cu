@@ -84,15 +84,17 @@ __global__ void assemble_kernel(const double* __restrict__ rec, int n_free,
 // of slot s and of the (r, c) / (c, r) blocks of off-diagonal target o.
 // Entry by entry the sums run in the same edge order as assemble_kernel,
 // so Hb holds exactly the dense H's non-zero blocks.
-__global__ void assemble_bsr_kernel(const double* __restrict__ rec, int n_free,
-                                    const int32_t* __restrict__ diag_ptr,
-                                    const int32_t* __restrict__ diag_items, int n_off,
-                                    const int32_t* __restrict__ off_ptr,
-                                    const int32_t* __restrict__ off_items,
-                                    const int32_t* __restrict__ diag_blk,
-                                    const int32_t* __restrict__ off_blk, double* __restrict__ Hb,
-                                    double* __restrict__ b) {
-  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void assemble_bsr_entry(long t, const double* __restrict__ rec,
+                                                   int n_free,
+                                                   const int32_t* __restrict__ diag_ptr,
+                                                   const int32_t* __restrict__ diag_items,
+                                                   int n_off,
+                                                   const int32_t* __restrict__ off_ptr,
+                                                   const int32_t* __restrict__ off_items,
+                                                   const int32_t* __restrict__ diag_blk,
+                                                   const int32_t* __restrict__ off_blk,
+                                                   double* __restrict__ Hb,
+                                                   double* __restrict__ b) {
   const long n_diag = 42L * n_free;
   if (t < n_diag) {
     const int s = (int)(t / 42), e = (int)(t - 42L * s);
@@ -133,8 +135,8 @@ __global__ void assemble_bsr_kernel(const double* __restrict__ rec, int n_free,
 
 // cost and count summed over pairs: each thread a contiguous edge range in
 // order, then a fixed tree — deterministic for a given pair count.
-__global__ void totals_kernel(const double* __restrict__ rec, int n_pairs,
-                              double* __restrict__ totals) {
+__device__ __forceinline__ void totals_block(const double* __restrict__ rec, int n_pairs,
+                                             double* __restrict__ totals) {
   __shared__ double sc[256], sn[256];
   const int tid = threadIdx.x;
   const int per = (n_pairs + 255) / 256;
@@ -158,6 +160,28 @@ __global__ void totals_kernel(const double* __restrict__ rec, int n_pairs,
     totals[0] = sc[0];
     totals[1] = sn[0];
   }
+}
+
+__global__ void totals_kernel(const double* __restrict__ rec, int n_pairs,
+                              double* __restrict__ totals) {
+  totals_block(rec, n_pairs, totals);
+}
+
+// The block-sparse assembly with the totals as one more CTA of the same
+// launch (the last one; 256 threads, the same fixed tree as totals_kernel),
+// so an LM step issues one launch for both.
+__global__ void __launch_bounds__(256) assemble_bsr_kernel(
+    const double* __restrict__ rec, int n_free, const int32_t* __restrict__ diag_ptr,
+    const int32_t* __restrict__ diag_items, int n_off, const int32_t* __restrict__ off_ptr,
+    const int32_t* __restrict__ off_items, const int32_t* __restrict__ diag_blk,
+    const int32_t* __restrict__ off_blk, double* __restrict__ Hb, double* __restrict__ b,
+    int n_pairs, double* __restrict__ totals) {
+  if (blockIdx.x == gridDim.x - 1) {
+    totals_block(rec, n_pairs, totals);
+    return;
+  }
+  assemble_bsr_entry((long)blockIdx.x * blockDim.x + threadIdx.x, rec, n_free, diag_ptr,
+                     diag_items, n_off, off_ptr, off_items, diag_blk, off_blk, Hb, b);
 }
 
 }  // namespace
@@ -263,17 +287,14 @@ extern "C" int pba_assemble_bsr(const double* records, int32_t n_pairs, int32_t 
   PBA_ARG_CHECK(n_free >= 0 && n_off >= 0 && n_pairs >= 0, "bad sizes");
   PBA_ARG_CHECK(totals != nullptr, "NULL totals");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (n_free > 0) {
+  if (n_free > 0)
     PBA_ARG_CHECK(Hb && b && diag_ptr && diag_blk && (n_off == 0 || (off_ptr && off_items &&
                                                                      off_blk)),
                   "NULL buffer");
-    const long threads = 42L * n_free + 36L * n_off;  // every block written: no memset
-    assemble_bsr_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
-        records, n_free, diag_ptr, diag_items, n_off, off_ptr, off_items, diag_blk, off_blk, Hb,
-        b);
-    PBA_LAUNCH_CHECK();
-  }
-  totals_kernel<<<1, 256, 0, st>>>(records, n_pairs, totals);
+  const long threads = n_free > 0 ? 42L * n_free + 36L * n_off : 0;  // every block written
+  assemble_bsr_kernel<<<(unsigned)((threads + 255) / 256 + 1), 256, 0, st>>>(
+      records, n_free, diag_ptr, diag_items, n_off, off_ptr, off_items, diag_blk, off_blk, Hb, b,
+      n_pairs, totals);
   PBA_LAUNCH_CHECK();
   return PBA_OK;
 }
