@@ -35,26 +35,19 @@ struct CopySegs {
   int n;
 };
 
-// One iteration's decision (thread 0; state layout in include/pba.h
-// PBA_LM_*), then — on acceptance — the candidate buffers copied over the
-// current ones by the whole CTA, so the loop body always reads buffer 0.
-__global__ void __launch_bounds__(256) lm_decide_kernel(double* __restrict__ s,
-                                                        double* __restrict__ records,
-                                                        const int32_t* __restrict__ status_solve,
-                                                        const int32_t* __restrict__ status_step,
-                                                        const double* __restrict__ new_totals,
-                                                        double* __restrict__ lam_dev,
-                                                        cudaGraphConditionalHandle handle,
-                                                        CopySegs segs) {
-  __shared__ int take;
-  if (threadIdx.x == 0) take = 0;
-  __syncthreads();
-  if (threadIdx.x == 0) {
+// One iteration's decision (state layout in include/pba.h PBA_LM_*): the
+// accept / reject, lambda, record and stop logic of solver.py:505-537.
+// Returns whether the candidate was accepted.
+__device__ bool lm_decide(double* __restrict__ s, double* __restrict__ records,
+                          const int32_t* __restrict__ status_solve,
+                          const int32_t* __restrict__ status_step,
+                          const double* __restrict__ new_totals, double* __restrict__ lam_dev,
+                          cudaGraphConditionalHandle handle) {
   double cost = s[PBA_LM_COST], count = s[PBA_LM_COUNT], lam = s[PBA_LM_LAMBDA];
   const double factor = s[PBA_LM_FACTOR], rel_tol = s[PBA_LM_REL_TOL];
   const double ceiling = s[PBA_LM_LAMBDA_CEILING], floor_pb = s[PBA_LM_COST_FLOOR];
   const int it = (int)s[PBA_LM_ITERATION], max_it = (int)s[PBA_LM_MAX_ITERATIONS];
-  int n_rec = (int)s[PBA_LM_N_RECORDS];
+  const int n_rec = (int)s[PBA_LM_N_RECORDS];
   bool stop = false, accepted = false, record = true;
   if (*status_solve != 0) {  // LinAlgError from the solve
     if (it == 1) {
@@ -102,8 +95,22 @@ __global__ void __launch_bounds__(256) lm_decide_kernel(double* __restrict__ s,
   s[PBA_LM_STOP] = stop ? 1.0 : 0.0;
   *lam_dev = lam;
   cudaGraphSetConditional(handle, stop ? 0u : 1u);
-  take = accepted ? 1 : 0;
-  }
+  return accepted;
+}
+
+// Thread 0 decides; on acceptance the whole CTA copies the candidate
+// buffers over the current ones, so the loop body always reads buffer 0.
+__global__ void __launch_bounds__(256) lm_decide_kernel(double* __restrict__ s,
+                                                        double* __restrict__ records,
+                                                        const int32_t* __restrict__ status_solve,
+                                                        const int32_t* __restrict__ status_step,
+                                                        const double* __restrict__ new_totals,
+                                                        double* __restrict__ lam_dev,
+                                                        cudaGraphConditionalHandle handle,
+                                                        CopySegs segs) {
+  __shared__ int take;
+  if (threadIdx.x == 0)
+    take = lm_decide(s, records, status_solve, status_step, new_totals, lam_dev, handle) ? 1 : 0;
   __syncthreads();
   if (!take) return;
   for (int k = 0; k < segs.n; ++k)
