@@ -642,7 +642,7 @@ __global__ void __launch_bounds__(kT, kMinBlocks)
     constexpr bool kNoPrefetch = kLean;
     constexpr bool kEarlyMP = kLean;
     if constexpr (kNoPrefetch) {
-      const double2* t = s_tex + sp;
+      const double2* t = s_tex + PBA_DCHECK_INDEX(sp, sg.z);
       nx0 = __ldg(t);
       nx2 = __ldg(t + kPairNzM * sg.z);
     }
