@@ -204,6 +204,30 @@ def test_host_planning_functions():
     assert b"stride" in lib.pba_last_error()
 
 
+def test_new_entry_points_reject_bad_arguments():
+    """Argument checks of the round-2 entry points run before any CUDA call
+    (so they are exercised here, without a GPU): PBA_ERR_ARG and a message."""
+    lib = native.load()
+    cam = native.Camera(0, 160, 120, 0, 70.0, 70.0, 80.0, 60.0, 0.1, 50.0)
+    assert lib.pba_build_texels_batch(ctypes.byref(cam), -1, None, None, None, None, None, None,
+                                      None) == native.PBA_ERR_ARG
+    assert b"n_frames" in lib.pba_last_error()
+    assert lib.pba_build_texels_batch(ctypes.byref(cam), 0, None, None, None, None, None, None,
+                                      None) == native.PBA_OK  # nothing to do
+    loop, handle = ctypes.c_void_p(), ctypes.c_uint64()
+    assert lib.pba_lm_loop_begin(None, ctypes.byref(loop), ctypes.byref(handle)) == \
+        native.PBA_ERR_ARG  # the default stream cannot be captured
+    assert lib.pba_lm_decide(None, None, None, None, None, None, 0, None, None, None, 0,
+                             None) == native.PBA_ERR_ARG
+    buf = ctypes.create_string_buffer(64)
+    p = ctypes.addressof(buf)
+    assert lib.pba_lm_decide(p, p, p, p, p, p, 0, None, None, None, native.LM_MAX_COPY + 1,
+                             None) == native.PBA_ERR_ARG
+    assert lib.pba_lm_loop_end(None) == native.PBA_ERR_ARG
+    assert lib.pba_lm_loop_launch(None, None) == native.PBA_ERR_ARG
+    lib.pba_lm_loop_destroy(None)  # no-op
+
+
 def test_chunk_plan_whole_row_bands():
     """pba_plan_chunks rounds a pair's chunk to whole 8-row bands when the
     strided grid width is a multiple of 16 and 8 rows fit the requested size
