@@ -326,6 +326,43 @@ def level_contexts(problems, level, cfg):
     return out
 
 
+class LevelTables:
+    """level_contexts as arrays, in the same pair order: per pair the problem,
+    the two node (pose) indices and the occlusion tolerance; per problem its
+    nodes.  Built with one pass over the edges instead of a tuple per pair."""
+
+    def __init__(self, problems, level, cfg, tolerance_override=None):
+        self.problems = problems
+        prob, pi, pj, tol = [], [], [], []
+        for p, problem in enumerate(problems):
+            nodes = problem.graph.nodes
+            index_of = {n.id: k for k, n in enumerate(nodes)}
+            edges = problem.graph.edges
+            ei = np.fromiter((index_of[e.i] for e in edges), dtype=np.int64, count=len(edges))
+            ej = np.fromiter((index_of[e.j] for e in edges), dtype=np.int64, count=len(edges))
+            sensor_code = {}
+            codes = np.fromiter((sensor_code.setdefault(n.sensor_id, len(sensor_code))
+                                 for n in nodes), dtype=np.int64, count=len(nodes))
+            if len(edges) and np.any(codes[ei] != codes[ej]):
+                from .bundle import FusionConfigError
+                raise FusionConfigError("edges must connect frames of one sensor")
+            scale = np.fromiter((n.pyramid.scales[level] for n in nodes), dtype=np.float64,
+                                count=len(nodes))
+            prob.append(np.full(len(edges), p, dtype=np.int64))
+            pi.append(ei)
+            pj.append(ej)
+            tol.append(cfg.occlusion_depth_tolerance / scale[ei] if tolerance_override is None
+                       else np.full(len(edges), float(tolerance_override)))
+        cat = (lambda a, dt: np.concatenate(a).astype(dt) if a else np.zeros(0, dt))
+        self.prob = cat(prob, np.int64)
+        self.pose_i = cat(pi, np.int64)
+        self.pose_j = cat(pj, np.int64)
+        self.tol = cat(tol, np.float64)
+
+    def __len__(self) -> int:
+        return len(self.pose_i)
+
+
 def config_struct(cfg) -> N.Config:
     c = N.Config()
     c.huber_delta[:] = [cfg.huber_delta_intensity, cfg.huber_delta_depth, cfg.huber_delta_normal]
@@ -354,68 +391,73 @@ class DeviceLevel:
         self.n_poses = len(problems[0].graph.nodes)
         self.gauge = problems[0].gauge_index
         self.ccfg = config_struct(cfg)
-        ctxs = level_contexts(problems, level, cfg)
-        if tolerance_override is not None:
-            ctxs = [c[:5] + (tolerance_override,) for c in ctxs]
-        self.n_pairs_total = len(ctxs)
-        self.pose_i = np.array([c[0] for c in ctxs], dtype=np.int32)
-        self.pose_j = np.array([c[1] for c in ctxs], dtype=np.int32)
+        tabs = LevelTables(problems, level, cfg, tolerance_override)
+        self.n_pairs_total = len(tabs)
+        self.pose_i = tabs.pose_i.astype(np.int32)
+        self.pose_j = tabs.pose_j.astype(np.int32)
         # chunk size from the whole level (shard-independent)
         stride = int(cfg.pixel_stride)
-        px_of_node: dict = {}  # strided source-grid size per source node
-
-        def grid_px(node):
-            v = px_of_node.get(id(node))
-            if v is None:
-                intr = node.pyramid.levels[level].intrinsics
-                v = px_of_node[id(node)] = (math.ceil(intr.width / stride)
-                                            * math.ceil(intr.height / stride))
-            return v
-
-        pair_px = np.array([grid_px(c[2]) for c in ctxs], dtype=np.int64)
+        node_px = [np.fromiter((math.ceil(n.pyramid.levels[level].intrinsics.width / stride)
+                                * math.ceil(n.pyramid.levels[level].intrinsics.height / stride)
+                                for n in pr.graph.nodes), dtype=np.int64,
+                               count=len(pr.graph.nodes)) for pr in problems]
+        pair_px = np.zeros(len(tabs), dtype=np.int64)
+        for p, px in enumerate(node_px):
+            sel = tabs.prob == p
+            pair_px[sel] = px[tabs.pose_i[sel]]
         total_px = int(pair_px.sum())
         self.total_pixels = total_px
         self.chunk_pixels = chunk_pixels_for(total_px)
-        lo, hi = (0, len(ctxs)) if pair_range is None else pair_range
+        lo, hi = (0, len(tabs)) if pair_range is None else pair_range
         self.pair_lo, self.pair_hi = lo, hi
-        mine = ctxs[lo:hi]
-        self.n_pairs = len(mine)
-        # frame / extrinsics tables for this shard
-        store.prefetch([node.pyramid.levels[level] for c in mine for node in (c[2], c[3])])
-        frames, frame_slot, node_slot, ext_rows, ext_slot, ext_of = [], {}, {}, [], {}, {}
-
-        def slot_of(node):  # frame table slot of a node's level image
-            s_ = node_slot.get(id(node))
+        m_prob, m_i, m_j = tabs.prob[lo:hi], tabs.pose_i[lo:hi], tabs.pose_j[lo:hi]
+        self.n_pairs = hi - lo
+        # frame / extrinsics tables for this shard: one slot per node image
+        # used, in first-use order (source then destination, pair by pair)
+        order = np.stack([m_i, m_j], axis=1).reshape(-1) if self.n_pairs else np.zeros(0, np.int64)
+        order_prob = np.repeat(m_prob, 2)
+        key = order_prob * (1 << 32) + order
+        _, first = np.unique(key, return_index=True)
+        used = key[np.sort(first)]  # unique nodes, first-use order
+        used_nodes = [problems[int(k >> 32)].graph.nodes[int(k & 0xFFFFFFFF)] for k in used]
+        store.prefetch([n.pyramid.levels[level] for n in used_nodes])
+        frames, frame_slot, ext_rows, ext_slot = [], {}, [], {}
+        node_slot = np.empty(len(used), dtype=np.int64)
+        for u, node in enumerate(used_nodes):
+            cue = node.pyramid.levels[level]
+            s_ = frame_slot.get(id(cue))
             if s_ is None:
-                cue = node.pyramid.levels[level]
-                s_ = frame_slot.get(id(cue))
-                if s_ is None:
-                    tex, mask, ray, cam = store.frame(cue)
-                    s_ = frame_slot[id(cue)] = len(frames)
-                    frames.append(N.Frame(tex.data_ptr(), mask.data_ptr(), ray.data_ptr(), cam))
-                node_slot[id(node)] = s_
-            return s_
+                tex, mask, ray, cam = store.frame(cue)
+                s_ = frame_slot[id(cue)] = len(frames)
+                frames.append(N.Frame(tex.data_ptr(), mask.data_ptr(), ray.data_ptr(), cam))
+            node_slot[u] = s_
+        ext_of_sensor: dict = {}
 
-        def ext_of_pair(ext):
-            e_ = ext_of.get(id(ext))
+        def ext_index(p, sensor_id):
+            e_ = ext_of_sensor.get((p, sensor_id))
             if e_ is None:
-                off = ext.offset
+                off = problems[p].extrinsics_of(sensor_id).offset
                 ekey = (np.asarray(off.rotation, float).tobytes(),
                         np.asarray(off.translation, float).tobytes())
                 if ekey not in ext_slot:
                     ext_slot[ekey] = len(ext_rows)
                     ext_rows.append(np.concatenate([np.asarray(off.rotation, float).reshape(9),
                                                     np.asarray(off.translation, float).reshape(3)]))
-                e_ = ext_of[id(ext)] = ext_slot[ekey]
+                e_ = ext_of_sensor[(p, sensor_id)] = ext_slot[ekey]
             return e_
 
+        node_ext = np.array([ext_index(int(k >> 32), n.sensor_id)
+                             for k, n in zip(used, used_nodes)], dtype=np.int64)
         idx = np.zeros((max(1, self.n_pairs), 5), dtype=np.int32)  # pose_i, pose_j, src, dst, ext
         tols = np.zeros(max(1, self.n_pairs))
-        if mine:
-            idx[: self.n_pairs] = np.array(
-                [(c[0], c[1], slot_of(c[2]), slot_of(c[3]), ext_of_pair(c[4])) for c in mine],
-                dtype=np.int32)
-            tols[: self.n_pairs] = [c[5] for c in mine]
+        if self.n_pairs:
+            pos_i = np.searchsorted(used, m_prob * (1 << 32) + m_i, sorter=np.argsort(used))
+            pos_j = np.searchsorted(used, m_prob * (1 << 32) + m_j, sorter=np.argsort(used))
+            srt = np.argsort(used)
+            ui, uj = srt[pos_i], srt[pos_j]
+            idx[: self.n_pairs] = np.stack([m_i, m_j, node_slot[ui], node_slot[uj], node_ext[ui]],
+                                           axis=1).astype(np.int32)
+            tols[: self.n_pairs] = tabs.tol[lo:hi]
         # the pba_pair / pba_camera tables built in one go (32 B / 64 B records)
         pair_rec = np.zeros(max(1, self.n_pairs), dtype=[("i", "<i4", 6), ("tol", "<f8")])
         pair_rec["i"][:, :5] = idx
