@@ -305,31 +305,12 @@ class FrameStore:
         return sum(v[1].numel() + v[2].numel() for v in self._frames.values())
 
 
-def level_contexts(problems, level, cfg):
-    """Reference contexts of _LevelProblem.__init__ (solver.py:400-414) as
-    (pose_i, pose_j, node_i, node_j, extrinsics, occlusion_tol) tuples."""
-    out = []
-    for problem in problems:
-        nodes = problem.graph.nodes
-        index_of = {n.id: k for k, n in enumerate(nodes)}
-        ext_of = {}
-        for edge in problem.graph.edges:
-            ni, nj = nodes[index_of[edge.i]], nodes[index_of[edge.j]]
-            if ni.sensor_id != nj.sensor_id:
-                from .bundle import FusionConfigError
-                raise FusionConfigError("edges must connect frames of one sensor")
-            ext = ext_of.get(ni.sensor_id)
-            if ext is None:
-                ext = ext_of[ni.sensor_id] = problem.extrinsics_of(ni.sensor_id)
-            tol = cfg.occlusion_depth_tolerance / ni.pyramid.scales[level]
-            out.append((index_of[edge.i], index_of[edge.j], ni, nj, ext, tol))
-    return out
-
-
 class LevelTables:
-    """level_contexts as arrays, in the same pair order: per pair the problem,
-    the two node (pose) indices and the occlusion tolerance; per problem its
-    nodes.  Built with one pass over the edges instead of a tuple per pair."""
+    """The contexts of _LevelProblem.__init__ (solver.py:400-414) as arrays,
+    in its pair order (problem by problem, edge order): per pair the problem,
+    the two node (pose) indices and the occlusion tolerance (solver.py:410);
+    cross-sensor edges raise FusionConfigError (solver.py:406-407).  One pass
+    over the edges instead of a tuple per pair."""
 
     def __init__(self, problems, level, cfg, tolerance_override=None):
         self.problems = problems

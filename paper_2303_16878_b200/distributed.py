@@ -166,13 +166,17 @@ class ShardedLevel:
 
 
 def pair_pixels(problems, level, cfg) -> list:
-    from .device import level_contexts
+    """Strided source-grid pixels of every pair of the level, in pair order."""
+    from .device import LevelTables
 
     s = int(cfg.pixel_stride)
-    out = []
-    for c in level_contexts(problems, level, cfg):
-        intr = c[2].pyramid.levels[level].intrinsics
-        out.append(-(-intr.width // s) * -(-intr.height // s))
+    tabs = LevelTables(problems, level, cfg)
+    out = [0] * len(tabs)
+    for p, problem in enumerate(problems):
+        px = [-(-n.pyramid.levels[level].intrinsics.width // s)
+              * -(-n.pyramid.levels[level].intrinsics.height // s) for n in problem.graph.nodes]
+        for k in np.nonzero(tabs.prob == p)[0]:
+            out[k] = px[tabs.pose_i[k]]
     return out
 
 
