@@ -285,27 +285,29 @@ def _gpu_overlap_verdicts(nodes, candidates, crit, extrinsics, level, stride, ca
                                    trans_t.data_ptr(), cams_t.data_ptr(), len(src_np), 1e-6,
                                    counts.data_ptr(), torch.cuda.current_stream(dev).cuda_stream),
             "pba_overlap_counts")
-    counts = counts.cpu().numpy()
+    counts = counts.cpu().numpy().reshape(-1, 2)  # (a -> b, b -> a) per gated pair
     n_valid = np.diff(np.array(offsets))
-    verdicts = {}
     kw = dict(level=level, stride=stride, extrinsics=extrinsics, _cache=cache)
     margin_pts = 8
-    for k, (a, b) in enumerate(gated):
+    nv = np.stack([n_valid[ab[:, 0]], n_valid[ab[:, 1]]], axis=1).astype(np.float64)
+    with np.errstate(invalid="ignore", divide="ignore"):
+        ratio = np.where(nv > 0, counts / np.where(nv > 0, nv, 1.0), 0.0)
+    near = (nv > 0) & (np.abs(counts - crit.min_overlap_ratio * nv) <= margin_pts)
+    passes = ratio >= crit.min_overlap_ratio
+    verdicts = {}
+    for k in np.nonzero(near.any(axis=1))[0]:  # near the threshold: the exact host path
+        a, b = gated[k]
         ok = True
         for d, (i, j) in enumerate(((a, b), (b, a))):
-            nv = int(n_valid[i])
-            if nv == 0:
-                ratio = 0.0
-            else:
-                c = int(counts[2 * k + d])
-                if abs(c - crit.min_overlap_ratio * nv) <= margin_pts:  # near the threshold
-                    ratio = overlap_ratio(nodes[i], nodes[j], **kw)
-                else:
-                    ratio = float(c) / float(nv)
-            if ratio < crit.min_overlap_ratio:
+            r = overlap_ratio(nodes[i], nodes[j], **kw) if near[k, d] else float(ratio[k, d])
+            if r < crit.min_overlap_ratio:
                 ok = False
                 break
         verdicts[(a, b)] = ok
+    settled = ~near.any(axis=1)
+    ok_all = passes[:, 0] & passes[:, 1]
+    for k in np.nonzero(settled)[0]:
+        verdicts[gated[k]] = bool(ok_all[k])
     return verdicts
 
 
